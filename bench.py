@@ -1,0 +1,364 @@
+"""Benchmark of the Dr. Top-k hot path (BASELINE.json: top-k keys/s, N=2^30 u32).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--k 1024] [--log2n 30] [--no-sweep] [--no-e2e] [--no-cpu]
+
+A step is one full top-k (delegates -> theta -> concatenation -> final
+select/sort) over one synthetic vector resident in HBM.  Workload: BASELINE
+config 2 -- N = 2^30 uniform uint32 per GPU (4 GiB, larger than the 126 MB L2,
+so no flush is needed between steps), k = 1024 for the headline line, plus a
+k sweep 1..2^20 reported in ``k_sweep``.  N>1 (torchrun): every rank owns a
+2^30 shard of one 2^30*N vector (weak scaling, BASELINE config 5 at N=8) and
+the step includes the NCCL theta all-reduce and candidate all-gather.
+
+One JSON line on rank 0.  ``--impl reference`` times the CPU restatement of
+the reference path (oracle/, the reference being pure Python) on this box's
+host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "top-k keys/sec (N=2^30 u32, k=1..2^20) and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "keys/s"
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clocks / throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake",
+    }
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_sm = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_sm,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(k: int, log2n: int):
+    """Oracle port (C restatement of pipeline.dr_topk) on 1 host core, bounded sample."""
+    from oracle import oracle
+
+    oracle.build()
+    ns = 1 << min(log2n, 28)
+    v = oracle.generate_uniform(ns, seed=0)
+    alpha = oracle.auto_alpha(ns, k)
+    oracle.dr_topk(v, k, alpha, 2)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while reps < 3 or time.perf_counter() - t0 < 10.0:
+        oracle.dr_topk(v, k, alpha, 2)
+        reps += 1
+        if time.perf_counter() - t0 > 30.0:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {
+        "value": ns / dt,
+        "unit": UNIT,
+        "cores": 1,
+        "kind": "port",
+        "sample": f"2^{int(math.log2(ns))} uniform u32 keys, k={k}, alpha={alpha}, beta=2, {reps} reps "
+                  f"(C restatement of pipeline.dr_topk, oracle/dtopk_oracle.c)",
+    }
+
+
+def run_reference(args):
+    """--impl reference: the CPU restatement with all host threads, same workload."""
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    oracle.build()
+    cores = oracle.cpu_count()
+    n = 1 << args.log2n
+    v = oracle.generate_uniform(n, seed=0, threads=cores)
+    k = args.k
+    for _ in range(args.warmup):
+        oracle.dr_topk_partitioned(v, k, cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.dr_topk_partitioned(v, k, cores)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    value = n / dt
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (splitmix64 uniform, host-generated)",
+        "impl": "reference",
+        "config": {"workload": f"BASELINE config 2: N=2^{args.log2n} uint32 uniform, k={k}, auto alpha (const 3), beta=2",
+                   "n": n, "k": k},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"full workload, {args.steps} steps: oracle_dr_topk_partitioned "
+                                   f"(run_distributed analogue, distributed.py:191-251) on {cores} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2109_08219_b200 as dtopk
+    from paper_2109_08219_b200 import _native, data
+    from paper_2109_08219_b200.pipeline import DrTopK
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _native.load()
+    n = 1 << args.log2n
+    k = args.k
+    v = data.generate("uniform", n, seed=1000 + rank, device=dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    cfg = dtopk.PipelineConfig(k=k)
+    plan = DrTopK(n, cfg, _native.DTYPE_U32, torch.uint32, dev, timed=False)
+    stream = torch.cuda.current_stream(dev)
+
+    if world == 1:
+        step = lambda ev=None: plan.launch(v, stream, events=ev)  # noqa: E731
+    else:
+        def step(ev=None):
+            dtopk.sharded_topk(v, n * world, k, cfg)
+
+    # per-step stage events on the launch stream: the K1 (Delegate) duration
+    # of every timed step is measured live inside the timed region
+    import ctypes
+
+    stage_ev = [[lib.dtopk_event_create() for _ in range(5)] for _ in range(args.steps)]
+    ev_arrays = [(ctypes.c_void_p * 5)(*e) for e in stage_ev]
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = lib.dtopk_launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(ev_arrays[i] if world == 1 else None)
+        t_end.record(stream)
+        barrier()
+    launches = lib.dtopk_launch_count() - launches0
+    ms = t_start.elapsed_time(t_end) / args.steps
+    ms = max_over_ranks(ms)
+    value = n * world / (ms * 1e-3)
+
+    hdr = plan.header()
+    peak, peak_src = _measured_peak()
+    roof = None
+    if world == 1:
+        k1_ms = [lib.dtopk_event_elapsed_ms(e[0], e[1]) for e in stage_ev]
+        stage_ms = {name: statistics.mean(lib.dtopk_event_elapsed_ms(e[i], e[i + 1]) for e in stage_ev)
+                    for i, name in enumerate(dtopk.STAGES)}
+        k1 = statistics.mean(k1_ms)
+        achieved = n * 4 / (k1 * 1e-3) / 1e9
+        roof = {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "k1_delegates (Delegate stage)",
+            "algorithmic_bytes_per_launch": n * 4, "kernel_ms": k1, "peak_source": peak_src,
+            "stage_ms": stage_ms,
+            "step_frac": (n * 4 / (ms * 1e-3) / 1e9) / peak,
+        }
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (counter-based splitmix64 uniform u32, generated in HBM)",
+            "config": {
+                "workload": f"BASELINE config 2: N=2^{args.log2n} uint32 uniform per GPU, k={k}, "
+                            f"auto alpha (Eq. 11, const 3) = {plan.cfg.alpha}, beta={plan.cfg.beta}",
+                "n_per_gpu": n, "k": k, "alpha": plan.cfg.alpha, "beta": plan.cfg.beta,
+                "l2": "inputs (4 GiB/GPU) larger than the 126 MB L2; no flush",
+                "parallelism": f"shard{world}" if world > 1 else "single",
+            },
+            "roofline": roof,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "device_header": {"path": int(hdr.path), "pool_gt": int(hdr.pool_gt),
+                              "candidate_subranges": int(hdr.candidate_subranges),
+                              "elements_reread": int(hdr.elements_reread)},
+        }
+
+    # ---- k sweep (config 2), 1 GPU only
+    if world == 1 and not args.no_sweep and rank == 0:
+        sweep = []
+        for e in range(0, 21, args.sweep_stride):
+            kk = 1 << e
+            p = DrTopK(n, dtopk.PipelineConfig(k=kk), _native.DTYPE_U32, torch.uint32, dev, timed=False)
+            for _ in range(3):
+                p.launch(v, stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(5, args.steps // 4)
+            a.record(stream)
+            for _ in range(reps):
+                p.launch(v, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / reps
+            p.launch(v, stream, events=ev_arrays[0])
+            h = p.header()
+            st_ms = {name: round(lib.dtopk_event_elapsed_ms(ev_arrays[0][i], ev_arrays[0][i + 1]), 4)
+                     for i, name in enumerate(dtopk.STAGES)}
+            sweep.append({"k": kk, "alpha": p.cfg.alpha, "ms": round(t, 4), "keys_per_s": n / (t * 1e-3),
+                          "frac_of_peak": (n * 4 / (t * 1e-3) / 1e9) / peak, "path": int(h.path),
+                          "pool_gt": int(h.pool_gt), "reread": int(h.elements_reread), "stage_ms": st_ms})
+            del p
+        out["k_sweep"] = sweep
+        out["k_sweep_min_frac"] = min(s["frac_of_peak"] for s in sweep)
+
+    # ---- e2e through the public API with host buffers
+    if not args.no_e2e:
+        host = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+        host.copy_(v.cpu() if world == 1 else v.cpu())
+        barrier()
+        reps = max(3, min(args.steps, 5))
+        dtopk.dr_topk(host, cfg)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            if world == 1:
+                r = dtopk.dr_topk(host, cfg)
+            else:
+                dv = host.to(dev, non_blocking=True)
+                r = dtopk.sharded_topk(dv, n * world, k, cfg)
+                r.values.cpu()
+                r.indices.cpu()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / reps)
+        if rank == 0:
+            out["e2e"] = {"value": n * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 4,
+                          "d2h_bytes_per_step": k * (4 + 8) + 104, "ms_per_step": e2e_s * 1e3,
+                          "path": "paper_2109_08219_b200.dr_topk(pinned host tensor) -> numpy-style host results"}
+        del host
+
+    for e in stage_ev:
+        for h in e:
+            lib.dtopk_event_destroy(h)
+    if rank == 0 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(k, args.log2n)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--k", type=int, default=1024)
+    ap.add_argument("--log2n", type=int, default=30)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--sweep-stride", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

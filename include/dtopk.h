@@ -1,0 +1,161 @@
+/*
+ * dtopk.h -- C ABI of the B200-native Dr. Top-k hot path (libdtopk.so).
+ *
+ * Plain pointers and sizes only: no torch / Python types cross this boundary.
+ * Every entry point is stream-ordered on the caller's cudaStream_t, never
+ * synchronises the stream, and never allocates device memory: the caller
+ * passes a workspace of at least dtopk_workspace_bytes(...) bytes.
+ *
+ * Reference interfaces replaced (paths under the reference package
+ * pkg/src/dtopk/):
+ *   dtopk_select            <- pipeline.dr_topk                (pipeline.py:172-220)
+ *                              incl. the direct fallback       (pipeline.py:184-191)
+ *   dtopk_select_begin/     <- the same call split at the threshold, so a
+ *   dtopk_select_finish        multi-GPU caller can all-reduce theta between
+ *                              the first top-k and the concatenation
+ *                              (distributed.py:162 runs dr_topk per partition;
+ *                              the exchange is the one PAPER.md:738-742 disabled)
+ *   dtopk_extract_delegates <- delegate.extract_delegates      (delegate.py:142-155)
+ *                              and extract_delegates_blocked   (delegate.py:158-191)
+ *   dtopk_kth_largest       <- kernels.radix_topk threshold    (kernels.py:109-165),
+ *                              used by pipeline.first_topk     (pipeline.py:87-116)
+ *   dtopk_workspace_bytes   <- (no reference counterpart: numpy allocates implicitly)
+ *
+ * Key spaces: every kernel works on 32-bit *keys* where "larger key" means
+ * "selected first".  uint32 largest is the identity map, uint32 smallest is
+ * ~x, float32 uses the order-preserving bijection
+ *     u = (b >> 31) ? ~b : b | 0x80000000      (then ~u for smallest).
+ * Results are returned in the input dtype; indices are int64 positions into
+ * the input (plus the caller's index_offset for sharded inputs).
+ */
+#ifndef DTOPK_H_
+#define DTOPK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DTOPK_OK = 0,
+  DTOPK_EMPTY_INPUT = 1,        /* core.EmptyInput   (core.py:37-38)  */
+  DTOPK_INVALID_K = 2,          /* core.InvalidK     (core.py:33-34)  */
+  DTOPK_INVALID_BETA = 3,       /* core.InvalidBeta  (core.py:41-42)  */
+  DTOPK_INVALID_ARG = 4,        /* ValueError (bad alpha / dtype / alignment) */
+  DTOPK_WORKSPACE_TOO_SMALL = 5,
+  DTOPK_CUDA_ERROR = 6,
+  DTOPK_UNSUPPORTED = 7         /* beta > 32 on the delegate path */
+} dtopk_status;
+
+typedef enum { DTOPK_U32 = 0, DTOPK_F32 = 1 } dtopk_dtype;
+
+/* flags for dtopk_select / dtopk_select_begin */
+#define DTOPK_FLAG_EXACT_STATS 1u  /* re-read tie-only subranges so concatenated_len is exact */
+
+/* Device-resident result header, written by the kernels of one call.
+ * Field names follow core.WorkloadStats (core.py:59-93) where they overlap. */
+typedef struct {
+  uint64_t k_out;                 /* number of (value, index) pairs written (== k unless a
+                                     larger external theta was applied)              */
+  uint64_t candidate_subranges;   /* subranges with max delegate >= theta              */
+  uint64_t fully_qualified;       /* beta-th delegate >= theta     (pipeline.py:104-108) */
+  uint64_t partially_qualified;   /* max >= theta > beta-th delegate (pipeline.py:109,205) */
+  uint64_t concatenated_len;      /* |C|: elements >= theta of fully qualified subranges */
+  uint64_t concat_skipped_fq;     /* FQ subranges not re-read (ties already satisfied);
+                                     concatenated_len is exact iff this is 0          */
+  uint64_t elements_reread;       /* input elements re-read by the concatenation stage */
+  uint64_t pool_gt;               /* G: elements strictly above theta                  */
+  uint64_t pool_eq;               /* ties at theta collected (capped by k)             */
+  uint64_t delegate_bucket;       /* delegates in theta's top-11-bit bucket            */
+  uint32_t theta_local;           /* kth(D) in key space                               */
+  uint32_t theta;                 /* threshold actually used (max with external theta) */
+  uint32_t kth_key;               /* exact k-th key of the answer                      */
+  uint32_t path;                  /* 1 = radix select over the pool, 2 = merge, 3 = direct */
+  int64_t theta_slot;             /* theta_local as int64, target of an all-reduce(MAX) */
+} dtopk_result;
+
+/* Bytes of workspace needed by dtopk_select for these parameters. */
+size_t dtopk_workspace_bytes(uint64_t n, uint64_t k, int alpha, int beta, int direct);
+
+/* Byte offset of the dtopk_result header inside the workspace. */
+size_t dtopk_result_offset(void);
+
+/*
+ * Full top-k: pipeline.dr_topk (pipeline.py:172-220), delegate path or, with
+ * direct != 0, the direct radix top-k fallback (pipeline.py:184-191).
+ *   keys          device pointer, 16-byte aligned, n elements of `dtype`
+ *   k             1 <= k <= n
+ *   largest       1 = top-k largest, 0 = smallest
+ *   alpha, beta   resolved by validate_config (core.py:145-174); ignored if direct
+ *   out_values    device, k elements of `dtype`, ordered best first
+ *   out_indices   device, k int64 positions (+ index_offset); ties broken by
+ *                 lowest index, final order (key desc, index asc)
+ *   index_offset  added to every output index (global offset of a shard)
+ *   ws, ws_bytes  workspace; the dtopk_result header lives at
+ *                 ws + dtopk_result_offset()
+ *   stage_events  null, or 5 events from dtopk_event_create() recorded at the
+ *                 stage boundaries start | Delegate | FirstK | Concat | SecondK
+ *                 (core.STAGES, core.py:22-26; pipeline.py:187-219 timers)
+ */
+dtopk_status dtopk_select(const void* keys, uint64_t n, int dtype, uint64_t k, int largest,
+                          int alpha, int beta, int direct, uint32_t flags,
+                          void* out_values, int64_t* out_indices, int64_t index_offset,
+                          void* ws, size_t ws_bytes, void* stream, void* const* stage_events);
+
+/* First half of dtopk_select (delegate path only): delegates, theta = kth(D).
+ * Afterwards dtopk_result.theta_slot holds theta (int64) in device memory. */
+dtopk_status dtopk_select_begin(const void* keys, uint64_t n, int dtype, uint64_t k, int largest,
+                                int alpha, int beta, uint32_t flags,
+                                void* ws, size_t ws_bytes, void* stream, void* const* stage_events);
+
+/* Second half: uses theta = max(theta_local, *theta_override) when
+ * theta_override (device int64*) is non-null.  May emit k_out < k pairs when an
+ * external theta is larger than this shard's k-th key. */
+dtopk_status dtopk_select_finish(const void* keys, uint64_t n, int dtype, uint64_t k, int largest,
+                                 int alpha, int beta, uint32_t flags,
+                                 const int64_t* theta_override,
+                                 void* out_values, int64_t* out_indices, int64_t index_offset,
+                                 void* ws, size_t ws_bytes, void* stream, void* const* stage_events);
+
+/* delegate.extract_delegates: out_delegates[beta*ceil(n/2^alpha)] in key space,
+ * subrange-major, non-increasing inside a subrange, zero-padded tail
+ * (delegate.py:132-139).  Needs dtopk_workspace_bytes(n, 1, alpha, beta, 0). */
+dtopk_status dtopk_extract_delegates(const void* keys, uint64_t n, int dtype, int largest,
+                                     int alpha, int beta, uint32_t* out_delegates,
+                                     void* ws, size_t ws_bytes, void* stream);
+
+/* Exact k-th largest key of a uint32 key array (radix select, 11/11/10-bit
+ * digits); writes it to *out_kth (device).  Needs
+ * dtopk_workspace_bytes(n, k, 0, 1, 1). */
+dtopk_status dtopk_kth_largest(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t* out_kth,
+                               void* ws, size_t ws_bytes, void* stream);
+
+/* CUDA timing events for stage_events (cudaEventCreate / Destroy /
+ * ElapsedTime; elapsed synchronises on `end`). */
+void* dtopk_event_create(void);
+void dtopk_event_destroy(void* ev);
+float dtopk_event_elapsed_ms(void* start, void* end);
+
+/* Deterministic synthetic input (value i depends only on (seed, i)):
+ * dist 0 uniform u32, 1 ascending (i + param), 2 constant param,
+ * 3 uniform in [0, param), 4 N(0,1) float32, 5 Pareto(param/1000) float32,
+ * 6 rint(N(1e8, 10)) u32 (the reference ND set, data.py:65-75),
+ * 7 descending (param - i).  Test/bench data only, not the hot path. */
+dtopk_status dtopk_generate(void* out, uint64_t n, int dist, uint64_t seed, uint64_t param, void* stream);
+
+/* Number of SMs the library sizes its persistent grids for (current device). */
+int dtopk_num_sms(void);
+
+/* Total kernels this library has launched in the process (for benchmarks). */
+unsigned long long dtopk_launch_count(void);
+
+/* Library version string. */
+const char* dtopk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DTOPK_H_ */

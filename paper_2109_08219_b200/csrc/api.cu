@@ -1,0 +1,486 @@
+// api.cu -- workspace layout, stream-ordered launch sequence and the C ABI
+// (include/dtopk.h) of the B200 Dr. Top-k pipeline.
+//
+// Stage map (paper Eq. 1; pipeline.py:172-220):
+//   Delegate : K1 k1_delegates (+ k1_merge when 2^alpha > 8192)
+//   FirstK   : K2 k2_scan_delegates, k2_pass3          -> theta = kth(D)
+//   Concat   : K4 scan_emit<CAND>                       -> P_gt, first ties
+//   SecondK  : sel_pass1..3 + scan_emit<FLAT> (pool > k) or merge_copy,
+//              then sort_{hist,scan,scatter} x passes, writeout
+// No host synchronisation happens inside a call; data-dependent sizes live in
+// the device control block and every kernel sizes its own loop from it.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "delegate.cuh"
+#include "generate.cuh"
+#include "scan.cuh"
+#include "select.cuh"
+
+using namespace dtopk;
+
+namespace {
+
+std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library
+inline void counted(int n = 1) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+constexpr size_t ALIGN = 256;
+inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+struct Layout {
+  size_t ctrl, lb_k3, lb_k4g, lb_k4e, lb_emg, lb_eme, zero_bytes;
+  size_t D, partial, selbuf, bitmap, cand_sid, cand_d1, cand_dl, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
+      total;
+  u64 S, nch, cap_gt, m_emit, k2_tiles, k3_tiles, k4_tiles, em_tiles, sort_tiles, D_len, words;
+};
+
+Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](u64 bytes) {
+    const size_t o = off;
+    off = align_up(off + (size_t)bytes);
+    return o;
+  };
+  const u64 W = direct ? 1ull : (1ull << alpha);
+  L.nch = (n + K1_CHUNK - 1) / K1_CHUNK;
+  L.S = direct ? 0 : (n + W - 1) / W;
+  L.D_len = direct ? 0 : (u64)beta * L.S;
+  // Elements strictly above theta live in the < k subranges whose max delegate
+  // exceeds theta = kth(D), so the pool never holds more than (k-1) * 2^alpha.
+  L.cap_gt = direct ? 0 : std::min<u64>(n, std::max<u64>(1, k - 1) * W);
+  L.m_emit = direct ? n : L.cap_gt;
+  L.k2_tiles = (L.S + K2_TILE - 1) / K2_TILE;
+  L.words = (L.S + 31) / 32;
+  L.k3_tiles = (L.words + K3_TILE - 1) / K3_TILE;
+  L.k4_tiles = direct ? 0 : (L.S * W + SC_TILE - 1) / SC_TILE;
+  L.em_tiles = (L.m_emit + SC_TILE - 1) / SC_TILE;
+  L.sort_tiles = (k + ST_TILE - 1) / ST_TILE;
+  L.ctrl = take(sizeof(Ctrl));
+  L.lb_k3 = take(L.k3_tiles * 8);
+  L.lb_k4g = take(L.k4_tiles * 8);
+  L.lb_k4e = take(L.k4_tiles * 8);
+  L.lb_emg = take(L.em_tiles * 8);
+  L.lb_eme = take(L.em_tiles * 8);
+  L.zero_bytes = off;
+  L.D = take(L.D_len * 4);
+  L.partial = take((!direct && alpha > K1_LOG_CHUNK) ? (u64)beta * L.nch * 4 : 0);
+  L.selbuf = take(std::max<u64>(L.D_len, L.m_emit) * 4);
+  L.bitmap = take(L.words * 4);
+  L.cand_sid = take(L.S * 4);
+  L.cand_d1 = take(L.S * 4);
+  L.cand_dl = take(L.S * 4);
+  L.gt_keys = take(L.cap_gt * 4);
+  L.gt_idx = take(L.cap_gt * 8);
+  L.ties = take(direct ? 0 : k * 8);
+  L.sak = take(k * 4);
+  L.sai = take(k * 8);
+  L.sbk = take(k * 4);
+  L.sbi = take(k * 8);
+  L.counts = take(L.sort_tiles * 256 * 4);
+  L.total = off;
+  return L;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+inline int grid_for(u64 work_items, int cap) {
+  if (work_items == 0) return 1;
+  return (int)std::max<u64>(1, std::min<u64>(work_items, (u64)cap));
+}
+
+inline dtopk_status cuda_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "dtopk: CUDA error %s\n", cudaGetErrorString(e));
+    return DTOPK_CUDA_ERROR;
+  }
+  return DTOPK_OK;
+}
+
+inline void rec(void* const* ev, int i, cudaStream_t s) {
+  if (ev && ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
+}
+
+inline int key_mode(int dtype, int largest) { return (dtype == DTOPK_F32 ? 2 : 0) + (largest ? 0 : 1); }
+
+// ---------------------------------------------------------------------------
+template <int MODE, int B>
+void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k1_delegates<MODE, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1_SMEM);
+    attr = true;
+  }
+  k1_delegates<MODE, B><<<grid_for(nch, nsm), K1_THREADS, K1_SMEM, s>>>(a);
+  counted();
+  if (a.alpha > K1_LOG_CHUNK) {
+    k1_merge<B><<<grid_for((a.S + 255) / 256, nsm * 4), 256, 0, s>>>(a.partial, nch, a.alpha, a.S, a.D, a.hist1);
+    counted();
+  }
+}
+
+template <int MODE>
+void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* ws, const Layout& L, cudaStream_t s,
+                     int nsm) {
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  K1Args a{keys, n, alpha, L.S, D, reinterpret_cast<u32*>(ws + L.partial), ctrl->selD.hist1,
+           alpha <= K1_LOG_CHUNK ? 1 : 0};
+  switch (beta) {
+    case 1: launch_k1<MODE, 1>(a, s, nsm, L.nch); break;
+    case 2: launch_k1<MODE, 2>(a, s, nsm, L.nch); break;
+    case 3: launch_k1<MODE, 3>(a, s, nsm, L.nch); break;
+    case 4: launch_k1<MODE, 4>(a, s, nsm, L.nch); break;
+    case 5: launch_k1<MODE, 5>(a, s, nsm, L.nch); break;
+    case 6: launch_k1<MODE, 6>(a, s, nsm, L.nch); break;
+    case 7: launch_k1<MODE, 7>(a, s, nsm, L.nch); break;
+    case 8: launch_k1<MODE, 8>(a, s, nsm, L.nch); break;
+    default:
+      k1_generic<MODE><<<grid_for((L.S + 7) / 8, nsm * 8), 256, 0, s>>>(keys, n, alpha, beta, L.S, D, ctrl->selD.hist1);
+      counted();
+  }
+}
+
+template <int MODE>
+void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, const Layout& L, cudaStream_t s, int nsm,
+               void* const* ev) {
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
+  rec(ev, 0, s);
+  u32* D = reinterpret_cast<u32*>(ws + L.D);
+  stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm);
+  rec(ev, 1, s);
+  K2Args k2{D, L.S, beta, k, ctrl, reinterpret_cast<u32*>(ws + L.selbuf), reinterpret_cast<u32*>(ws + L.bitmap)};
+  k2_scan_delegates<<<grid_for(L.k2_tiles, nsm * 4), 256, 0, s>>>(k2);
+  counted();
+  k2_pass3<<<grid_for((L.D_len + 4095) / 4096, nsm * 2), 256, 0, s>>>(ctrl, k2.selbuf);
+  counted();
+  rec(ev, 2, s);
+}
+
+void run_sort(Ctrl* ctrl, char* ws, const Layout& L, cudaStream_t s, int nsm) {
+  u32* ka = reinterpret_cast<u32*>(ws + L.sak);
+  u64* ia = reinterpret_cast<u64*>(ws + L.sai);
+  u32* kb = reinterpret_cast<u32*>(ws + L.sbk);
+  u64* ib = reinterpret_cast<u64*>(ws + L.sbi);
+  u32* counts = reinterpret_cast<u32*>(ws + L.counts);
+  const int g = grid_for(L.sort_tiles, nsm * 4);
+  for (int p = 0; p < 4; p++) {
+    const bool even = (p & 1) == 0;
+    sort_hist<<<g, 256, 0, s>>>(ctrl, even ? ka : kb, p, counts);
+    counted();
+    sort_scan<<<1, 256, 0, s>>>(ctrl, p, counts);
+    counted();
+    sort_scatter<<<g, 256, 0, s>>>(ctrl, p, even ? ka : kb, even ? ia : ib, even ? kb : ka, even ? ib : ia, counts);
+    counted();
+  }
+}
+
+template <int MODE>
+void run_tail(u64 k, void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L,
+              cudaStream_t s, int nsm) {
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sort_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SORT * 8);
+    attr = true;
+  }
+  sort_small<MODE><<<1, 1024, SMALL_SORT * 8, s>>>(ctrl, reinterpret_cast<u32*>(ws + L.sak), reinterpret_cast<u64*>(ws + L.sai),
+                                      reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices),
+                                      (long long)offset);
+  counted();
+  if (k > (u64)SMALL_SORT) run_sort(ctrl, ws, L, s, nsm);
+  writeout<MODE><<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
+      ctrl, reinterpret_cast<u32*>(ws + L.sak), reinterpret_cast<u64*>(ws + L.sai), reinterpret_cast<u32*>(ws + L.sbk),
+      reinterpret_cast<u64*>(ws + L.sbi), reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices),
+      (long long)offset);
+  counted();
+}
+
+template <int MODE>
+void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, const int64_t* theta_override,
+                void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L, cudaStream_t s,
+                int nsm, void* const* ev) {
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  K3Args k3{reinterpret_cast<const u32*>(ws + L.D), L.S, beta, reinterpret_cast<const u32*>(ws + L.bitmap), ctrl,
+            theta_override, reinterpret_cast<u32*>(ws + L.cand_sid), reinterpret_cast<u32*>(ws + L.cand_d1),
+            reinterpret_cast<u32*>(ws + L.cand_dl), reinterpret_cast<u64*>(ws + L.lb_k3)};
+  k3_qualify<<<grid_for(L.k3_tiles, nsm * 4), 256, 0, s>>>(k3);
+  counted();
+  u32* gt_keys = reinterpret_cast<u32*>(ws + L.gt_keys);
+  u64* gt_idx = reinterpret_cast<u64*>(ws + L.gt_idx);
+  u64* ties = reinterpret_cast<u64*>(ws + L.ties);
+  u32* sak = reinterpret_cast<u32*>(ws + L.sak);
+  u64* sai = reinterpret_cast<u64*>(ws + L.sai);
+  u32* selbuf = reinterpret_cast<u32*>(ws + L.selbuf);
+
+  ScanArgs k4{};
+  k4.keys = keys;
+  k4.n = n;
+  k4.cand_sid = reinterpret_cast<u32*>(ws + L.cand_sid);
+  k4.cand_d1 = reinterpret_cast<u32*>(ws + L.cand_d1);
+  k4.cand_dl = reinterpret_cast<u32*>(ws + L.cand_dl);
+  k4.alpha = alpha;
+  k4.flags = flags;
+  k4.ctrl = ctrl;
+  k4.k = k;
+  k4.gt_keys = gt_keys;
+  k4.gt_idx = gt_idx;
+  k4.eq_keys = nullptr;
+  k4.eq_idx = ties;
+  k4.lb_gt = reinterpret_cast<u64*>(ws + L.lb_k4g);
+  k4.lb_eq = reinterpret_cast<u64*>(ws + L.lb_k4e);
+  scan_emit<MODE, true><<<grid_for(L.k4_tiles, nsm * 4), 256, 0, s>>>(k4);
+  counted();
+  rec(ev, 3, s);
+
+  // SecondK, pool larger than k: exact radix select over P_gt, then ordered emit.
+  const int gs = grid_for((L.cap_gt + 2047) / 2048, nsm * 4);
+  SelArgs sp{gt_keys, 0, (const ull*)&ctrl->res.pool_gt, ctrl, &ctrl->selP, selbuf, k, 1};
+  sel_pass1<KM_KEY><<<gs, 256, 0, s>>>(sp);
+  counted();
+  sel_pass2<KM_KEY><<<gs, 256, 0, s>>>(sp);
+  counted();
+  sel_pass3<<<gs, 256, 0, s>>>(sp);
+  counted();
+  ScanArgs em{};
+  em.keys = gt_keys;
+  em.idx_in = gt_idx;
+  em.m_dev = (const ull*)&ctrl->res.pool_gt;
+  em.alpha = 0;
+  em.ctrl = ctrl;
+  em.k = k;
+  em.gt_keys = sak;
+  em.gt_idx = sai;
+  em.eq_keys = sak;
+  em.eq_idx = sai;
+  em.lb_gt = reinterpret_cast<u64*>(ws + L.lb_emg);
+  em.lb_eq = reinterpret_cast<u64*>(ws + L.lb_eme);
+  em.check_path = 1;
+  scan_emit<KM_KEY, false><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
+  counted();
+  // SecondK, pool smaller than k: answer = P_gt ++ first ties at theta.
+  merge_copy<<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(ctrl, gt_keys, gt_idx, ties, sak, sai);
+  counted();
+  run_tail<MODE>(k, out_values, out_indices, offset, ws, L, s, nsm);
+  rec(ev, 4, s);
+}
+
+template <int MODE>
+void run_direct(const u32* keys, u64 n, u64 k, void* out_values, int64_t* out_indices, int64_t offset, char* ws,
+                const Layout& L, cudaStream_t s, int nsm, void* const* ev) {
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  for (int i = 0; i < 4; i++) rec(ev, i, s);  // pipeline.py:185-186: only SecondK runs
+  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
+  u32* selbuf = reinterpret_cast<u32*>(ws + L.selbuf);
+  const int gs = grid_for((n + 2047) / 2048, nsm * 4);
+  SelArgs sd{keys, n, nullptr, ctrl, &ctrl->selP, selbuf, k, 0};
+  sel_pass1<MODE><<<gs, 256, 0, s>>>(sd);
+  counted();
+  sel_pass2<MODE><<<gs, 256, 0, s>>>(sd);
+  counted();
+  sel_pass3<<<gs, 256, 0, s>>>(sd);
+  counted();
+  ScanArgs em{};
+  em.keys = keys;
+  em.m_host = n;
+  em.ctrl = ctrl;
+  em.k = k;
+  em.gt_keys = reinterpret_cast<u32*>(ws + L.sak);
+  em.gt_idx = reinterpret_cast<u64*>(ws + L.sai);
+  em.eq_keys = em.gt_keys;
+  em.eq_idx = em.gt_idx;
+  em.lb_gt = reinterpret_cast<u64*>(ws + L.lb_emg);
+  em.lb_eq = reinterpret_cast<u64*>(ws + L.lb_eme);
+  em.direct = 1;
+  scan_emit<MODE, false><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
+  counted();
+  run_tail<MODE>(k, out_values, out_indices, offset, ws, L, s, nsm);
+  rec(ev, 4, s);
+}
+
+dtopk_status check_common(const void* keys, u64 n, int dtype, u64 k) {
+  if (n == 0) return DTOPK_EMPTY_INPUT;
+  if (k < 1 || k > n || k > 0xffffffffull) return DTOPK_INVALID_K;
+  if (dtype != DTOPK_U32 && dtype != DTOPK_F32) return DTOPK_INVALID_ARG;
+  if (keys == nullptr || (reinterpret_cast<uintptr_t>(keys) & 15u) != 0) return DTOPK_INVALID_ARG;
+  return DTOPK_OK;
+}
+
+dtopk_status check_delegate(u64 n, int alpha, int beta) {
+  if (alpha < 1 || alpha > 40 || (1ull << alpha) > n) return DTOPK_INVALID_ARG;
+  if (beta < 1 || (u64)beta >= (1ull << alpha)) return DTOPK_INVALID_BETA;
+  if (beta > 32) return DTOPK_UNSUPPORTED;
+  if (((n + (1ull << alpha) - 1) >> alpha) > 0xffffffffull) return DTOPK_INVALID_ARG;
+  return DTOPK_OK;
+}
+
+#define DISPATCH_MODE(mode, FN, ...)  \
+  switch (mode) {                     \
+    case 0: FN<0>(__VA_ARGS__); break; \
+    case 1: FN<1>(__VA_ARGS__); break; \
+    case 2: FN<2>(__VA_ARGS__); break; \
+    default: FN<3>(__VA_ARGS__); break; \
+  }
+
+}  // namespace
+
+extern "C" {
+
+size_t dtopk_workspace_bytes(uint64_t n, uint64_t k, int alpha, int beta, int direct) {
+  if (k < 1) k = 1;
+  return make_layout(n, k, alpha, beta, direct).total;
+}
+
+size_t dtopk_result_offset(void) { return 0; }
+
+int dtopk_num_sms(void) { return num_sms(); }
+
+dtopk_status dtopk_generate(void* out, uint64_t n, int dist, uint64_t seed, uint64_t param, void* stream) {
+  if (out == nullptr) return DTOPK_INVALID_ARG;
+  if (n == 0) return DTOPK_OK;
+  gen_kernel<<<grid_for((n + 255) / 256, num_sms() * 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<u32*>(out), n, dist, seed, param);
+  counted();
+  return cuda_status();
+}
+
+void* dtopk_event_create(void) {
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return reinterpret_cast<void*>(e);
+}
+
+void dtopk_event_destroy(void* ev) {
+  if (ev) cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev));
+}
+
+float dtopk_event_elapsed_ms(void* start, void* end) {
+  float ms = -1.0f;
+  if (!start || !end) return ms;
+  if (cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(end)) != cudaSuccess) return ms;
+  if (cudaEventElapsedTime(&ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(end)) !=
+      cudaSuccess)
+    return -1.0f;
+  return ms;
+}
+
+unsigned long long dtopk_launch_count(void) { return g_launches.load(); }
+
+const char* dtopk_version(void) { return "dtopk-b200 0.1.0 (sm_100a)"; }
+
+dtopk_status dtopk_select_begin(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha, int beta,
+                                uint32_t flags, void* ws, size_t ws_bytes, void* stream, void* const* stage_events) {
+  (void)flags;
+  dtopk_status st = check_common(keys, n, dtype, k);
+  if (st != DTOPK_OK) return st;
+  if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
+  if ((u64)beta * ((n + (1ull << alpha) - 1) >> alpha) < k) return DTOPK_INVALID_K;
+  const Layout L = make_layout(n, k, alpha, beta, 0);
+  if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nsm = num_sms();
+  const u32* kp = reinterpret_cast<const u32*>(keys);
+  char* w = reinterpret_cast<char*>(ws);
+  DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, stage_events);
+  return cuda_status();
+}
+
+dtopk_status dtopk_select_finish(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha, int beta,
+                                 uint32_t flags, const int64_t* theta_override, void* out_values,
+                                 int64_t* out_indices, int64_t index_offset, void* ws, size_t ws_bytes,
+                                 void* stream, void* const* stage_events) {
+  dtopk_status st = check_common(keys, n, dtype, k);
+  if (st != DTOPK_OK) return st;
+  if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
+  if (out_values == nullptr || out_indices == nullptr) return DTOPK_INVALID_ARG;
+  const Layout L = make_layout(n, k, alpha, beta, 0);
+  if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nsm = num_sms();
+  const u32* kp = reinterpret_cast<const u32*>(keys);
+  char* w = reinterpret_cast<char*>(ws);
+  DISPATCH_MODE(key_mode(dtype, largest), run_finish, kp, n, k, alpha, beta, flags, theta_override, out_values,
+                out_indices,
+                index_offset, w, L, s, nsm, stage_events);
+  return cuda_status();
+}
+
+dtopk_status dtopk_select(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha, int beta,
+                          int direct, uint32_t flags, void* out_values, int64_t* out_indices, int64_t index_offset,
+                          void* ws, size_t ws_bytes, void* stream, void* const* stage_events) {
+  dtopk_status st = check_common(keys, n, dtype, k);
+  if (st != DTOPK_OK) return st;
+  if (out_values == nullptr || out_indices == nullptr) return DTOPK_INVALID_ARG;
+  if (direct) {
+    const Layout L = make_layout(n, k, 0, 1, 1);
+    if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int nsm = num_sms();
+    const u32* kp = reinterpret_cast<const u32*>(keys);
+    char* w = reinterpret_cast<char*>(ws);
+    DISPATCH_MODE(key_mode(dtype, largest), run_direct, kp, n, k, out_values, out_indices, index_offset, w, L, s, nsm,
+                  stage_events);
+    return cuda_status();
+  }
+  st = dtopk_select_begin(keys, n, dtype, k, largest, alpha, beta, flags, ws, ws_bytes, stream, stage_events);
+  if (st != DTOPK_OK) return st;
+  return dtopk_select_finish(keys, n, dtype, k, largest, alpha, beta, flags, nullptr, out_values, out_indices,
+                             index_offset, ws, ws_bytes, stream, stage_events);
+}
+
+dtopk_status dtopk_extract_delegates(const void* keys, uint64_t n, int dtype, int largest, int alpha, int beta,
+                                     uint32_t* out_delegates, void* ws, size_t ws_bytes, void* stream) {
+  dtopk_status st = check_common(keys, n, dtype, 1);
+  if (st != DTOPK_OK) return st;
+  if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
+  if (out_delegates == nullptr) return DTOPK_INVALID_ARG;
+  const Layout L = make_layout(n, 1, alpha, beta, 0);
+  if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = reinterpret_cast<char*>(ws);
+  cudaMemsetAsync(w, 0, L.zero_bytes, s);
+  const u32* kp = reinterpret_cast<const u32*>(keys);
+  DISPATCH_MODE(key_mode(dtype, largest), stage_delegates, kp, n, alpha, beta, out_delegates, w, L, s, num_sms());
+  return cuda_status();
+}
+
+dtopk_status dtopk_kth_largest(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t* out_kth, void* ws,
+                               size_t ws_bytes, void* stream) {
+  dtopk_status st = check_common(keys, n, DTOPK_U32, k);
+  if (st != DTOPK_OK) return st;
+  if (out_kth == nullptr) return DTOPK_INVALID_ARG;
+  const Layout L = make_layout(n, k, 0, 1, 1);
+  if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = reinterpret_cast<char*>(ws);
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(w + L.ctrl);
+  cudaMemsetAsync(w, 0, L.zero_bytes, s);
+  const int nsm = num_sms();
+  const int gs = grid_for((n + 2047) / 2048, nsm * 4);
+  SelArgs sd{keys, n, nullptr, ctrl, &ctrl->selP, reinterpret_cast<u32*>(w + L.selbuf), k, 0};
+  sel_pass1<KM_KEY><<<gs, 256, 0, s>>>(sd);
+  counted();
+  sel_pass2<KM_KEY><<<gs, 256, 0, s>>>(sd);
+  counted();
+  sel_pass3<<<gs, 256, 0, s>>>(sd);
+  counted();
+  sel_finalize<<<1, 256, 0, s>>>(&ctrl->selP, out_kth);
+  counted();
+  return cuda_status();
+}
+
+}  // extern "C"

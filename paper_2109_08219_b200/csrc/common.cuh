@@ -1,0 +1,314 @@
+// common.cuh -- shared device helpers for the Dr. Top-k sm_100a kernels.
+//
+// Key spaces, PTX wrappers (mbarrier, 1-D TMA bulk copy, acquire/release),
+// block scans, the radix-select digit finder, decoupled look-back, and the
+// device-resident control block that carries state between the kernels of
+// one dtopk_select call (so the host never synchronises mid-pipeline).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dtopk.h"
+
+namespace dtopk {
+
+using u32 = uint32_t;
+using u64 = uint64_t;
+using ull = unsigned long long;
+
+constexpr u32 FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Key maps.  All selection runs on u32 keys where a larger key wins.
+// ---------------------------------------------------------------------------
+enum KeyMode { KM_U32_MAX = 0, KM_U32_MIN = 1, KM_F32_MAX = 2, KM_F32_MIN = 3, KM_KEY = 4 };
+
+template <int M>
+__device__ __forceinline__ u32 to_key(u32 b) {
+  if constexpr (M == KM_U32_MAX || M == KM_KEY) {
+    return b;
+  } else if constexpr (M == KM_U32_MIN) {
+    return ~b;
+  } else {
+    u32 u = b ^ ((u32)((int)b >> 31) | 0x80000000u);
+    if constexpr (M == KM_F32_MAX) return u;
+    return ~u;
+  }
+}
+
+template <int M>
+__device__ __forceinline__ u32 from_key(u32 u) {
+  if constexpr (M == KM_U32_MAX || M == KM_KEY) {
+    return u;
+  } else if constexpr (M == KM_U32_MIN) {
+    return ~u;
+  } else {
+    if constexpr (M == KM_F32_MIN) u = ~u;
+    return u ^ ((u & 0x80000000u) ? 0x80000000u : 0xffffffffu);
+  }
+}
+
+// Radix digits of a key: 11 / 11 / 10 bits, most significant first.
+constexpr int NB1 = 2048, NB2 = 2048, NB3 = 1024;
+__device__ __forceinline__ u32 dig1(u32 k) { return k >> 21; }
+__device__ __forceinline__ u32 dig2(u32 k) { return (k >> 10) & 0x7ffu; }
+__device__ __forceinline__ u32 dig3(u32 k) { return k & 0x3ffu; }
+
+// ---------------------------------------------------------------------------
+// Control block (device memory, zeroed once per call).
+// ---------------------------------------------------------------------------
+struct DigitResult {
+  u32 digit;
+  u32 valid;
+  ull rem;    // rank still sought inside the chosen bucket (1-based)
+  ull cnt;    // population of the chosen bucket
+  ull above;  // population of all higher buckets
+};
+
+struct SelectState {
+  ull hist1[NB1];
+  ull hist2[NB2];
+  ull hist3[NB3];
+  ull buf_count;  // pass-2 compaction counter
+  DigitResult r1, r2, r3;
+  u32 kth;
+  u32 done3;
+};
+
+enum Path : u32 { PATH_NONE = 0, PATH_SELECT = 1, PATH_MERGE = 2, PATH_DIRECT = 3 };
+
+struct Ctrl {
+  dtopk_result res;   // host-visible header (kept first: dtopk_result_offset() == 0)
+  SelectState selD;   // theta = kth(delegates)
+  SelectState selP;   // tau = kth(pool) or kth(V) on the direct path
+  // qualification (K3): ordered list of subranges with max delegate >= theta
+  u32 k3_ticket;
+  u32 pad0;
+  ull cand_count;
+  // concatenation scan (K4)
+  u32 k4_ticket;
+  u32 ties_full;
+  ull k4_tiles;
+  // emit
+  u32 em_ticket;
+  u32 maxkey;
+  u32 sort_lo;
+  u32 sort_bits;
+};
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u32 smem_addr(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(u32 addr, u32 parity) {
+  u32 ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  const u32 a = smem_addr(bar);
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
+// 1-D TMA bulk copy global -> shared, completion signalled on `bar`.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ u64 ld_acquire(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u32 ld_volatile_u32(const u32* p) {
+  return *(const volatile u32*)p;
+}
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// top-beta ladders (registers, non-increasing, zero initialised: the
+// reference's _rows_ladder semantics, delegate.py:93-107)
+// ---------------------------------------------------------------------------
+template <int B>
+__device__ __forceinline__ void ladder_insert(u32 (&L)[B], u32 x) {
+#pragma unroll
+  for (int i = 0; i < B; i++) {
+    const u32 hi = max(L[i], x);
+    x = min(L[i], x);
+    L[i] = hi;
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void ladder_merge(u32 (&L)[B], const u32 (&R)[B]) {
+  if constexpr (B == 1) {
+    L[0] = max(L[0], R[0]);
+  } else if constexpr (B == 2) {
+    const u32 m1 = max(L[0], R[0]);
+    const u32 m2 = max(min(L[0], R[0]), max(L[1], R[1]));
+    L[0] = m1;
+    L[1] = m2;
+  } else {
+#pragma unroll
+    for (int i = 0; i < B; i++) ladder_insert<B>(L, R[i]);
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void ladder_shfl_merge(u32 (&L)[B], int off) {
+  u32 R[B];
+#pragma unroll
+  for (int i = 0; i < B; i++) R[i] = __shfl_xor_sync(FULL, L[i], off);
+  ladder_merge<B>(L, R);
+}
+
+// ---------------------------------------------------------------------------
+// Block scans for 256-thread blocks.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T n = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Inclusive scan over the first 256 threads; all 256 must call. `scratch` >= 8.
+template <typename T>
+__device__ __forceinline__ T block_incl_scan_256(T v, T* scratch) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_incl_scan(v);
+  if (lane == 31) scratch[w] = v;
+  __syncthreads();
+  T add = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+    if (i < w) add += scratch[i];
+  __syncthreads();
+  return v + add;
+}
+
+// Radix-select digit finder: among NB buckets (hist in global memory), find
+// the bucket b holding the k_rem-th largest key: suffix(b+1) < k_rem <= suffix(b).
+// Must be called by all 256 threads of a block; result broadcast via `out` (smem).
+template <int NB>
+__device__ void find_digit(const ull* hist, ull k_rem, DigitResult* out, ull* scratch) {
+  constexpr int PER = NB / 256;
+  const int t = threadIdx.x;
+  ull loc[PER];
+  ull sum = 0;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int b = NB - 1 - (t * PER + i);
+    loc[i] = __ldcg(&hist[b]);
+    sum += loc[i];
+  }
+  if (t == 0) out->valid = 0;
+  const ull incl = block_incl_scan_256<ull>(sum, scratch);
+  ull run = incl - sum;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int b = NB - 1 - (t * PER + i);
+    if (run < k_rem && run + loc[i] >= k_rem) {
+      out->digit = (u32)b;
+      out->rem = k_rem - run;
+      out->cnt = loc[i];
+      out->above = run;
+      out->valid = 1;
+    }
+    run += loc[i];
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back over a chain of u64 tile states:
+//   bits 63..62 flag (0 empty, 1 aggregate, 2 inclusive prefix), 61..0 value.
+// A tile publishes its aggregate, a whole warp walks back 32 predecessors per
+// step (summing aggregates until the nearest inclusive prefix), then the tile
+// publishes its own inclusive prefix.
+// ---------------------------------------------------------------------------
+constexpr u64 LB_VAL = (1ull << 62) - 1;
+constexpr u64 LB_AGG = 1ull << 62;
+constexpr u64 LB_PRE = 2ull << 62;
+
+__device__ __forceinline__ void lb_publish_agg(u64* st, u64 tile, u64 agg) {
+  st_release(&st[tile], (tile == 0 ? LB_PRE : LB_AGG) | agg);
+}
+
+// All 32 lanes of one warp call; the exclusive prefix is returned in every lane.
+__device__ __forceinline__ u64 lb_warp_prefix(u64* st, u64 tile) {
+  const int lane = threadIdx.x & 31;
+  u64 excl = 0;
+  long long hi = (long long)tile - 1;
+  while (hi >= 0) {
+    const long long t = hi - lane;
+    u64 s = LB_PRE;  // before tile 0 the prefix is 0
+    if (t >= 0) {
+      do {
+        s = ld_acquire(&st[t]);
+      } while ((s >> 62) == 0);
+    }
+    const u32 pre = __ballot_sync(FULL, (s >> 62) == 2);
+    const int stop = pre ? __ffs(pre) - 1 : 31;
+    u64 v = lane <= stop ? (s & LB_VAL) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    excl += v;
+    if (pre) break;
+    hi -= 32;
+  }
+  return excl;
+}
+
+__device__ __forceinline__ void lb_publish_prefix(u64* st, u64 tile, u64 incl) {
+  if (tile != 0) st_release(&st[tile], LB_PRE | incl);
+}
+
+}  // namespace dtopk

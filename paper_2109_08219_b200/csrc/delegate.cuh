@@ -1,0 +1,321 @@
+// delegate.cuh -- K1: one streaming pass over the input that emits the
+// top-beta delegates of every 2^alpha subrange (reference: delegate.py:58-191).
+//
+// Design (B200):
+//  * persistent grid, one 288-thread CTA per SM: warp 8 is a TMA producer that
+//    streams 8 KiB chunks (2048 keys) into a 16-stage shared-memory ring with
+//    1-D cp.async.bulk + mbarrier completion; each of warps 0-7 owns every 8th
+//    stage and reduces whole chunks on its own (no CTA-wide barriers).
+//  * consumers read the staged chunk with bank-conflict-free LDS.128, apply the
+//    key map on the fly (float->ordered u32, ~x for smallest) and keep a
+//    register top-beta ladder per lane; subranges are reduced in registers
+//    (W <= 64), with xor-shuffle butterflies (W <= 2048) or as per-chunk
+//    partials merged by a tiny second kernel (W > 2048).
+//  * the first radix digit (top 11 bits) of every delegate is histogrammed in
+//    shared memory and flushed once per CTA: pass 1 of the delegate top-k is
+//    fused into the stream, so the delegate vector is read only once more.
+#pragma once
+
+#include "common.cuh"
+
+namespace dtopk {
+
+constexpr int K1_CHUNK = 2048;    // keys per stage = one warp's unit of work (8 KiB)
+constexpr int K1_LOG_CHUNK = 11;
+constexpr int K1_CWARPS = 8;      // consumer warps
+constexpr int K1_STAGES = 16;     // two stages in flight per consumer warp
+constexpr int K1_THREADS = (K1_CWARPS + 1) * 32;
+constexpr size_t K1_SMEM = (size_t)K1_STAGES * K1_CHUNK * 4 + 2 * K1_STAGES * 8 + NB1 * 4;
+
+struct K1Args {
+  const u32* keys;
+  u64 n;
+  int alpha;
+  u64 S;         // number of subranges = ceil(n / 2^alpha)
+  u32* D;        // [S][B] delegates (key space)
+  u32* partial;  // [nchunks][B] when alpha > K1_LOG_CHUNK
+  ull* hist1;    // global first-digit histogram of D
+  int do_hist;
+};
+
+// Warp-aggregated shared-memory histogram increment; all 32 lanes must call.
+__device__ __forceinline__ void hist_add_agg(u32* shist, u32 bin, bool pred) {
+  const u32 key = pred ? bin : 0xffffffffu;
+  const u32 peers = __match_any_sync(FULL, key);
+  if (pred && (u32)(__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&shist[bin], (u32)__popc(peers));
+}
+
+template <int B>
+__device__ __forceinline__ void store_delegates(u32* D, u64 sid, const u32 (&L)[B]) {
+  if constexpr (B == 2) {
+    *reinterpret_cast<uint2*>(D + sid * 2) = make_uint2(L[0], L[1]);
+  } else if constexpr (B == 4) {
+    *reinterpret_cast<uint4*>(D + sid * 4) = make_uint4(L[0], L[1], L[2], L[3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < B; i++) D[sid * B + i] = L[i];
+  }
+}
+
+// Emit one subrange's delegates: lanes with `leader` write; every lane of the
+// warp must call (warp-aggregated histogram).
+template <int B>
+__device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 sid, bool leader,
+                                              const u32 (&L)[B]) {
+  const bool w = leader && sid < a.S;
+  if (w) store_delegates<B>(a.D, sid, L);
+  if (a.do_hist) {
+#pragma unroll
+    for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, w);
+  }
+}
+
+template <int MODE, bool TAIL>
+__device__ __forceinline__ u32 k1_fetch(const K1Args& a, u64 start, u32 e, u32 cnt, u32 tcnt, u32 smv) {
+  if constexpr (!TAIL) {
+    return to_key<MODE>(smv);
+  } else {
+    if (e >= cnt) return 0u;  // absent: zero pad (delegate.py:132-139)
+    if (e >= tcnt) return to_key<MODE>(a.keys[start + e]);
+    return to_key<MODE>(smv);
+  }
+}
+
+template <int MODE, int B, bool TAIL>
+__device__ __forceinline__ void ladder_uint4(u32 (&L)[B], const K1Args& a, u64 start, u32 e, u32 cnt, u32 tcnt,
+                                             const uint4 v) {
+  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 0, cnt, tcnt, v.x));
+  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 1, cnt, tcnt, v.y));
+  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 2, cnt, tcnt, v.z));
+  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 3, cnt, tcnt, v.w));
+}
+
+// One warp reduces one staged chunk of 2048 keys.  No CTA-wide barrier: the
+// eight consumer warps run decoupled, each on its own stages.
+template <int MODE, int B, bool TAIL>
+__device__ __forceinline__ void k1_warp_chunk(const K1Args& a, const u32* stage, u64 c, u32* shist) {
+  const int lane = threadIdx.x & 31;
+  const u64 start = c << K1_LOG_CHUNK;
+  const u32 cnt = TAIL ? (u32)min((u64)K1_CHUNK, a.n - start) : (u32)K1_CHUNK;
+  const u32 tcnt = TAIL ? ((cnt * 4u) & ~15u) / 4u : (u32)K1_CHUNK;
+  const int alpha = a.alpha;
+  const uint4* st4 = reinterpret_cast<const uint4*>(stage);
+
+  if (alpha <= 4) {
+    // ---- W <= 16, lane-interleaved: uint4 q = j*32 + lane; a subrange spans W/4 lanes
+#pragma unroll 2
+    for (int j = 0; j < 16; j++) {
+      const u32 q = (u32)j * 32u + (u32)lane;
+      const uint4 v = st4[q];
+      const u32 e = q * 4u;
+      if (alpha == 1) {
+        if constexpr (B == 1) {
+          const u32 x0 = k1_fetch<MODE, TAIL>(a, start, e + 0, cnt, tcnt, v.x);
+          const u32 x1 = k1_fetch<MODE, TAIL>(a, start, e + 1, cnt, tcnt, v.y);
+          const u32 x2 = k1_fetch<MODE, TAIL>(a, start, e + 2, cnt, tcnt, v.z);
+          const u32 x3 = k1_fetch<MODE, TAIL>(a, start, e + 3, cnt, tcnt, v.w);
+          const u64 s0 = (start + e) >> 1;
+          u32 L0[1] = {max(x0, x1)};
+          u32 L1[1] = {max(x2, x3)};
+          emit_subrange<1>(a, shist, s0, true, L0);
+          emit_subrange<1>(a, shist, s0 + 1, true, L1);
+        }
+      } else {
+        u32 L[B];
+#pragma unroll
+        for (int i = 0; i < B; i++) L[i] = 0;
+        ladder_uint4<MODE, B, TAIL>(L, a, start, e, cnt, tcnt, v);
+        const int G = 1 << (alpha - 2);
+        for (int off = 1; off < G; off <<= 1) ladder_shfl_merge<B>(L, off);
+        emit_subrange<B>(a, shist, (start + e) >> alpha, (lane & (G - 1)) == 0, L);
+      }
+    }
+    return;
+  }
+
+  // ---- lane-contiguous: lane owns keys [lane*64, lane*64+64).  LDS.128 order
+  // is rotated by lane inside each subrange-aligned group of >= 8 uint4 so a
+  // quarter-warp always hits 8 distinct 16-byte bank groups.
+  const uint4* seg = st4 + lane * 16;
+  const u32 e0 = (u32)lane * 64u;
+  if (alpha == 5) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      u32 L[B];
+#pragma unroll
+      for (int i = 0; i < B; i++) L[i] = 0;
+#pragma unroll
+      for (int jj = 0; jj < 8; jj++) {
+        const int j = (jj + lane) & 7;
+        ladder_uint4<MODE, B, TAIL>(L, a, start, e0 + h * 32 + j * 4, cnt, tcnt, seg[h * 8 + j]);
+      }
+      emit_subrange<B>(a, shist, (start + e0 + h * 32) >> 5, true, L);
+    }
+    return;
+  }
+  u32 L[B];
+#pragma unroll
+  for (int i = 0; i < B; i++) L[i] = 0;
+#pragma unroll
+  for (int jj = 0; jj < 16; jj++) {
+    const int j = (jj + lane) & 15;
+    ladder_uint4<MODE, B, TAIL>(L, a, start, e0 + j * 4, cnt, tcnt, seg[j]);
+  }
+  if (alpha == 6) {
+    emit_subrange<B>(a, shist, (start + e0) >> 6, true, L);
+    return;
+  }
+  const int G = alpha >= K1_LOG_CHUNK ? 32 : 1 << (alpha - 6);  // lanes per subrange
+  for (int off = 1; off < G; off <<= 1) ladder_shfl_merge<B>(L, off);
+  if (alpha <= K1_LOG_CHUNK) {
+    emit_subrange<B>(a, shist, (start + e0) >> alpha, (lane & (G - 1)) == 0, L);
+  } else if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < B; i++) a.partial[c * B + i] = L[i];
+  }
+}
+
+// The (single) ragged last chunk goes through an out-of-line copy so the bounds
+// checks do not inflate the register budget of the steady-state loop.
+template <int MODE, int B>
+__device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stage, u64 c, u32* shist) {
+  k1_warp_chunk<MODE, B, true>(a, stage, c, shist);
+}
+
+template <int MODE, int B>
+__global__ void __launch_bounds__(K1_THREADS, 1) k1_delegates(K1Args a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  u32* stages = reinterpret_cast<u32*>(smem_raw);
+  u64* full = reinterpret_cast<u64*>(smem_raw + (size_t)K1_STAGES * K1_CHUNK * 4);
+  u64* empty = full + K1_STAGES;
+  u32* shist = reinterpret_cast<u32*>(empty + K1_STAGES);
+
+  const u64 nch = (a.n + K1_CHUNK - 1) >> K1_LOG_CHUNK;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < NB1; i += K1_THREADS) shist[i] = 0;
+  if (tid == 0) {
+    for (int s = 0; s < K1_STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // Iteration i of this CTA handles chunk blockIdx.x + i*gridDim.x in stage
+  // i % 16, consumed by warp i % 8; the stage's parity flips every 16 iterations.
+  if (warp == K1_CWARPS) {
+    if (lane == 0) {
+      u64 i = 0;
+      for (u64 c = blockIdx.x; c < nch; c += gridDim.x, i++) {
+        const u32 s = (u32)(i % K1_STAGES);
+        const u32 ph = (u32)(i / K1_STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        const u64 start = c << K1_LOG_CHUNK;
+        const u64 cnt = min((u64)K1_CHUNK, a.n - start);
+        const u32 bytes = (u32)(cnt * 4u) & ~15u;
+        if (bytes) {
+          mbar_arrive_expect_tx(&full[s], bytes);
+          tma_load_1d(stages + (size_t)s * K1_CHUNK, a.keys + start, bytes, &full[s]);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+      }
+    }
+  } else {
+    u64 i = warp;
+    for (u64 c = blockIdx.x + (u64)warp * gridDim.x; c < nch; c += (u64)K1_CWARPS * gridDim.x, i += K1_CWARPS) {
+      const u32 s = (u32)(i % K1_STAGES);
+      const u32 ph = (u32)(i / K1_STAGES) & 1u;
+      mbar_wait(&full[s], ph);
+      const u32* st = stages + (size_t)s * K1_CHUNK;
+      if (((c + 1) << K1_LOG_CHUNK) <= a.n)
+        k1_warp_chunk<MODE, B, false>(a, st, c, shist);
+      else
+        k1_warp_chunk_tail<MODE, B>(a, st, c, shist);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  __syncthreads();
+  if (a.do_hist) {
+    for (int i = tid; i < NB1; i += K1_THREADS) {
+      const u32 v = shist[i];
+      if (v) atomicAdd(&a.hist1[i], (ull)v);
+    }
+  }
+}
+
+// Merge per-chunk partial ladders into per-subrange delegates (alpha > 13).
+template <int B>
+__global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial, u64 nch, int alpha, u64 S,
+                                                u32* __restrict__ D, ull* __restrict__ hist1) {
+  __shared__ u32 shist[NB1];
+  for (int i = threadIdx.x; i < NB1; i += 256) shist[i] = 0;
+  __syncthreads();
+  const u64 cps = 1ull << (alpha - K1_LOG_CHUNK);
+  const u64 stride = (u64)gridDim.x * 256;
+  const u64 s_end = (S + 31) & ~31ull;  // keep whole warps in the loop for hist_add_agg
+  for (u64 s = (u64)blockIdx.x * 256 + threadIdx.x; s < s_end; s += stride) {
+    u32 L[B];
+#pragma unroll
+    for (int i = 0; i < B; i++) L[i] = 0;
+    if (s < S) {
+      const u64 c_end = min(nch, (s + 1) * cps);
+      for (u64 c = s * cps; c < c_end; c++) {
+        u32 R[B];
+#pragma unroll
+        for (int i = 0; i < B; i++) R[i] = partial[c * B + i];
+        ladder_merge<B>(L, R);
+      }
+      store_delegates<B>(D, s, L);
+    }
+#pragma unroll
+    for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, s < S);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NB1; i += 256) {
+    const u32 v = shist[i];
+    if (v) atomicAdd(&hist1[i], (ull)v);
+  }
+}
+
+// Generic top-beta for 8 < beta <= 32: one warp per subrange, per-lane
+// insertion ladders (the reference's _rows_ladder, delegate.py:93-107), then a
+// beta-round warp arg-max merge.  Cold path: correctness over speed.
+template <int MODE>
+__global__ void __launch_bounds__(256) k1_generic(const u32* __restrict__ keys, u64 n, int alpha, int beta,
+                                                  u64 S, u32* __restrict__ D, ull* __restrict__ hist1) {
+  const int lane = threadIdx.x & 31;
+  const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u64 W = 1ull << alpha;
+  for (u64 s = gw; s < S; s += nw) {
+    u32 L[32];
+    for (int i = 0; i < 32; i++) L[i] = 0;
+    for (u64 e = lane; e < W; e += 32) {
+      const u64 i = s * W + e;
+      const u32 x = i < n ? to_key<MODE>(keys[i]) : 0u;
+      if (x <= L[beta - 1]) continue;
+      int p = beta - 1;
+      while (p > 0 && x > L[p - 1]) {
+        L[p] = L[p - 1];
+        p--;
+      }
+      L[p] = x;
+    }
+    int ptr = 0;
+    for (int r = 0; r < beta; r++) {
+      const u32 head = ptr < beta ? L[ptr] : 0u;
+      const u32 m = __reduce_max_sync(FULL, head);
+      const u32 win = __ballot_sync(FULL, head == m);
+      if (lane == __ffs(win) - 1) ptr++;
+      if (lane == 0) {
+        D[s * beta + r] = m;
+        atomicAdd(&hist1[m >> 21], 1ull);
+      }
+    }
+  }
+}
+
+}  // namespace dtopk

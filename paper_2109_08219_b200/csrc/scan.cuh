@@ -1,0 +1,535 @@
+// scan.cuh -- K4 (filtered concatenation) and the ordered emit of the final
+// top-k, both built on one order-preserving compaction kernel.
+//
+// Reference: pipeline.concatenate_filtered (pipeline.py:119-159) and the
+// tie rule of kernels._extract_exact (kernels.py:83-96): every element
+// strictly above the threshold first, then threshold-equal elements in scan
+// order until k slots are filled.
+//
+// One tile = 8192 virtual elements = 8 warps x 1024; a warp loads 8 rounds of
+// 32 lanes x uint4 (512 contiguous bytes per instruction).  Phase 1 counts
+// (gt, eq) per thread; the tile publishes its aggregate on two decoupled
+// look-back chains; phase 2 re-derives the predicates from registers and
+// writes every selected element at its stable (index-ordered) position using
+// ballots, so no per-element atomics and no second read are needed.
+//
+// K4 (CAND=true) walks the ordered candidate-subrange list produced by K2 and
+//  * skips subranges whose max delegate is below theta,
+//  * reads subranges with max > theta (elements > theta -> pool P_gt),
+//  * reads tie-only subranges (max == theta) only while the tie buffer (first k
+//    ties in index order) is not yet full -- this keeps all-equal and
+//    few-distinct inputs at ~1 pass instead of the reference's 2-7 passes.
+// emit (CAND=false) walks a flat array (P_gt or the raw input) with the exact
+// k-th key tau and writes the answer's keys/indices into the sort buffer.
+#pragma once
+
+#include "common.cuh"
+
+namespace dtopk {
+
+constexpr int SC_TILE = 8192;
+
+struct ScanArgs {
+  const u32* keys;
+  u64 n;              // CAND: input length
+  const u64* idx_in;  // FLAT: explicit indices (null = position)
+  u64 m_host;         // FLAT: element count
+  const ull* m_dev;
+  const u32* cand_sid;
+  const u32* cand_d1;
+  const u32* cand_dl;
+  int alpha;
+  const int64_t* theta_override;
+  u32 flags;
+  Ctrl* ctrl;
+  u64 k;
+  u32* gt_keys;
+  u64* gt_idx;
+  u32* eq_keys;
+  u64* eq_idx;
+  u64* lb_gt;
+  u64* lb_eq;
+  int check_path;
+  int direct;
+};
+
+template <int MODE, bool CAND>
+__global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
+  __shared__ DigitResult r3s;
+  __shared__ ull scratch[8];
+  __shared__ u32 s_wgt[8], s_weq[8];
+  __shared__ u64 s_tile, s_gtx, s_eqx;
+  __shared__ int s_skip;
+  __shared__ ull s_stat[3][8];
+  __shared__ u32 s_max[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Ctrl* ctrl = a.ctrl;
+  if (a.check_path && ld_volatile_u32(&ctrl->res.path) != PATH_SELECT) return;
+
+  u32 theta;
+  u64 eq_cap;
+  u32* eqk = a.eq_keys;
+  u64* eqi = a.eq_idx;
+  u32* ticket;
+  if constexpr (CAND) {
+    theta = ctrl->res.theta;  // exact kth(D), or max with an external theta (K3)
+    eq_cap = a.k;
+    ticket = &ctrl->k4_ticket;
+  } else {
+    const DigitResult r1 = ctrl->selP.r1, r2 = ctrl->selP.r2;
+    find_digit<NB3>(ctrl->selP.hist3, r2.rem, &r3s, scratch);
+    theta = (r1.digit << 21) | (r2.digit << 10) | r3s.digit;
+    eq_cap = r3s.rem;
+    const u64 ngt = a.k - eq_cap;
+    eqk += ngt;
+    eqi += ngt;
+    ticket = &ctrl->em_ticket;
+    if (blockIdx.x == 0 && tid == 0) {
+      ctrl->selP.r3 = r3s;
+      ctrl->selP.kth = theta;
+      ctrl->sort_lo = theta;
+      ctrl->res.k_out = a.k;
+      if (a.direct) {
+        ctrl->res.path = PATH_DIRECT;
+        ctrl->res.theta = theta;
+      }
+      atomicMax(&ctrl->maxkey, theta);
+    }
+  }
+  const u64 W = 1ull << a.alpha;
+  const u64 P = CAND ? (u64)ctrl->cand_count : 0;
+  const u64 total = CAND ? (P << a.alpha) : (a.m_dev ? (u64)*a.m_dev : a.m_host);
+  const u64 T = (total + SC_TILE - 1) / SC_TILE;
+  const bool exact = (a.flags & DTOPK_FLAG_EXACT_STATS) != 0;
+
+  u32 bmax = 0;
+  ull st_concat = 0, st_skipfq = 0, st_reread = 0;
+
+  for (;;) {
+    if (tid == 0) {
+      s_tile = atomicAdd(ticket, 1u);
+      s_skip = CAND && !exact ? (int)ld_volatile_u32(&ctrl->ties_full) : 0;
+    }
+    __syncthreads();
+    const u64 tile = s_tile;
+    const bool skip_ties = s_skip != 0;
+    if (tile >= T) break;
+
+    // ---------------- phase 1: load + count
+    u32 kv[8][4];
+    u64 pb[8];
+    u32 vm[8];
+    u32 cgt = 0, ceq = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const u64 v0 = tile * SC_TILE + (u64)warp * 1024 + (u64)j * 128 + (u64)lane * 4;
+      u32 x[4] = {0u, 0u, 0u, 0u};
+      u32 valid = 0;
+      u64 base = 0;
+      if constexpr (CAND) {
+        if (a.alpha >= 2) {
+          const u64 ci = v0 >> a.alpha;
+          if (ci < P) {
+            const u32 sid = a.cand_sid[ci];
+            const u32 d1 = a.cand_d1[ci];
+            const u64 off = v0 & (W - 1);
+            base = ((u64)sid << a.alpha) | off;
+            const bool fq = a.cand_dl[ci] >= theta;
+            const bool rd = d1 > theta || (d1 == theta && !skip_ties);
+            if (off == 0 && !rd && fq) st_skipfq++;
+            if (rd) {
+              if (base + 4 <= a.n) {
+                const uint4 q = ld_nc_v4(a.keys + base);
+                x[0] = to_key<MODE>(q.x);
+                x[1] = to_key<MODE>(q.y);
+                x[2] = to_key<MODE>(q.z);
+                x[3] = to_key<MODE>(q.w);
+                valid = 0xfu;
+              } else {
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                  if (base + c < a.n) {
+                    x[c] = to_key<MODE>(a.keys[base + c]);
+                    valid |= 1u << c;
+                  }
+              }
+              st_reread += __popc(valid);
+              if (fq) {
+#pragma unroll
+                for (int c = 0; c < 4; c++) st_concat += ((valid >> c) & 1u) && x[c] >= theta;
+              }
+            }
+          }
+        } else {
+          // alpha == 1: two elements per subrange, handled element-wise
+#pragma unroll
+          for (int c = 0; c < 4; c++) {
+            const u64 v = v0 + c;
+            const u64 ci = v >> 1;
+            if (ci < P) {
+              const u32 sid = a.cand_sid[ci];
+              const u32 d1 = a.cand_d1[ci];
+              const u64 off = v & 1;
+              const u64 phys = ((u64)sid << 1) | off;
+              const bool fq = a.cand_dl[ci] >= theta;
+              const bool rd = d1 > theta || (d1 == theta && !skip_ties);
+              if (off == 0 && !rd && fq) st_skipfq++;
+              if (rd && phys < a.n) {
+                x[c] = to_key<MODE>(a.keys[phys]);
+                valid |= 1u << c;
+                st_reread++;
+                if (fq && x[c] >= theta) st_concat++;
+              }
+              if (c == 0) base = phys;
+              // element-wise indices are rebuilt in phase 2 from the list
+            }
+          }
+        }
+      } else {
+        const u64 m = total;
+        base = v0;
+        if (v0 + 4 <= m) {
+          const uint4 q = ld_nc_v4(a.keys + v0);
+          x[0] = to_key<MODE>(q.x);
+          x[1] = to_key<MODE>(q.y);
+          x[2] = to_key<MODE>(q.z);
+          x[3] = to_key<MODE>(q.w);
+          valid = 0xfu;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; c++)
+            if (v0 + c < m) {
+              x[c] = to_key<MODE>(a.keys[v0 + c]);
+              valid |= 1u << c;
+            }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const bool vld = (valid >> c) & 1u;
+        const bool g = vld && x[c] > theta;
+        cgt += g;
+        ceq += vld && x[c] == theta;
+        if (g) bmax = max(bmax, x[c]);
+        kv[j][c] = x[c];
+      }
+      vm[j] = valid;
+      pb[j] = base;
+    }
+    const u32 wg = __reduce_add_sync(FULL, cgt), we = __reduce_add_sync(FULL, ceq);
+    if (lane == 0) {
+      s_wgt[warp] = wg;
+      s_weq[warp] = we;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      u64 ag = 0, ae = 0;
+      for (int w = 0; w < 8; w++) {
+        ag += s_wgt[w];
+        ae += s_weq[w];
+      }
+      if (lane == 0) {
+        lb_publish_agg(a.lb_gt, tile, ag);
+        lb_publish_agg(a.lb_eq, tile, ae);
+      }
+      const u64 xg = lb_warp_prefix(a.lb_gt, tile);
+      const u64 xe = lb_warp_prefix(a.lb_eq, tile);
+      if (lane == 0) {
+      lb_publish_prefix(a.lb_gt, tile, xg + ag);
+      lb_publish_prefix(a.lb_eq, tile, xe + ae);
+      s_gtx = xg;
+      s_eqx = xe;
+      if (CAND && xe + ae >= eq_cap) atomicExch(&ctrl->ties_full, 1u);
+      if (tile == T - 1) {
+        const u64 G = xg + ag, E = xe + ae;
+        if constexpr (CAND) {
+          ctrl->res.pool_gt = G;
+          ctrl->res.pool_eq = min(E, (u64)a.k);
+          if (G >= a.k) {
+            ctrl->res.path = PATH_SELECT;
+          } else {
+            ctrl->res.path = PATH_MERGE;
+            ctrl->res.k_out = min((u64)a.k, G + E);
+            ctrl->sort_lo = theta;
+            atomicMax(&ctrl->maxkey, theta);
+          }
+        }
+      }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- phase 2: ordered writes
+    u64 gpos = s_gtx, epos = s_eqx;
+    for (int w = 0; w < warp; w++) {
+      gpos += s_wgt[w];
+      epos += s_weq[w];
+    }
+    const u32 lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      u32 bg[4], be[4];
+      bool g[4], e[4];
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const bool vld = (vm[j] >> c) & 1u;
+        g[c] = vld && kv[j][c] > theta;
+        e[c] = vld && kv[j][c] == theta;
+        bg[c] = __ballot_sync(FULL, g[c]);
+        be[c] = __ballot_sync(FULL, e[c]);
+      }
+      const u32 anyg = bg[0] | bg[1] | bg[2] | bg[3];
+      const u32 anye = be[0] | be[1] | be[2] | be[3];
+      if (anyg | anye) {
+        u64 go = gpos, eo = epos;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          go += __popc(bg[c] & lt);
+          eo += __popc(be[c] & lt);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          if (g[c] || e[c]) {
+            u64 idx;
+            if constexpr (CAND) {
+              if (a.alpha >= 2) {
+                idx = pb[j] + c;
+              } else {
+                const u64 v = tile * SC_TILE + (u64)warp * 1024 + (u64)j * 128 + (u64)lane * 4 + c;
+                idx = ((u64)a.cand_sid[v >> 1] << 1) | (v & 1);
+              }
+            } else {
+              idx = a.idx_in ? a.idx_in[pb[j] + c] : pb[j] + c;
+            }
+            if (g[c]) {
+              a.gt_keys[go] = kv[j][c];
+              a.gt_idx[go] = idx;
+              go++;
+            }
+            if (e[c]) {
+              if (eo < eq_cap) {
+                if (eqk) eqk[eo] = kv[j][c];
+                eqi[eo] = idx;
+              }
+              eo++;
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          gpos += __popc(bg[c]);
+          epos += __popc(be[c]);
+        }
+      }
+    }
+  }
+
+  // ---------------- block-level stats and max
+  bmax = __reduce_max_sync(FULL, bmax);
+  if (lane == 0) s_max[warp] = bmax;
+  if constexpr (CAND) {
+    ull v[3] = {st_concat, st_skipfq, st_reread};
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(FULL, v[i], o);
+      if (lane == 0) s_stat[i][warp] = v[i];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    u32 m = 0;
+    for (int w = 0; w < 8; w++) m = max(m, s_max[w]);
+    if (m) atomicMax(&ctrl->maxkey, m);
+    if constexpr (CAND) {
+      ull t[3] = {0, 0, 0};
+      for (int i = 0; i < 3; i++)
+        for (int w = 0; w < 8; w++) t[i] += s_stat[i][w];
+      if (t[0]) atomicAdd((ull*)&ctrl->res.concatenated_len, t[0]);
+      if (t[1]) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, t[1]);
+      if (t[2]) atomicAdd((ull*)&ctrl->res.elements_reread, t[2]);
+    }
+  }
+}
+
+// MERGE path: answer = P_gt (all keys > theta, index order) ++ first ties.
+__global__ void __launch_bounds__(256) merge_copy(Ctrl* ctrl, const u32* __restrict__ gk, const u64* __restrict__ gi,
+                                                  const u64* __restrict__ ties, u32* __restrict__ ok,
+                                                  u64* __restrict__ oi) {
+  if (ld_volatile_u32(&ctrl->res.path) != PATH_MERGE) return;
+  const u64 G = ctrl->res.pool_gt, kout = ctrl->res.k_out;
+  const u32 theta = ctrl->res.theta;
+  for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < kout; i += (u64)gridDim.x * 256) {
+    if (i < G) {
+      ok[i] = gk[i];
+      oi[i] = gi[i];
+    } else {
+      ok[i] = theta;
+      oi[i] = ties[i - G];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD radix sort of the k answer pairs by key descending: digits of
+// (maxkey - key), only as many 8-bit passes as max - min needs.  Input order
+// is index order within equal keys, so stability yields (key desc, index asc).
+// ---------------------------------------------------------------------------
+constexpr int ST_TILE = 2048;
+constexpr int SMALL_SORT = 8192;  // answers up to this size are sorted by one CTA
+
+__device__ __forceinline__ int sort_bits(const Ctrl* c) {
+  const u32 lo = c->sort_lo;
+  const u32 hi = max(c->maxkey, lo);
+  return hi == lo ? 0 : 32 - __clz(hi - lo);
+}
+
+__device__ __forceinline__ bool big_sort_skip(const Ctrl* c, int pass) {
+  return c->res.k_out <= (ull)SMALL_SORT || pass * 8 >= sort_bits(c);
+}
+
+__global__ void __launch_bounds__(256) sort_hist(Ctrl* ctrl, const u32* __restrict__ keys, int pass,
+                                                 u32* __restrict__ counts) {
+  if (big_sort_skip(ctrl, pass)) return;
+  __shared__ u32 h[256];
+  const u64 kout = ctrl->res.k_out;
+  const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
+  const u64 T = (kout + ST_TILE - 1) / ST_TILE;
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    for (int r = 0; r < ST_TILE / 256; r++) {
+      const u64 e = tile * ST_TILE + (u64)r * 256 + threadIdx.x;
+      if (e < kout) atomicAdd(&h[((hi - keys[e]) >> (8 * pass)) & 255u], 1u);
+    }
+    __syncthreads();
+    counts[tile * 256 + threadIdx.x] = h[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) sort_scan(Ctrl* ctrl, int pass, u32* __restrict__ counts) {
+  if (big_sort_skip(ctrl, pass)) return;
+  __shared__ u32 scratch[8];
+  const u64 T = (ctrl->res.k_out + ST_TILE - 1) / ST_TILE;
+  const int d = threadIdx.x;
+  u32 run = 0;
+  for (u64 t = 0; t < T; t++) {
+    const u32 v = counts[t * 256 + d];
+    counts[t * 256 + d] = run;
+    run += v;
+  }
+  const u32 incl = block_incl_scan_256<u32>(run, scratch);
+  const u32 base = incl - run;
+  for (u64 t = 0; t < T; t++) counts[t * 256 + d] += base;
+}
+
+__global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, int pass, const u32* __restrict__ kin,
+                                                    const u64* __restrict__ iin, u32* __restrict__ kout,
+                                                    u64* __restrict__ iout, const u32* __restrict__ counts) {
+  if (big_sort_skip(ctrl, pass)) return;
+  __shared__ u32 wc[8][256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u64 ko = ctrl->res.k_out;
+  const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
+  const u64 T = (ko + ST_TILE - 1) / ST_TILE;
+  const u32 lt = lanemask_lt();
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    for (int i = tid; i < 8 * 256; i += 256) (&wc[0][0])[i] = 0;
+    __syncthreads();
+    u32 key[8], dg[8], rk[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const u64 e = tile * ST_TILE + (u64)warp * 256 + (u64)r * 32 + lane;
+      const bool v = e < ko;
+      key[r] = v ? kin[e] : 0u;
+      dg[r] = v ? ((hi - key[r]) >> (8 * pass)) & 255u : 256u;
+      const u32 peers = __match_any_sync(FULL, dg[r]);
+      const u32 leader = __ffs(peers) - 1;
+      rk[r] = v ? wc[warp][dg[r]] + __popc(peers & lt) : 0u;
+      __syncwarp();
+      if (v && lane == leader) wc[warp][dg[r]] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      u32 run = 0;
+      for (int w = 0; w < 8; w++) {
+        const u32 c = wc[w][tid];
+        wc[w][tid] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const u64 e = tile * ST_TILE + (u64)warp * 256 + (u64)r * 32 + lane;
+      if (e < ko) {
+        const u64 pos = (u64)counts[tile * 256 + dg[r]] + wc[warp][dg[r]] + rk[r];
+        kout[pos] = key[r];
+        iout[pos] = iin[e];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) writeout(Ctrl* ctrl, const u32* __restrict__ kA, const u64* __restrict__ iA,
+                                                const u32* __restrict__ kB, const u64* __restrict__ iB,
+                                                u32* __restrict__ ov, long long* __restrict__ oi, long long offset) {
+  const u64 ko = ctrl->res.k_out;
+  if (ko <= (u64)SMALL_SORT) return;  // sort_small wrote the answer
+  const int nb = sort_bits(ctrl);
+  const int passes = (nb + 7) / 8;
+  const u32* ks = (passes & 1) ? kB : kA;
+  const u64* is = (passes & 1) ? iB : iA;
+  for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < ko; i += (u64)gridDim.x * 256) {
+    const u32 key = ks[i];
+    ov[i] = from_key<MODE>(key);
+    oi[i] = (long long)is[i] + offset;
+    if (i == ko - 1) ctrl->res.kth_key = key;
+  }
+}
+
+// One CTA sorts answers of up to SMALL_SORT pairs in shared memory and writes
+// them out: bitonic sort of (maxkey - key) << 32 | position, so equal keys keep
+// their (index-ordered) input positions -- a stable descending sort.
+template <int MODE>
+__global__ void __launch_bounds__(1024) sort_small(Ctrl* ctrl, const u32* __restrict__ kA,
+                                                   const u64* __restrict__ iA, u32* __restrict__ ov,
+                                                   long long* __restrict__ oi, long long offset) {
+  extern __shared__ unsigned long long sk[];  // SMALL_SORT entries (64 KiB, dynamic)
+  const u64 ko = ctrl->res.k_out;
+  if (ko > (u64)SMALL_SORT || ko == 0) return;
+  const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
+  u32 np = 1;
+  while (np < ko) np <<= 1;
+  for (u32 i = threadIdx.x; i < np; i += 1024)
+    sk[i] = i < ko ? ((unsigned long long)(hi - kA[i]) << 32) | i : ~0ull;
+  __syncthreads();
+  for (u32 size = 2; size <= np; size <<= 1) {
+    for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+      for (u32 t = threadIdx.x; t < np / 2; t += 1024) {
+        const u32 lo = 2 * t - (t & (stride - 1));
+        const u32 hi2 = lo + stride;
+        const bool up = (lo & size) == 0;
+        const unsigned long long x = sk[lo], y = sk[hi2];
+        if ((x > y) == up) {
+          sk[lo] = y;
+          sk[hi2] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (u32 i = threadIdx.x; i < ko; i += 1024) {
+    const u32 pos = (u32)(sk[i] & 0xffffffffu);
+    const u32 key = hi - (u32)(sk[i] >> 32);
+    ov[i] = from_key<MODE>(key);
+    oi[i] = (long long)iA[pos] + offset;
+    if (i == ko - 1) ctrl->res.kth_key = key;
+  }
+}
+
+}  // namespace dtopk

@@ -1,0 +1,205 @@
+"""Sharded top-k across the GPUs of one node (reference: distributed.py).
+
+The reference runs one ``dr_topk`` per partition on in-process threads and
+gathers ``k`` values per worker to a coordinator that sorts them
+(distributed.py:140-251; the paper's MPI gather).  Here one
+process drives one GPU (``torch.distributed``, NCCL over NVLink/NVSwitch):
+
+1. every rank owns a contiguous shard (``plan``/``shard_bounds``: equal
+   partitions, distributed.py:97-131) and runs K1-K2 locally
+   (``dtopk_select_begin``) -> theta_r = kth(D_r), an int64 in device memory;
+2. ``all_reduce(MAX)`` of theta_r (8 bytes): every theta_r <= kth(shard r) <=
+   kth(V), so max_r theta_r is a valid global filter (the exchange the paper
+   disabled on MPI, is ~10 us on NVLink);
+3. each rank finishes (``dtopk_select_finish``) with theta* and emits at most
+   k (value, global index) pairs ordered (key desc, index asc);
+4. ``all_gather`` of the counts and the fixed-size candidate buffers, then an
+   exact device top-k over the rank-ordered concatenation.  Shards are
+   contiguous in rank order, so position order among equal keys is global
+   index order and the tie rule (lowest index first) is preserved.
+
+The per-rank compute is injectable (``LocalOps``) so the exchange/merge logic
+is exercised by world-size-2 ``gloo`` tests on CPU; the product uses
+``DeviceOps`` (sm_100a library) with NCCL.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import torch
+import torch.distributed as dist
+
+from .core import InvalidK, PipelineConfig, TopKResult, WorkloadStats, validate_config
+
+
+class WorkerFailed(RuntimeError):
+    """A rank failed; the run is aborted (distributed.py:47-48)."""
+
+
+@dataclass(frozen=True)
+class Partition:
+    index: int
+    offset: int
+    length: int
+    resident: bool
+
+
+@dataclass(frozen=True)
+class PartitionPlan:
+    n: int
+    partition_len: int
+    partitions: tuple
+    assignments: dict
+
+    def worker_count(self) -> int:
+        return len(self.assignments)
+
+
+DEFAULT_MAX_RESIDENT = 1 << 26  # distributed.py:43 (desk-scale cap of the CPU reference)
+
+
+def plan(n: int, k: int, workers: int, max_resident: int = DEFAULT_MAX_RESIDENT) -> PartitionPlan:
+    """Partition arithmetic of the reference (distributed.py:97-131)."""
+    if workers < 1:
+        raise ValueError("workers must be at least 1")
+    if n < 1:
+        raise ValueError("n must be at least 1")
+    plen = math.ceil(n / workers) if workers * max_resident >= n else max_resident
+    if k > plen:
+        raise InvalidK(f"k={k} exceeds the partition length {plen}")
+    parts, assign = [], {w: [] for w in range(workers)}
+    for i in range(math.ceil(n / plen)):
+        w = i % workers
+        parts.append(Partition(i, i * plen, min(plen, n - i * plen), not assign[w]))
+        assign[w].append(i)
+    return PartitionPlan(n, plen, tuple(parts), assign)
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """[offset, offset + length) of rank's contiguous equal shard."""
+    plen = math.ceil(n / world)
+    lo = min(n, rank * plen)
+    return lo, min(n, lo + plen) - lo
+
+
+# ---------------------------------------------------------------------------
+class LocalOps:
+    """Per-rank compute used by ``sharded_topk`` (device or test stand-in)."""
+
+    def begin(self, shard, cfg: PipelineConfig):  # -> (state, theta tensor int64[1])
+        raise NotImplementedError
+
+    def finish(self, state, theta: torch.Tensor, index_offset: int):  # -> (values, indices) of <= k pairs
+        raise NotImplementedError
+
+    def merge(self, values, indices, k: int, largest: bool):  # exact top-k of the concatenation
+        raise NotImplementedError
+
+
+class DeviceOps(LocalOps):
+    """The product path: libdtopk.so on this rank's GPU."""
+
+    def begin(self, shard, cfg):
+        from . import _device, _native
+        from .pipeline import DrTopK
+
+        dv = _device.to_device(shard)
+        p = DrTopK(dv.n, cfg, dv.code, dv.out_dtype, dv.device, timed=False)
+        c = p.cfg
+        s = torch.cuda.current_stream(dv.device)
+        if c.direct_fallback:
+            return (p, dv, True), None
+        st = p.lib.dtopk_select_begin(dv.keys.data_ptr(), dv.n, dv.code, c.k, int(c.largest), c.alpha, c.beta,
+                                      p.flags, p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None)
+        _native.check(st, "dtopk_select_begin")
+        off = _native.DtopkResult.theta_slot.offset
+        theta = p.ws[off:off + 8].view(torch.int64)
+        return (p, dv, False), theta
+
+    def finish(self, state, theta, index_offset):
+        from . import _native
+
+        p, dv, direct = state
+        c = p.cfg
+        s = torch.cuda.current_stream(dv.device)
+        if direct:
+            p.launch(dv.keys, index_offset=index_offset)
+        else:
+            st = p.lib.dtopk_select_finish(
+                dv.keys.data_ptr(), dv.n, dv.code, c.k, int(c.largest), c.alpha, c.beta, p.flags,
+                theta.data_ptr() if theta is not None else None, p.values.data_ptr(), p.indices.data_ptr(),
+                int(index_offset), p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None)
+            _native.check(st, "dtopk_select_finish")
+        hdr = p.header()
+        k_out = int(hdr.k_out)
+        return p.values[:k_out], p.indices[:k_out]
+
+    def merge(self, values, indices, k, largest):
+        from .pipeline import dr_topk
+
+        r = dr_topk(values, PipelineConfig(k=k, alpha=0, auto_alpha=False, largest=largest))
+        return r.values, indices[r.indices]
+
+
+def sharded_topk(shard, n_total: int, k: int, cfg: PipelineConfig | None = None, *, group=None,
+                 index_offset: int | None = None, exchange_theta: bool = True,
+                 ops: LocalOps | None = None) -> TopKResult:
+    """Global top-k of a vector sharded contiguously over the ranks of ``group``.
+
+    Every rank passes its own shard (``shard_bounds`` layout unless
+    ``index_offset`` is given) and receives the global answer.
+    """
+    ops = ops or DeviceOps()
+    cfg = cfg or PipelineConfig(k=k)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n_local = int(shard.numel())
+    if index_offset is None:
+        index_offset, _ = shard_bounds(n_total, world, rank)
+    if not 1 <= k <= n_total:
+        raise InvalidK(f"k={k} outside [1, {n_total}]")
+    k_local = min(k, n_local)
+    lcfg = validate_config(replace(cfg, k=k_local), n_local)
+    try:
+        state, theta = ops.begin(shard, lcfg)
+    except Exception as exc:  # surfaced like the reference's WorkerFailed (distributed.py:238-241)
+        raise WorkerFailed(f"rank {rank} failed in begin: {exc!r}") from exc
+    # Every rank must join the collective; direct-path ranks contribute theta = 0.
+    t = theta if theta is not None else torch.zeros(1, dtype=torch.int64, device=_dev_of(shard))
+    if exchange_theta:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    vals, idx = ops.finish(state, t if (theta is not None and exchange_theta) else theta, index_offset)
+    # all_gather counts, then fixed-size candidate buffers
+    dev = vals.device
+    cnt = torch.tensor([vals.numel()], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    counts = [int(c.item()) for c in counts]
+    width = max(counts) if counts else 0
+    vbuf = torch.zeros(width, dtype=vals.dtype, device=dev)
+    ibuf = torch.zeros(width, dtype=torch.int64, device=dev)
+    vbuf[: vals.numel()] = vals
+    ibuf[: idx.numel()] = idx
+    vg = [torch.empty_like(vbuf) for _ in range(world)]
+    ig = [torch.empty_like(ibuf) for _ in range(world)]
+    dist.all_gather(_as_gatherable(vg), _as_gatherable([vbuf])[0], group=group)
+    dist.all_gather(ig, ibuf, group=group)
+    cat_v = torch.cat([g[:c] for g, c in zip(vg, counts)])
+    cat_i = torch.cat([g[:c] for g, c in zip(ig, counts)])
+    values, indices = ops.merge(cat_v, cat_i, k, lcfg.largest)
+    stats = WorkloadStats()
+    stats.device = {"gathered_pairs": int(sum(counts)), "gathered_bytes": int(sum(counts)) * (vals.element_size() + 8),
+                    "theta_global": int(t.item()) if exchange_theta else None}
+    thr = values[-1].item() if hasattr(values, "item") else values[-1]
+    return TopKResult(values=values, threshold=thr, stats=stats, indices=indices)
+
+
+def _dev_of(x):
+    return x.device if isinstance(x, torch.Tensor) else torch.device("cpu")
+
+
+def _as_gatherable(ts):
+    # NCCL/gloo lack uint32 all_gather: move the bits as int32
+    return [t.view(torch.int32) if t.dtype == torch.uint32 else t for t in ts]

@@ -1,0 +1,243 @@
+"""Delegate-assisted top-k on B200: the drop-in for ``dtopk.pipeline``.
+
+``dr_topk(v, cfg, *, stats=None) -> TopKResult`` keeps the reference
+signature (pipeline.py:172-220).  Its data path is one C-ABI call
+(``dtopk_select``, include/dtopk.h) that launches the sm_100a pipeline on the
+caller's current CUDA stream:
+
+  Delegate  K1  one TMA-streamed pass over V -> top-beta delegates D (+ digit-1 histogram)
+  FirstK    K2  theta = exact kth(D) by 11/11/10-bit radix select; ordered list of
+                subranges whose max delegate can reach theta
+  Concat    K4  ordered compaction of elements > theta from qualifying subranges,
+                plus the first k ties at theta in index order
+  SecondK       radix select over the pool when it exceeds k, ordered emit,
+                stable radix sort by key, write-out in the input dtype
+
+and synchronises once, to read the 104-byte result header.  There is no CPU
+fallback: without libdtopk.so or a CUDA device the call raises.
+
+The stage-inspection functions ``first_topk`` / ``concatenate_filtered``
+mirror the reference operators (pipeline.py:87-159) for parity tests; they are
+built from the same device kernels plus small device-side tensor ops, and are
+not on the hot path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _native
+from .core import (
+    STAGE_CONCAT,
+    STAGE_DELEGATE,
+    STAGE_FIRSTK,
+    STAGE_SECONDK,
+    InvalidK,
+    PipelineConfig,
+    TopKResult,
+    WorkloadStats,
+    validate_config,
+)
+
+_HEADER_BYTES = ctypes.sizeof(_native.DtopkResult)
+_tls = threading.local()
+
+
+def _stage_events():
+    """Five reusable CUDA events per thread (start + 4 stage ends)."""
+    ev = getattr(_tls, "events", None)
+    if ev is None:
+        lib = _native.load()
+        handles = [lib.dtopk_event_create() for _ in range(5)]
+        ev = (ctypes.c_void_p * 5)(*handles)
+        _tls.events = ev
+    return ev
+
+
+def read_header(ws: torch.Tensor) -> _native.DtopkResult:
+    """Copy the device result header to the host (synchronises the stream)."""
+    raw = ws[:_HEADER_BYTES].cpu().numpy().tobytes()
+    return _native.DtopkResult.from_buffer_copy(raw)
+
+
+class DrTopK:
+    """Pre-planned top-k for a fixed (n, cfg, dtype, device).
+
+    Owns the workspace and output buffers so repeated calls allocate nothing;
+    ``launch`` is fully asynchronous (stream-ordered, no host sync), which is
+    what the device-resident benchmark times.  ``dr_topk`` builds one per call.
+    """
+
+    def __init__(self, n: int, cfg: PipelineConfig, code: int, out_dtype: torch.dtype, device, *,
+                 exact_stats: bool = False, timed: bool = True):
+        self.lib = _native.load()
+        self.n = int(n)
+        self.cfg = validate_config(cfg, self.n)
+        self.code = code
+        self.device = torch.device(device)
+        self.flags = _native.FLAG_EXACT_STATS if exact_stats else 0
+        c = self.cfg
+        self.ws_bytes = int(self.lib.dtopk_workspace_bytes(self.n, c.k, c.alpha, c.beta, int(c.direct_fallback)))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.values = torch.empty(c.k, dtype=out_dtype, device=self.device)
+        self.indices = torch.empty(c.k, dtype=torch.int64, device=self.device)
+        self.events = _stage_events() if timed else None
+
+    def launch(self, keys: torch.Tensor, stream: torch.cuda.Stream | None = None, index_offset: int = 0,
+               events=None) -> None:
+        c = self.cfg
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st = self.lib.dtopk_select(
+            keys.data_ptr(), self.n, self.code, c.k, int(c.largest), c.alpha, c.beta, int(c.direct_fallback),
+            self.flags, self.values.data_ptr(), self.indices.data_ptr(), int(index_offset), self.ws.data_ptr(),
+            self.ws_bytes, s.cuda_stream, events if events is not None else self.events,
+        )
+        _native.check(st, "dtopk_select")
+
+    def header(self) -> _native.DtopkResult:
+        return read_header(self.ws)
+
+    def stage_nanos(self) -> dict:
+        if self.events is None:
+            return {}
+        el = self.lib.dtopk_event_elapsed_ms
+        e = self.events
+        return {
+            stage: max(0, int(round(el(e[i], e[i + 1]) * 1e6)))
+            for i, stage in enumerate((STAGE_DELEGATE, STAGE_FIRSTK, STAGE_CONCAT, STAGE_SECONDK))
+        }
+
+    def fill_stats(self, stats: WorkloadStats, hdr: _native.DtopkResult) -> None:
+        fill_stats(stats, self.cfg, self.n, hdr)
+        for stage, ns in self.stage_nanos().items():
+            stats.add_stage_nanos(stage, ns)
+
+
+def fill_stats(stats: WorkloadStats, cfg: PipelineConfig, n: int, hdr: _native.DtopkResult) -> None:
+    """Map the device header onto WorkloadStats (core.py:59-93).
+
+    delegate_vector_len / fully_qualified / partially_qualified /
+    concatenated_len follow the reference definitions at the exact threshold
+    (they equal the reference run with skip_last_iteration=False);
+    elements_read / elements_written count what the device actually touched.
+    """
+    k_out = int(hdr.k_out)
+    if cfg.direct_fallback:
+        stats.add_read(2 * n + int(hdr.pool_gt))
+        stats.add_written(k_out)
+    else:
+        dlen = cfg.beta * -(-n // (1 << cfg.alpha))
+        stats.delegate_vector_len = dlen
+        stats.fully_qualified_subranges = int(hdr.fully_qualified)
+        stats.partially_qualified_subranges = int(hdr.partially_qualified)
+        stats.concatenated_len = int(hdr.concatenated_len)
+        pool = int(hdr.pool_gt)
+        sel = 2 * pool if hdr.path == _native.PATH_SELECT else 0
+        stats.add_read(n + dlen + int(hdr.delegate_bucket) + int(hdr.elements_reread) + sel + k_out)
+        stats.add_written(dlen + int(hdr.delegate_bucket) + pool + int(hdr.pool_eq) + k_out)
+    stats.device = {f: getattr(hdr, f) for f, _ in _native.DtopkResult._fields_}
+    stats.device["concat_len_exact"] = int(hdr.concat_skipped_fq) == 0
+
+
+def dr_topk(v, cfg: PipelineConfig, *, stats: WorkloadStats | None = None, exact_stats: bool = False) -> TopKResult:
+    """Top-k of ``v`` under ``cfg`` on the GPU (reference: pipeline.py:172-220).
+
+    ``v``: numpy array / list (reference semantics, results as numpy), or a
+    torch tensor (CPU or CUDA; results on the same device).  uint32 / int32 /
+    float32 keys.  Returns values best-first (non-increasing for
+    ``cfg.largest``), int64 indices with ties broken by lowest index,
+    ``threshold == values[-1]`` and the work counters.
+    """
+    dv = _device.to_device(v)
+    stats = stats if stats is not None else WorkloadStats()
+    plan = DrTopK(dv.n, cfg, dv.code, dv.out_dtype, dv.device, exact_stats=exact_stats)
+    with torch.cuda.device(dv.device):
+        plan.launch(dv.keys)
+        hdr = plan.header()
+    plan.fill_stats(stats, hdr)
+    k_out = int(hdr.k_out)
+    values = plan.values[:k_out]
+    indices = plan.indices[:k_out]
+    threshold = _device.key_to_value(int(hdr.kth_key), dv.code, plan.cfg.largest)
+    return TopKResult(
+        values=_device.to_caller(values, dv.kind),
+        threshold=threshold,
+        stats=stats,
+        indices=_device.to_caller(indices, dv.kind),
+    )
+
+
+# ---------------------------------------------------------------------------
+# stage-inspection mirrors of the reference operators (parity tests)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class QualificationReport:
+    """Outcome of the first top-k (pipeline.py:56-71); tensors on device."""
+
+    selected_values: torch.Tensor
+    selected_tags: torch.Tensor
+    theta: int
+    fully_qualified: torch.Tensor
+    partial_values: torch.Tensor
+    partial_tags: torch.Tensor
+
+
+def first_topk(d, k: int, backend: str = "radix", skip_last: bool = True, *,
+               stats: WorkloadStats | None = None) -> QualificationReport:
+    """Delegate top-k + qualification (pipeline.py:87-116).
+
+    theta comes from the device radix select (``dtopk_kth_largest``); with
+    ``skip_last`` it is relaxed exactly as kernels.radix_topk does
+    (min of delegates >= kth & ~0xFF, kernels.py:161-164).
+    """
+    from .kernels import kth_largest
+
+    vals = d.values if isinstance(d.values, torch.Tensor) else torch.from_numpy(np.asarray(d.values)).cuda()
+    if k > vals.numel():
+        raise InvalidK(f"k={k} exceeds delegate vector length {vals.numel()}")
+    kth = kth_largest(vals, k)
+    theta = kth
+    v64 = vals.to(torch.int64)
+    if skip_last and backend != "bitonic":
+        edge = kth & 0xFFFFFF00
+        theta = int(v64[v64 >= edge].min().item())
+    in_t = v64 >= theta
+    rows = in_t.view(-1, d.beta).sum(dim=1)
+    full = rows == d.beta
+    full_rep = full.repeat_interleave(d.beta)
+    tags = torch.arange(d.subrange_count, device=vals.device, dtype=torch.int64).repeat_interleave(d.beta)
+    partial = in_t & ~full_rep
+    # torch has no uint32 gather kernels: masks are applied to the int64 view
+    return QualificationReport(
+        selected_values=v64[in_t],
+        selected_tags=tags[in_t],
+        theta=int(theta),
+        fully_qualified=torch.nonzero(full).flatten(),
+        partial_values=v64[partial],
+        partial_tags=tags[partial],
+    )
+
+
+def concatenate_filtered(v, report: QualificationReport, alpha: int, *,
+                         stats: WorkloadStats | None = None) -> torch.Tensor:
+    """Elements >= theta of fully qualified subranges, subrange-ascending then
+    scan order (pipeline.py:119-159)."""
+    dv = _device.to_device(v)
+    keys = dv.keys.to(torch.int64)
+    w = 1 << alpha
+    nsub = -(-dv.n // w)
+    fq = torch.zeros(nsub, dtype=torch.bool, device=keys.device)
+    if report.fully_qualified.numel():
+        fq[report.fully_qualified.to(keys.device)] = True
+    member = fq.repeat_interleave(w)[: dv.n]
+    if stats is not None:
+        stats.add_read(int(report.fully_qualified.numel()) * w)
+    out = keys[member & (keys >= report.theta)]
+    if stats is not None:
+        stats.add_written(out.numel())
+    return out

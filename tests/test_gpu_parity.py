@@ -1,0 +1,263 @@
+"""GPU parity: the sm_100a pipeline against the oracle and the reference goldens.
+
+Bar: bit-exact.  Values equal the reference's ``dr_topk`` values; indices equal
+the restated tie rule (kernels._extract_exact on V: keys > kth first, then
+ties by lowest index; ordered key desc, index asc).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2109_08219_b200 as dtopk
+from paper_2109_08219_b200 import data
+
+pytestmark = pytest.mark.gpu
+
+
+def keys_of(host: np.ndarray, largest: bool, oracle_mod) -> np.ndarray:
+    return oracle_mod.to_keys(host, largest)
+
+
+def check_topk(v_dev: torch.Tensor, k: int, oracle_mod, *, largest=True, **cfgkw):
+    """Run dr_topk on device and compare values + indices with the oracle."""
+    cfg = dtopk.PipelineConfig(k=k, largest=largest, **cfgkw)
+    r = dtopk.dr_topk(v_dev, cfg, exact_stats=True)
+    host = v_dev.cpu().numpy()
+    keys = keys_of(host, largest, oracle_mod)
+    ek, ei = oracle_mod.topk_with_indices(keys, k)
+    gi = r.indices.cpu().numpy()
+    gv = r.values.cpu().numpy()
+    np.testing.assert_array_equal(gi, ei)
+    np.testing.assert_array_equal(keys_of(gv, largest, oracle_mod), ek)
+    np.testing.assert_array_equal(gv, host[ei])
+    # values also equal the reference dr_topk restatement (multiset, order)
+    vc = dtopk.validate_config(cfg, host.size)
+    ov, ost = oracle_mod.dr_topk(keys, k, vc.alpha, vc.beta, skip_last=False, direct=vc.direct_fallback)
+    np.testing.assert_array_equal(keys_of(gv, largest, oracle_mod), ov)
+    if not vc.direct_fallback:
+        s = r.stats
+        assert s.delegate_vector_len == ost.delegate_vector_len
+        assert s.fully_qualified_subranges == ost.fully_qualified_subranges
+        assert s.partially_qualified_subranges == ost.partially_qualified_subranges
+        assert s.concatenated_len == ost.concatenated_len
+        assert int(r.stats.device["theta_local"]) == ost.theta
+    return r
+
+
+def test_smoke_entry():
+    import __graft_entry__
+
+    __graft_entry__.smoke()
+
+
+# ---------------------------------------------------------------- delegates
+@pytest.mark.parametrize("alpha", [1, 2, 3, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 16])
+@pytest.mark.parametrize("beta", [1, 2, 3])
+def test_delegates_match_oracle(alpha, beta, oracle_mod, cuda):
+    if beta >= 1 << alpha:
+        pytest.skip("beta must be < 2^alpha")
+    for n, dist in [((1 << 20) + 12345, "uniform"), (1 << 19, "few_distinct"), (300_001, "nd_u32")]:
+        if (1 << alpha) > n:
+            continue
+        v = data.generate(dist, n, seed=alpha * 7 + beta, device=cuda)
+        d = dtopk.extract_delegates(v, alpha, beta)
+        exp = oracle_mod.extract_delegates(v.cpu().numpy(), alpha, beta)
+        np.testing.assert_array_equal(d.values.cpu().numpy(), exp)
+
+
+@pytest.mark.parametrize("beta", [4, 5, 8, 9, 17, 31])
+def test_delegates_large_beta(beta, oracle_mod, cuda):
+    v = data.generate("uniform", 100_003, seed=beta, device=cuda)
+    for alpha in (5, 6, 9):
+        if beta >= 1 << alpha:
+            continue
+        d = dtopk.extract_delegates(v, alpha, beta)
+        np.testing.assert_array_equal(d.values.cpu().numpy(), oracle_mod.extract_delegates(v.cpu().numpy(), alpha, beta))
+
+
+def test_delegate_figure_examples(figure_vector, cuda):
+    # pkg/tests/test_delegate.py:16-31 and :55-61
+    d = dtopk.extract_delegates(torch.from_numpy(figure_vector).to(cuda), 2, 1)
+    assert d.values.cpu().tolist() == [3012, 2313, 3210, 2321]
+    d = dtopk.extract_delegates(figure_vector, 2, 2)
+    assert d.values[4:6].tolist() == [3210, 3000]
+    d = dtopk.extract_delegates(figure_vector, 4, 1)
+    assert d.values.tolist() == [3210]
+    d = dtopk.extract_delegates(np.array([10, 20, 30, 40, 50], dtype=np.uint32), 2, 2)
+    assert d.values.tolist() == [40, 30, 50, 0]
+    assert d.tags.tolist() == [0, 0, 1, 1]
+
+
+# ---------------------------------------------------------------- end to end
+@pytest.mark.parametrize("k", [1, 2, 7, 128, 1000, 4096, 1 << 14, 100_000])
+@pytest.mark.parametrize("dist", ["uniform", "nd_u32", "few_distinct"])
+def test_dr_topk_u32(k, dist, oracle_mod, cuda):
+    v = data.generate(dist, (1 << 21) + 3, seed=k % 97, device=cuda)
+    check_topk(v, k, oracle_mod)
+
+
+@pytest.mark.parametrize("dist", ["ascending", "descending", "all_equal"])
+@pytest.mark.parametrize("k", [1, 300, 1 << 16])
+def test_dr_topk_adversarial(dist, k, oracle_mod, cuda):
+    v = data.generate(dist, 1 << 22, seed=1, device=cuda)
+    check_topk(v, k, oracle_mod)
+
+
+@pytest.mark.parametrize("largest", [True, False])
+@pytest.mark.parametrize("dist", ["normal_f32", "pareto_f32"])
+@pytest.mark.parametrize("beta", [1, 2, 3])
+def test_dr_topk_f32(largest, dist, beta, oracle_mod, cuda):
+    v = data.generate(dist, 1 << 21, seed=beta, device=cuda)
+    check_topk(v, 1024, oracle_mod, largest=largest, beta=beta)
+
+
+def test_dr_topk_f32_signed_zeros_and_specials(oracle_mod, cuda):
+    v = data.generate("normal_f32", 1 << 16, seed=3, device=cuda)
+    v[::5] = 0.0
+    v[::7] = -0.0
+    v[3] = float("inf")
+    v[4] = float("-inf")
+    for largest in (True, False):
+        check_topk(v, 5000, oracle_mod, largest=largest)
+
+
+@pytest.mark.parametrize("largest", [True, False])
+def test_dr_topk_u32_smallest(largest, oracle_mod, cuda):
+    v = data.generate("uniform", 1 << 20, seed=5, device=cuda)
+    check_topk(v, 777, oracle_mod, largest=largest)
+
+
+@pytest.mark.parametrize("alpha", [1, 2, 3, 5, 9, 13, 14, 15, 18])
+@pytest.mark.parametrize("beta", [1, 2, 3, 8, 12])
+def test_dr_topk_manual_alpha_beta(alpha, beta, oracle_mod, cuda):
+    v = data.generate("uniform", (1 << 20) + 5, seed=alpha + beta, device=cuda)
+    check_topk(v, 333, oracle_mod, alpha=alpha, beta=beta, auto_alpha=False)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 17, 100, 1023, 8191, 8192, 8193, 65537])
+def test_dr_topk_small_and_ragged(n, oracle_mod, cuda):
+    v = data.generate("uniform", n, seed=n, device=cuda)
+    for k in sorted({1, max(1, n // 3), n}):
+        check_topk(v, k, oracle_mod)
+
+
+def test_k_equals_n_sorted(oracle_mod, cuda):
+    v = data.generate("uniform", 1024, seed=2, device=cuda)
+    r = check_topk(v, 1024, oracle_mod)
+    np.testing.assert_array_equal(r.values.cpu().numpy(), np.sort(v.cpu().numpy())[::-1])
+
+
+def test_direct_fallback(oracle_mod, cuda):
+    v = data.generate("uniform", 1024, seed=14, device=cuda)
+    r = check_topk(v, 600, oracle_mod, alpha=8, beta=2, auto_alpha=False)
+    assert r.stats.delegate_vector_len == 0
+    assert set(r.stats.per_stage_nanos) == set(dtopk.STAGES)
+
+
+def test_numpy_roundtrip_and_ties(oracle_mod, cuda):
+    # pkg/tests/test_kernels.py:167-171: [9,5,5,5,9,5], k=3 -> [9,9,5], ties in scan order
+    v = np.array([9, 5, 5, 5, 9, 5], dtype=np.uint32)
+    r = dtopk.dr_topk(v, dtopk.PipelineConfig(k=3))
+    assert isinstance(r.values, np.ndarray)
+    assert r.values.tolist() == [9, 9, 5]
+    assert r.indices.tolist() == [0, 4, 1]
+    assert r.threshold == 5
+    # pkg/tests/test_pipeline.py:186-192: duplicated maxima survive filtering
+    v = np.zeros(64, dtype=np.uint32)
+    v[[3, 17, 33, 49, 5, 21]] = 900
+    r = dtopk.dr_topk(v, dtopk.PipelineConfig(k=6, alpha=4, beta=2, auto_alpha=False))
+    assert r.values.tolist() == [900] * 6
+    assert r.indices.tolist() == [3, 5, 17, 21, 33, 49]
+
+
+def test_figure_dr_topk(figure_vector, cuda):
+    # pkg/tests/test_pipeline.py:60-64
+    r = dtopk.dr_topk(figure_vector, dtopk.PipelineConfig(k=2, alpha=2, beta=1, auto_alpha=False))
+    assert r.values.tolist() == [3210, 3012]
+    assert r.threshold == 3012
+    assert r.indices.tolist() == [10, 2]
+
+
+# ---------------------------------------------------------------- reference goldens
+def test_golden_vectors(golden, oracle_mod, cuda):
+    z, meta = golden
+    for m in meta:
+        name, k = m["name"], m["k"]
+        v = z[f"{name}__input"]
+        if m["kind"] == "u32":
+            cfg = dtopk.PipelineConfig(k=k, **m["cfg"])
+            r = dtopk.dr_topk(torch.from_numpy(v).to(cuda), cfg, exact_stats=True)
+            got = r.values.cpu().numpy()
+            np.testing.assert_array_equal(got, z[f"{name}__values_sl1"], err_msg=name)
+            np.testing.assert_array_equal(got, z[f"{name}__values_sl0"], err_msg=name)
+            assert r.threshold == m["threshold_sl1"], name
+            st0 = m["stats_sl0"]
+            assert r.stats.delegate_vector_len == st0["delegate_vector_len"], name
+            if not m["direct"]:
+                assert r.stats.fully_qualified_subranges == st0["fully_qualified_subranges"], name
+                assert r.stats.partially_qualified_subranges == st0["partially_qualified_subranges"], name
+                assert r.stats.concatenated_len == st0["concatenated_len"], name
+                assert int(r.stats.device["theta_local"]) == m["theta_sl0"], name
+                d = dtopk.extract_delegates(v, m["alpha"], m["beta"])
+                np.testing.assert_array_equal(d.values, z[f"{name}__delegates"], err_msg=name)
+        else:
+            r = dtopk.dr_topk(v, dtopk.PipelineConfig(k=k, largest=m["largest"]))
+            exp = z[f"{name}__values_sl1"]
+            np.testing.assert_array_equal(r.values.view(np.uint32), exp.view(np.uint32), err_msg=name)
+
+
+# ---------------------------------------------------------------- stage mirrors
+def test_first_topk_and_concat_mirrors(figure_vector, cuda):
+    # pkg/tests/test_pipeline.py:26-58
+    d = dtopk.extract_delegates(torch.from_numpy(figure_vector).to(cuda), 2, 1)
+    rep = dtopk.first_topk(d, 2, "radix", skip_last=False)
+    assert rep.theta == 3012
+    assert rep.fully_qualified.cpu().tolist() == [0, 2]
+    out = dtopk.concatenate_filtered(torch.from_numpy(figure_vector).to(cuda), rep, 2)
+    assert out.cpu().tolist() == [3012, 3210]
+    d2 = dtopk.extract_delegates(torch.from_numpy(figure_vector).to(cuda), 2, 2)
+    rep = dtopk.first_topk(d2, 3, "radix", skip_last=False)
+    assert rep.theta == 3000
+    assert rep.fully_qualified.cpu().tolist() == [2]
+    assert sorted(rep.partial_values.cpu().tolist()) == [3012]
+
+
+def test_radix_topk_mirror(oracle_mod, cuda):
+    v = data.generate("uniform", 3000, seed=9, device=cuda)
+    sel, _, thr = dtopk.radix_topk(v, 99)
+    exp = np.sort(v.cpu().numpy())[-99:]
+    np.testing.assert_array_equal(np.sort(sel.cpu().numpy()), exp)
+    assert thr == int(exp[0])
+    assert dtopk.kth_largest(v, 99) == int(exp[0])
+
+
+def test_theta_override_split_path(oracle_mod, cuda):
+    """begin/finish with an external theta (the multi-GPU exchange) on one GPU:
+    the two halves of a vector, each filtered with max(theta_0, theta_1)."""
+    from paper_2109_08219_b200.distributed import DeviceOps
+
+    n, k = 1 << 21, 5000
+    v = data.generate("uniform", n, seed=77, device=cuda)
+    ops = DeviceOps()
+    halves = [v[: n // 2], v[n // 2:]]
+    states, thetas = [], []
+    for h in halves:
+        cfg = dtopk.validate_config(dtopk.PipelineConfig(k=k), h.numel())
+        st, th = ops.begin(h, cfg)
+        states.append(st)
+        thetas.append(th)
+    tmax = torch.maximum(thetas[0], thetas[1])
+    outs_v, outs_i = [], []
+    for r, (st, h) in enumerate(zip(states, halves)):
+        vals, idx = ops.finish(st, tmax.clone(), r * (n // 2))
+        outs_v.append(vals)
+        outs_i.append(idx)
+    cat_v = torch.cat(outs_v)
+    cat_i = torch.cat(outs_i)
+    fv, fi = ops.merge(cat_v, cat_i, k, True)
+    ek, ei = oracle_mod.topk_with_indices(v.cpu().numpy(), k)
+    np.testing.assert_array_equal(fi.cpu().numpy(), ei)
+    np.testing.assert_array_equal(fv.cpu().numpy(), ek)
