@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "assemble.cuh"
 #include "delegate.cuh"
 #include "generate.cuh"
 #include "scan.cuh"
@@ -31,10 +32,11 @@ constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 struct Layout {
-  size_t ctrl, lb_k3, lb_k4g, lb_k4e, lb_emg, lb_eme, zero_bytes;
-  size_t D, partial, selbuf, bitmap, cand_sid, cand_d1, cand_dl, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
-      total;
-  u64 S, nch, cap_gt, m_emit, k2_tiles, k3_tiles, k4_tiles, em_tiles, sort_tiles, D_len, words;
+  size_t ctrl, lb_k3, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
+  size_t D, meta, partial, pmeta, selbuf, rec_sid, rec_d1, rec_meta, rec_x, e_sid, t_sid, t_cnt, stg_key, stg_idx,
+      seg_gt, seg_eq, d_rec, d_pos, d_need, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts, total;
+  u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k2_tiles, k3_tiles, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len,
+      nseg;
 };
 
 Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
@@ -46,33 +48,52 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
     return o;
   };
   const u64 W = direct ? 1ull : (1ull << alpha);
+  L.W = W;
   L.nch = (n + K1_CHUNK - 1) / K1_CHUNK;
   L.S = direct ? 0 : (n + W - 1) / W;
   L.D_len = direct ? 0 : (u64)beta * L.S;
   // Elements strictly above theta live in the < k subranges whose max delegate
-  // exceeds theta = kth(D), so the pool never holds more than (k-1) * 2^alpha.
-  L.cap_gt = direct ? 0 : std::min<u64>(n, std::max<u64>(1, k - 1) * W);
+  // exceeds theta = kth(D): the pool and the K4 staging hold <= (k-1) * 2^alpha.
+  const u64 kg = std::max<u64>(1, k - 1);
+  L.cap_gt = direct ? 0 : std::min<u64>(n, kg * W);
+  L.cap_e = direct ? 0 : std::min<u64>(L.S, kg);
+  L.cap_d = direct ? 0 : std::min<u64>(L.S, k);
+  const int lseg = alpha < 13 ? alpha : 13;
+  L.nseg = direct ? 0 : L.cap_e * (W >> lseg);
   L.m_emit = direct ? n : L.cap_gt;
-  L.k2_tiles = (L.S + K2_TILE - 1) / K2_TILE;
-  L.words = (L.S + 31) / 32;
-  L.k3_tiles = (L.words + K3_TILE - 1) / K3_TILE;
-  L.k4_tiles = direct ? 0 : (L.S * W + SC_TILE - 1) / SC_TILE;
+  L.k2_tiles = (L.D_len + 4095) / 4096;
+  L.k3_tiles = (L.S + K3_TILE - 1) / K3_TILE;
+  L.k4_tiles = (L.cap_e * W + K4_TILE - 1) / K4_TILE;
+  L.k5_tiles = (L.S + K5_TILE - 1) / K5_TILE;
   L.em_tiles = (L.m_emit + SC_TILE - 1) / SC_TILE;
   L.sort_tiles = (k + ST_TILE - 1) / ST_TILE;
   L.ctrl = take(sizeof(Ctrl));
   L.lb_k3 = take(L.k3_tiles * 8);
-  L.lb_k4g = take(L.k4_tiles * 8);
-  L.lb_k4e = take(L.k4_tiles * 8);
+  L.lb_k5g = take(L.k5_tiles * 8);
+  L.lb_k5e = take(L.k5_tiles * 8);
   L.lb_emg = take(L.em_tiles * 8);
   L.lb_eme = take(L.em_tiles * 8);
   L.zero_bytes = off;
   L.D = take(L.D_len * 4);
-  L.partial = take((!direct && alpha > K1_LOG_CHUNK) ? (u64)beta * L.nch * 4 : 0);
+  L.meta = take(L.S * 4);
+  const bool parts = !direct && alpha > K1_LOG_CHUNK;
+  L.partial = take(parts ? (u64)beta * L.nch * 4 : 0);
+  L.pmeta = take(parts ? 2 * L.nch * 4 : 0);
   L.selbuf = take(std::max<u64>(L.D_len, L.m_emit) * 4);
-  L.bitmap = take(L.words * 4);
-  L.cand_sid = take(L.S * 4);
-  L.cand_d1 = take(L.S * 4);
-  L.cand_dl = take(L.S * 4);
+  L.rec_sid = take(L.S * 4);
+  L.rec_d1 = take(L.S * 4);
+  L.rec_meta = take(L.S * 4);
+  L.rec_x = take(L.S * 4);
+  L.e_sid = take(L.cap_e * 4);
+  L.t_sid = take(L.S * 4);
+  L.t_cnt = take(L.S * 4);
+  L.stg_key = take(L.cap_e * W * 4);
+  L.stg_idx = take(L.cap_e * W * 8);
+  L.seg_gt = take(L.nseg * 4);
+  L.seg_eq = take(L.nseg * 4);
+  L.d_rec = take(L.cap_d * 4);
+  L.d_pos = take(L.cap_d * 8);
+  L.d_need = take(L.cap_d * 4);
   L.gt_keys = take(L.cap_gt * 4);
   L.gt_idx = take(L.cap_gt * 8);
   L.ties = take(direct ? 0 : k * 8);
@@ -128,7 +149,8 @@ void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch) {
   k1_delegates<MODE, B><<<grid_for(nch, nsm), K1_THREADS, K1_SMEM, s>>>(a);
   counted();
   if (a.alpha > K1_LOG_CHUNK) {
-    k1_merge<B><<<grid_for((a.S + 255) / 256, nsm * 4), 256, 0, s>>>(a.partial, nch, a.alpha, a.S, a.D, a.hist1);
+    k1_merge<B><<<grid_for((a.S + 255) / 256, nsm * 4), 256, 0, s>>>(a.partial, a.pmeta, nch, a.alpha, a.S, a.D,
+                                                                       a.meta, a.hist1);
     counted();
   }
 }
@@ -137,8 +159,16 @@ template <int MODE>
 void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* ws, const Layout& L, cudaStream_t s,
                      int nsm) {
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
-  K1Args a{keys, n, alpha, L.S, D, reinterpret_cast<u32*>(ws + L.partial), ctrl->selD.hist1,
-           alpha <= K1_LOG_CHUNK ? 1 : 0};
+  K1Args a{keys,
+           n,
+           alpha,
+           L.S,
+           D,
+           reinterpret_cast<u32*>(ws + L.partial),
+           ctrl->selD.hist1,
+           alpha <= K1_LOG_CHUNK ? 1 : 0,
+           reinterpret_cast<u32*>(ws + L.meta),
+           reinterpret_cast<u32*>(ws + L.pmeta)};
   switch (beta) {
     case 1: launch_k1<MODE, 1>(a, s, nsm, L.nch); break;
     case 2: launch_k1<MODE, 2>(a, s, nsm, L.nch); break;
@@ -149,7 +179,8 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
     case 7: launch_k1<MODE, 7>(a, s, nsm, L.nch); break;
     case 8: launch_k1<MODE, 8>(a, s, nsm, L.nch); break;
     default:
-      k1_generic<MODE><<<grid_for((L.S + 7) / 8, nsm * 8), 256, 0, s>>>(keys, n, alpha, beta, L.S, D, ctrl->selD.hist1);
+      k1_generic<MODE><<<grid_for((L.S + 7) / 8, nsm * 8), 256, 0, s>>>(
+          keys, n, alpha, beta, L.S, D, reinterpret_cast<u32*>(ws + L.meta), ctrl->selD.hist1);
       counted();
   }
 }
@@ -163,7 +194,7 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   u32* D = reinterpret_cast<u32*>(ws + L.D);
   stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm);
   rec(ev, 1, s);
-  K2Args k2{D, L.S, beta, k, ctrl, reinterpret_cast<u32*>(ws + L.selbuf), reinterpret_cast<u32*>(ws + L.bitmap)};
+  K2Args k2{D, L.S, beta, k, ctrl, reinterpret_cast<u32*>(ws + L.selbuf)};
   k2_scan_delegates<<<grid_for(L.k2_tiles, nsm * 4), 256, 0, s>>>(k2);
   counted();
   k2_pass3<<<grid_for((L.D_len + 4095) / 4096, nsm * 2), 256, 0, s>>>(ctrl, k2.selbuf);
@@ -190,125 +221,141 @@ void run_sort(Ctrl* ctrl, char* ws, const Layout& L, cudaStream_t s, int nsm) {
 }
 
 template <int MODE>
-void run_tail(u64 k, void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L,
+void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ull* m_dev, u64 m_host, int check_path,
+              int direct, void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L,
               cudaStream_t s, int nsm) {
+  // SecondK for pools beyond SMALL_POOL (or the direct path): exact radix select,
+  // ordered emit into the sort buffer, sort, write-out.
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  u32* sak = reinterpret_cast<u32*>(ws + L.sak);
+  u64* sai = reinterpret_cast<u64*>(ws + L.sai);
+  u32* selbuf = reinterpret_cast<u32*>(ws + L.selbuf);
+  const u64 mcap = m_dev ? L.cap_gt : m_host;
+  const int gs = grid_for((mcap + 2047) / 2048, nsm * 4);
+  SelArgs sp{keys_for_emit, m_host, m_dev, ctrl, &ctrl->selP, selbuf, k, check_path};
+  if (direct) {
+    sel_pass1<MODE><<<gs, 256, 0, s>>>(sp);
+    counted();
+    sel_pass2<MODE><<<gs, 256, 0, s>>>(sp);
+    counted();
+  } else {
+    sel_pass1<KM_KEY><<<gs, 256, 0, s>>>(sp);
+    counted();
+    sel_pass2<KM_KEY><<<gs, 256, 0, s>>>(sp);
+    counted();
+  }
+  sel_pass3<<<gs, 256, 0, s>>>(sp);
+  counted();
+  ScanArgs em{};
+  em.keys = keys_for_emit;
+  em.idx_in = idx_for_emit;
+  em.m_host = m_host;
+  em.m_dev = m_dev;
+  em.ctrl = ctrl;
+  em.k = k;
+  em.out_keys = sak;
+  em.out_idx = sai;
+  em.lb_gt = reinterpret_cast<u64*>(ws + L.lb_emg);
+  em.lb_eq = reinterpret_cast<u64*>(ws + L.lb_eme);
+  em.check_path = check_path;
+  em.direct = direct;
+  if (direct)
+    scan_emit<MODE><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
+  else
+    scan_emit<KM_KEY><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
+  counted();
+  if (!direct) {
+    merge_copy<<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
+        ctrl, reinterpret_cast<u32*>(ws + L.gt_keys), reinterpret_cast<u64*>(ws + L.gt_idx),
+        reinterpret_cast<u64*>(ws + L.ties), sak, sai);
+    counted();
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(sort_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SORT * 8);
     attr = true;
   }
-  sort_small<MODE><<<1, 1024, SMALL_SORT * 8, s>>>(ctrl, reinterpret_cast<u32*>(ws + L.sak), reinterpret_cast<u64*>(ws + L.sai),
-                                      reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices),
-                                      (long long)offset);
+  sort_small<MODE><<<1, 1024, SMALL_SORT * 8, s>>>(ctrl, sak, sai, reinterpret_cast<u32*>(out_values),
+                                                   reinterpret_cast<long long*>(out_indices), (long long)offset);
   counted();
-  if (k > (u64)SMALL_SORT) run_sort(ctrl, ws, L, s, nsm);
-  writeout<MODE><<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
-      ctrl, reinterpret_cast<u32*>(ws + L.sak), reinterpret_cast<u64*>(ws + L.sai), reinterpret_cast<u32*>(ws + L.sbk),
-      reinterpret_cast<u64*>(ws + L.sbi), reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices),
-      (long long)offset);
-  counted();
+  if (k > (u64)SMALL_SORT) {
+    run_sort(ctrl, ws, L, s, nsm);
+    writeout<MODE><<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
+        ctrl, sak, sai, reinterpret_cast<u32*>(ws + L.sbk), reinterpret_cast<u64*>(ws + L.sbi),
+        reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices), (long long)offset);
+    counted();
+  }
 }
 
 template <int MODE>
 void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, const int64_t* theta_override,
                 void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L, cudaStream_t s,
                 int nsm, void* const* ev) {
+  (void)flags;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
-  K3Args k3{reinterpret_cast<const u32*>(ws + L.D), L.S, beta, reinterpret_cast<const u32*>(ws + L.bitmap), ctrl,
-            theta_override, reinterpret_cast<u32*>(ws + L.cand_sid), reinterpret_cast<u32*>(ws + L.cand_d1),
-            reinterpret_cast<u32*>(ws + L.cand_dl), reinterpret_cast<u64*>(ws + L.lb_k3)};
+  Records rc{reinterpret_cast<u32*>(ws + L.rec_sid), reinterpret_cast<u32*>(ws + L.rec_d1),
+              reinterpret_cast<u32*>(ws + L.rec_meta), reinterpret_cast<u32*>(ws + L.rec_x)};
+  u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
+  u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);
+  u32* t_cnt = reinterpret_cast<u32*>(ws + L.t_cnt);
+  K3Args k3{reinterpret_cast<const u32*>(ws + L.D), reinterpret_cast<const u32*>(ws + L.meta),
+            L.S, n, alpha, beta, ctrl, theta_override, rc, e_sid, t_sid, L.cap_e,
+            reinterpret_cast<u64*>(ws + L.lb_k3)};
   k3_qualify<<<grid_for(L.k3_tiles, nsm * 4), 256, 0, s>>>(k3);
   counted();
-  u32* gt_keys = reinterpret_cast<u32*>(ws + L.gt_keys);
-  u64* gt_idx = reinterpret_cast<u64*>(ws + L.gt_idx);
-  u64* ties = reinterpret_cast<u64*>(ws + L.ties);
-  u32* sak = reinterpret_cast<u32*>(ws + L.sak);
-  u64* sai = reinterpret_cast<u64*>(ws + L.sai);
-  u32* selbuf = reinterpret_cast<u32*>(ws + L.selbuf);
-
-  ScanArgs k4{};
-  k4.keys = keys;
-  k4.n = n;
-  k4.cand_sid = reinterpret_cast<u32*>(ws + L.cand_sid);
-  k4.cand_d1 = reinterpret_cast<u32*>(ws + L.cand_d1);
-  k4.cand_dl = reinterpret_cast<u32*>(ws + L.cand_dl);
-  k4.alpha = alpha;
-  k4.flags = flags;
-  k4.ctrl = ctrl;
-  k4.k = k;
-  k4.gt_keys = gt_keys;
-  k4.gt_idx = gt_idx;
-  k4.eq_keys = nullptr;
-  k4.eq_idx = ties;
-  k4.lb_gt = reinterpret_cast<u64*>(ws + L.lb_k4g);
-  k4.lb_eq = reinterpret_cast<u64*>(ws + L.lb_k4e);
-  scan_emit<MODE, true><<<grid_for(L.k4_tiles, nsm * 4), 256, 0, s>>>(k4);
+  K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
+            reinterpret_cast<u64*>(ws + L.stg_idx), reinterpret_cast<u32*>(ws + L.seg_gt),
+            reinterpret_cast<u32*>(ws + L.seg_eq), L.cap_e};
+  k4_read<MODE><<<grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4), 256, 0, s>>>(k4);
+  counted();
+  k4t_count<MODE><<<grid_for((L.S + 7) / 8, nsm * 4), 256, 0, s>>>(keys, n, alpha, ctrl, t_sid, t_cnt);
+  counted();
+  K5Args k5{ctrl,
+            rc,
+            n,
+            alpha,
+            k,
+            reinterpret_cast<const u32*>(ws + L.stg_key),
+            reinterpret_cast<const u64*>(ws + L.stg_idx),
+            reinterpret_cast<const u32*>(ws + L.seg_gt),
+            reinterpret_cast<const u32*>(ws + L.seg_eq),
+            t_cnt,
+            reinterpret_cast<u32*>(ws + L.gt_keys),
+            reinterpret_cast<u64*>(ws + L.gt_idx),
+            reinterpret_cast<u64*>(ws + L.ties),
+            reinterpret_cast<u32*>(ws + L.d_rec),
+            reinterpret_cast<u64*>(ws + L.d_pos),
+            reinterpret_cast<u32*>(ws + L.d_need),
+            reinterpret_cast<u64*>(ws + L.lb_k5g),
+            reinterpret_cast<u64*>(ws + L.lb_k5e)};
+  k5_assemble<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
+  counted();
+  k6_ties<MODE><<<grid_for((L.cap_d + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, keys, n, alpha, rc.sid, k5.d_rec,
+                                                                      k5.d_pos, k5.d_need, k5.ties);
   counted();
   rec(ev, 3, s);
-
-  // SecondK, pool larger than k: exact radix select over P_gt, then ordered emit.
-  const int gs = grid_for((L.cap_gt + 2047) / 2048, nsm * 4);
-  SelArgs sp{gt_keys, 0, (const ull*)&ctrl->res.pool_gt, ctrl, &ctrl->selP, selbuf, k, 1};
-  sel_pass1<KM_KEY><<<gs, 256, 0, s>>>(sp);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(finish_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_POOL * 8);
+    attr = true;
+  }
+  finish_small<MODE><<<1, 1024, SMALL_POOL * 8, s>>>(ctrl, k5.gt_keys, k5.gt_idx, k5.ties,
+                                                     reinterpret_cast<u32*>(out_values),
+                                                     reinterpret_cast<long long*>(out_indices), (long long)offset);
   counted();
-  sel_pass2<KM_KEY><<<gs, 256, 0, s>>>(sp);
-  counted();
-  sel_pass3<<<gs, 256, 0, s>>>(sp);
-  counted();
-  ScanArgs em{};
-  em.keys = gt_keys;
-  em.idx_in = gt_idx;
-  em.m_dev = (const ull*)&ctrl->res.pool_gt;
-  em.alpha = 0;
-  em.ctrl = ctrl;
-  em.k = k;
-  em.gt_keys = sak;
-  em.gt_idx = sai;
-  em.eq_keys = sak;
-  em.eq_idx = sai;
-  em.lb_gt = reinterpret_cast<u64*>(ws + L.lb_emg);
-  em.lb_eq = reinterpret_cast<u64*>(ws + L.lb_eme);
-  em.check_path = 1;
-  scan_emit<KM_KEY, false><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
-  counted();
-  // SecondK, pool smaller than k: answer = P_gt ++ first ties at theta.
-  merge_copy<<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(ctrl, gt_keys, gt_idx, ties, sak, sai);
-  counted();
-  run_tail<MODE>(k, out_values, out_indices, offset, ws, L, s, nsm);
+  // pools beyond SMALL_POOL are only possible when the caps allow them
+  if (std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL)
+    big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 1, 0, out_values, out_indices,
+                   offset, ws, L, s, nsm);
   rec(ev, 4, s);
 }
 
 template <int MODE>
 void run_direct(const u32* keys, u64 n, u64 k, void* out_values, int64_t* out_indices, int64_t offset, char* ws,
                 const Layout& L, cudaStream_t s, int nsm, void* const* ev) {
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
-  for (int i = 0; i < 4; i++) rec(ev, i, s);  // pipeline.py:185-186: only SecondK runs
   cudaMemsetAsync(ws, 0, L.zero_bytes, s);
-  u32* selbuf = reinterpret_cast<u32*>(ws + L.selbuf);
-  const int gs = grid_for((n + 2047) / 2048, nsm * 4);
-  SelArgs sd{keys, n, nullptr, ctrl, &ctrl->selP, selbuf, k, 0};
-  sel_pass1<MODE><<<gs, 256, 0, s>>>(sd);
-  counted();
-  sel_pass2<MODE><<<gs, 256, 0, s>>>(sd);
-  counted();
-  sel_pass3<<<gs, 256, 0, s>>>(sd);
-  counted();
-  ScanArgs em{};
-  em.keys = keys;
-  em.m_host = n;
-  em.ctrl = ctrl;
-  em.k = k;
-  em.gt_keys = reinterpret_cast<u32*>(ws + L.sak);
-  em.gt_idx = reinterpret_cast<u64*>(ws + L.sai);
-  em.eq_keys = em.gt_keys;
-  em.eq_idx = em.gt_idx;
-  em.lb_gt = reinterpret_cast<u64*>(ws + L.lb_emg);
-  em.lb_eq = reinterpret_cast<u64*>(ws + L.lb_eme);
-  em.direct = 1;
-  scan_emit<MODE, false><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
-  counted();
-  run_tail<MODE>(k, out_values, out_indices, offset, ws, L, s, nsm);
+  for (int i = 0; i < 4; i++) rec(ev, i, s);  // pipeline.py:185-186: only SecondK runs
+  big_tail<MODE>(k, keys, nullptr, nullptr, n, 0, 1, out_values, out_indices, offset, ws, L, s, nsm);
   rec(ev, 4, s);
 }
 

@@ -82,14 +82,20 @@ struct Ctrl {
   dtopk_result res;   // host-visible header (kept first: dtopk_result_offset() == 0)
   SelectState selD;   // theta = kth(delegates)
   SelectState selP;   // tau = kth(pool) or kth(V) on the direct path
-  // qualification (K3): ordered list of subranges with max delegate >= theta
+  // qualification (K3): ordered records of subranges with max delegate >= theta
   u32 k3_ticket;
-  u32 pad0;
-  ull cand_count;
-  // concatenation scan (K4)
-  u32 k4_ticket;
+  u32 nE;          // class-E records (read by K4)
+  ull cand_count;  // records
+  ull nA;          // class-A records (one element > theta each)
+  ull gt_rec_end;  // 1 + last record index that holds elements > theta
+  ull sumEgt;      // elements > theta found by K4
+  // assembly (K5) and tie location (K6)
+  u32 k5_ticket;
   u32 ties_full;
-  ull k4_tiles;
+  u32 k6_count;
+  u32 small_done;  // finish_small wrote the answer
+  u32 nT;          // class-T records (tie-only, counted by K4T)
+  u32 pad1;
   // emit
   u32 em_ticket;
   u32 maxkey;

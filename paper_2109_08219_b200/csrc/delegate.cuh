@@ -36,7 +36,74 @@ struct K1Args {
   u32* partial;  // [nchunks][B] when alpha > K1_LOG_CHUNK
   ull* hist1;    // global first-digit histogram of D
   int do_hist;
+  u32* meta;     // [S] (min(c1, 0xffff) << 16) | (p1 & 0xffff): count and position of the max
+  u32* pmeta;    // [2 * nchunks] c1 / p1 of the chunk partials (alpha > K1_LOG_CHUNK)
 };
+
+// Per-lane accumulator: top-B ladder, uint4 index p of the running maximum
+// (updated only on a strictly larger uint4 maximum, so it names the first
+// uint4 that holds d_1) and the running minimum (a subrange is constant iff
+// min == max).  Per uint4 and B = 2 this is 13 integer min/max/select ops:
+// pairwise sort, top-2 of the four, merge into the ladder.
+template <int B>
+struct Acc {
+  u32 L[B];
+  u32 p;
+  u32 mn;
+  __device__ __forceinline__ void init(u32 p0) {
+#pragma unroll
+    for (int i = 0; i < B; i++) L[i] = 0;
+    p = p0;
+    mn = 0xffffffffu;
+  }
+};
+
+// x: keys for the ladder (absent = 0), y: keys for the minimum (absent = ~0)
+template <int B>
+__device__ __forceinline__ void acc_keys(Acc<B>& A, const u32 (&x)[4], const u32 (&y)[4], u32 q) {
+  if constexpr (B == 1) {
+    const u32 t1 = max(max(x[0], x[1]), max(x[2], x[3]));
+    A.p = t1 > A.L[0] ? q : A.p;
+    A.L[0] = max(A.L[0], t1);
+  } else if constexpr (B == 2) {
+    const u32 h1 = max(x[0], x[1]), l1 = min(x[0], x[1]);
+    const u32 h2 = max(x[2], x[3]), l2 = min(x[2], x[3]);
+    const u32 t1 = max(h1, h2), t2 = max(min(h1, h2), max(l1, l2));
+    A.p = t1 > A.L[0] ? q : A.p;
+    const u32 n1 = max(A.L[0], t1);
+    const u32 n2 = max(max(min(A.L[0], t1), A.L[1]), t2);
+    A.L[0] = n1;
+    A.L[1] = n2;
+  } else {
+    const u32 t1 = max(max(x[0], x[1]), max(x[2], x[3]));
+    A.p = t1 > A.L[0] ? q : A.p;
+#pragma unroll
+    for (int c = 0; c < 4; c++) ladder_insert<B>(A.L, x[c]);
+  }
+  A.mn = min(A.mn, min(min(y[0], y[1]), min(y[2], y[3])));
+}
+
+template <int B>
+__device__ __forceinline__ void acc_merge(Acc<B>& A, const u32 (&R)[B], u32 rp, u32 rmn) {
+  A.p = R[0] > A.L[0] ? rp : A.p;
+  A.mn = min(A.mn, rmn);
+  ladder_merge<B>(A.L, R);
+}
+
+template <int B>
+__device__ __forceinline__ void acc_shfl(Acc<B>& A, int off) {
+  u32 R[B];
+#pragma unroll
+  for (int i = 0; i < B; i++) R[i] = __shfl_xor_sync(FULL, A.L[i], off);
+  const u32 rp = __shfl_xor_sync(FULL, A.p, off);
+  const u32 rmn = __shfl_xor_sync(FULL, A.mn, off);
+  acc_merge<B>(A, R, rp, rmn);
+}
+
+// meta word of a subrange: bit 31 = constant subrange (every key equals d_1),
+// bits 0..30 = offset of an occurrence of d_1 inside the subrange (exact and
+// unique whenever d_2 < d_1).
+__device__ __forceinline__ u32 pack_meta(bool constant, u32 p1) { return (constant ? 0x80000000u : 0u) | (p1 & 0x7fffffffu); }
 
 // Warp-aggregated shared-memory histogram increment; all 32 lanes must call.
 __device__ __forceinline__ void hist_add_agg(u32* shist, u32 bin, bool pred) {
@@ -61,9 +128,12 @@ __device__ __forceinline__ void store_delegates(u32* D, u64 sid, const u32 (&L)[
 // warp must call (warp-aggregated histogram).
 template <int B>
 __device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 sid, bool leader,
-                                              const u32 (&L)[B]) {
+                                              const u32 (&L)[B], u32 meta) {
   const bool w = leader && sid < a.S;
-  if (w) store_delegates<B>(a.D, sid, L);
+  if (w) {
+    store_delegates<B>(a.D, sid, L);
+    a.meta[sid] = meta;
+  }
   if (a.do_hist) {
 #pragma unroll
     for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, w);
@@ -81,13 +151,36 @@ __device__ __forceinline__ u32 k1_fetch(const K1Args& a, u64 start, u32 e, u32 c
   }
 }
 
+// Insert the four keys of one uint4 at chunk offset e (p1 records chunk
+// offsets).  Absent tail keys (e >= cnt) are zero padded in the ladder --
+// inserting 0 into a zero-initialised ladder is a no-op -- and never counted.
+// Keys of the uint4 at chunk offset e (TAIL: absent keys become 0 for the
+// ladder and ~0 for the minimum).
+template <int MODE, bool TAIL>
+__device__ __forceinline__ void load_keys(const K1Args& a, u64 start, u32 e, u32 cnt, u32 tcnt, const uint4 v,
+                                          u32 (&x)[4], u32 (&y)[4]) {
+  const u32 r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    x[c] = k1_fetch<MODE, TAIL>(a, start, e + c, cnt, tcnt, r[c]);
+    y[c] = (TAIL && e + c >= cnt) ? 0xffffffffu : x[c];
+  }
+}
+
+// Resolve the exact position of d_1 inside the uint4 p (chunk-relative uint4
+// index) by re-reading it from the staged chunk; returns the subrange meta.
 template <int MODE, int B, bool TAIL>
-__device__ __forceinline__ void ladder_uint4(u32 (&L)[B], const K1Args& a, u64 start, u32 e, u32 cnt, u32 tcnt,
-                                             const uint4 v) {
-  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 0, cnt, tcnt, v.x));
-  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 1, cnt, tcnt, v.y));
-  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 2, cnt, tcnt, v.z));
-  ladder_insert<B>(L, k1_fetch<MODE, TAIL>(a, start, e + 3, cnt, tcnt, v.w));
+__device__ __forceinline__ u32 finalize_meta(const K1Args& a, const uint4* st4, u64 start, u32 cnt, u32 tcnt,
+                                             const Acc<B>& A) {
+  u32 x[4], y[4];
+  load_keys<MODE, TAIL>(a, start, A.p * 4u, cnt, tcnt, st4[A.p], x, y);
+  u32 c = 3;
+#pragma unroll
+  for (int i = 3; i >= 0; i--)
+    if (x[i] == A.L[0]) c = (u32)i;
+  const u32 e = A.p * 4u + c;
+  const u64 wmask = (1ull << a.alpha) - 1;
+  return pack_meta(A.mn == A.L[0], (u32)((start + e) & wmask));
 }
 
 // One warp reduces one staged chunk of 2048 keys.  No CTA-wide barrier: the
@@ -106,28 +199,27 @@ __device__ __forceinline__ void k1_warp_chunk(const K1Args& a, const u32* stage,
 #pragma unroll 2
     for (int j = 0; j < 16; j++) {
       const u32 q = (u32)j * 32u + (u32)lane;
-      const uint4 v = st4[q];
-      const u32 e = q * 4u;
+      u32 x[4], y[4];
+      load_keys<MODE, TAIL>(a, start, q * 4u, cnt, tcnt, st4[q], x, y);
       if (alpha == 1) {
         if constexpr (B == 1) {
-          const u32 x0 = k1_fetch<MODE, TAIL>(a, start, e + 0, cnt, tcnt, v.x);
-          const u32 x1 = k1_fetch<MODE, TAIL>(a, start, e + 1, cnt, tcnt, v.y);
-          const u32 x2 = k1_fetch<MODE, TAIL>(a, start, e + 2, cnt, tcnt, v.z);
-          const u32 x3 = k1_fetch<MODE, TAIL>(a, start, e + 3, cnt, tcnt, v.w);
-          const u64 s0 = (start + e) >> 1;
-          u32 L0[1] = {max(x0, x1)};
-          u32 L1[1] = {max(x2, x3)};
-          emit_subrange<1>(a, shist, s0, true, L0);
-          emit_subrange<1>(a, shist, s0 + 1, true, L1);
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const u32 lo = x[2 * h], hi = x[2 * h + 1];
+            u32 L0[1] = {max(lo, hi)};
+            const u32 mn = min(y[2 * h], y[2 * h + 1]);
+            const u32 off = hi > lo ? 1u : 0u;  // first occurrence of the max
+            emit_subrange<1>(a, shist, ((start + q * 4u) >> 1) + h, true, L0, pack_meta(mn == L0[0], off));
+          }
         }
       } else {
-        u32 L[B];
-#pragma unroll
-        for (int i = 0; i < B; i++) L[i] = 0;
-        ladder_uint4<MODE, B, TAIL>(L, a, start, e, cnt, tcnt, v);
+        Acc<B> A;
+        A.init(q);
+        acc_keys<B>(A, x, y, q);
         const int G = 1 << (alpha - 2);
-        for (int off = 1; off < G; off <<= 1) ladder_shfl_merge<B>(L, off);
-        emit_subrange<B>(a, shist, (start + e) >> alpha, (lane & (G - 1)) == 0, L);
+        for (int off = 1; off < G; off <<= 1) acc_shfl<B>(A, off);
+        const u32 meta = finalize_meta<MODE, B, TAIL>(a, st4, start, cnt, tcnt, A);
+        emit_subrange<B>(a, shist, (start + q * 4u) >> alpha, (lane & (G - 1)) == 0, A.L, meta);
       }
     }
     return;
@@ -135,43 +227,59 @@ __device__ __forceinline__ void k1_warp_chunk(const K1Args& a, const u32* stage,
 
   // ---- lane-contiguous: lane owns keys [lane*64, lane*64+64).  LDS.128 order
   // is rotated by lane inside each subrange-aligned group of >= 8 uint4 so a
-  // quarter-warp always hits 8 distinct 16-byte bank groups.
-  const uint4* seg = st4 + lane * 16;
-  const u32 e0 = (u32)lane * 64u;
+  // quarter-warp always hits 8 distinct 16-byte bank groups.  Two accumulators
+  // (even / odd uint4) halve the dependent chain through the ladder.
+  const u32 q0 = (u32)lane * 16u;
   if (alpha == 5) {
 #pragma unroll
     for (int h = 0; h < 2; h++) {
-      u32 L[B];
-#pragma unroll
-      for (int i = 0; i < B; i++) L[i] = 0;
+      Acc<B> A0, A1;
+      A0.init(q0 + h * 8);
+      A1.init(q0 + h * 8);
 #pragma unroll
       for (int jj = 0; jj < 8; jj++) {
-        const int j = (jj + lane) & 7;
-        ladder_uint4<MODE, B, TAIL>(L, a, start, e0 + h * 32 + j * 4, cnt, tcnt, seg[h * 8 + j]);
+        const u32 q = q0 + h * 8 + ((jj + lane) & 7);
+        u32 x[4], y[4];
+        load_keys<MODE, TAIL>(a, start, q * 4u, cnt, tcnt, st4[q], x, y);
+        acc_keys<B>((jj & 1) ? A1 : A0, x, y, q);
       }
-      emit_subrange<B>(a, shist, (start + e0 + h * 32) >> 5, true, L);
+      acc_merge<B>(A0, A1.L, A1.p, A1.mn);
+      const u32 meta = finalize_meta<MODE, B, TAIL>(a, st4, start, cnt, tcnt, A0);
+      emit_subrange<B>(a, shist, (start + (q0 + h * 8) * 4u) >> 5, true, A0.L, meta);
     }
     return;
   }
-  u32 L[B];
-#pragma unroll
-  for (int i = 0; i < B; i++) L[i] = 0;
+  Acc<B> A0, A1;
+  A0.init(q0);
+  A1.init(q0);
 #pragma unroll
   for (int jj = 0; jj < 16; jj++) {
-    const int j = (jj + lane) & 15;
-    ladder_uint4<MODE, B, TAIL>(L, a, start, e0 + j * 4, cnt, tcnt, seg[j]);
+    const u32 q = q0 + ((jj + lane) & 15);
+    u32 x[4], y[4];
+    load_keys<MODE, TAIL>(a, start, q * 4u, cnt, tcnt, st4[q], x, y);
+    acc_keys<B>((jj & 1) ? A1 : A0, x, y, q);
   }
-  if (alpha == 6) {
-    emit_subrange<B>(a, shist, (start + e0) >> 6, true, L);
-    return;
-  }
-  const int G = alpha >= K1_LOG_CHUNK ? 32 : 1 << (alpha - 6);  // lanes per subrange
-  for (int off = 1; off < G; off <<= 1) ladder_shfl_merge<B>(L, off);
+  acc_merge<B>(A0, A1.L, A1.p, A1.mn);
+  const int G = alpha >= K1_LOG_CHUNK ? 32 : 1 << (alpha - 6);  // lanes per subrange (alpha == 6: 1)
+  for (int off = 1; off < G; off <<= 1) acc_shfl<B>(A0, off);
   if (alpha <= K1_LOG_CHUNK) {
-    emit_subrange<B>(a, shist, (start + e0) >> alpha, (lane & (G - 1)) == 0, L);
-  } else if (lane == 0) {
+    const u32 meta = finalize_meta<MODE, B, TAIL>(a, st4, start, cnt, tcnt, A0);
+    emit_subrange<B>(a, shist, (start + q0 * 4u) >> alpha, (lane & (G - 1)) == 0, A0.L, meta);
+  } else {
+    // W > 2048: this chunk is one part of a subrange -> partial ladder + the
+    // exact offset of its max inside the subrange + its minimum
+    u32 x[4], y[4];
+    load_keys<MODE, TAIL>(a, start, A0.p * 4u, cnt, tcnt, st4[A0.p], x, y);
+    u32 cc = 3;
 #pragma unroll
-    for (int i = 0; i < B; i++) a.partial[c * B + i] = L[i];
+    for (int i = 3; i >= 0; i--)
+      if (x[i] == A0.L[0]) cc = (u32)i;
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < B; i++) a.partial[c * B + i] = A0.L[i];
+      a.pmeta[2 * c] = (u32)((start + A0.p * 4u + cc) & ((1ull << alpha) - 1));
+      a.pmeta[2 * c + 1] = A0.mn;
+    }
   }
 }
 
@@ -248,8 +356,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_delegates(K1Args a) {
 
 // Merge per-chunk partial ladders into per-subrange delegates (alpha > 13).
 template <int B>
-__global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial, u64 nch, int alpha, u64 S,
-                                                u32* __restrict__ D, ull* __restrict__ hist1) {
+__global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial, const u32* __restrict__ pmeta,
+                                                u64 nch, int alpha, u64 S, u32* __restrict__ D,
+                                                u32* __restrict__ meta, ull* __restrict__ hist1) {
   __shared__ u32 shist[NB1];
   for (int i = threadIdx.x; i < NB1; i += 256) shist[i] = 0;
   __syncthreads();
@@ -257,19 +366,22 @@ __global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial,
   const u64 stride = (u64)gridDim.x * 256;
   const u64 s_end = (S + 31) & ~31ull;  // keep whole warps in the loop for hist_add_agg
   for (u64 s = (u64)blockIdx.x * 256 + threadIdx.x; s < s_end; s += stride) {
-    u32 L[B];
-#pragma unroll
-    for (int i = 0; i < B; i++) L[i] = 0;
+    Acc<B> A;
+    A.init(0);
     if (s < S) {
       const u64 c_end = min(nch, (s + 1) * cps);
       for (u64 c = s * cps; c < c_end; c++) {
         u32 R[B];
 #pragma unroll
         for (int i = 0; i < B; i++) R[i] = partial[c * B + i];
-        ladder_merge<B>(L, R);
+        acc_merge<B>(A, R, pmeta[2 * c], pmeta[2 * c + 1]);
       }
-      store_delegates<B>(D, s, L);
+      store_delegates<B>(D, s, A.L);
+      meta[s] = pack_meta(A.mn == A.L[0], A.p);
     }
+    u32 L[B];
+#pragma unroll
+    for (int i = 0; i < B; i++) L[i] = A.L[i];
 #pragma unroll
     for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, s < S);
   }
@@ -285,7 +397,8 @@ __global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial,
 // beta-round warp arg-max merge.  Cold path: correctness over speed.
 template <int MODE>
 __global__ void __launch_bounds__(256) k1_generic(const u32* __restrict__ keys, u64 n, int alpha, int beta,
-                                                  u64 S, u32* __restrict__ D, ull* __restrict__ hist1) {
+                                                  u64 S, u32* __restrict__ D, u32* __restrict__ meta,
+                                                  ull* __restrict__ hist1) {
   const int lane = threadIdx.x & 31;
   const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
@@ -305,16 +418,31 @@ __global__ void __launch_bounds__(256) k1_generic(const u32* __restrict__ keys, 
       L[p] = x;
     }
     int ptr = 0;
+    u32 d1 = 0;
     for (int r = 0; r < beta; r++) {
       const u32 head = ptr < beta ? L[ptr] : 0u;
       const u32 m = __reduce_max_sync(FULL, head);
       const u32 win = __ballot_sync(FULL, head == m);
       if (lane == __ffs(win) - 1) ptr++;
+      if (r == 0) d1 = m;
       if (lane == 0) {
         D[s * beta + r] = m;
         atomicAdd(&hist1[m >> 21], 1ull);
       }
     }
+    // position of the first max and constant-subrange flag: second pass (cold path)
+    u32 pos = 0xffffffffu, mn = 0xffffffffu;
+    for (u64 e = lane; e < W; e += 32) {
+      const u64 i = s * W + e;
+      if (i < n) {
+        const u32 x = to_key<MODE>(keys[i]);
+        mn = min(mn, x);
+        if (x == d1) pos = min(pos, (u32)e);
+      }
+    }
+    pos = __reduce_min_sync(FULL, pos);
+    mn = __reduce_min_sync(FULL, mn);
+    if (lane == 0) meta[s] = pack_meta(mn == d1, pos);
   }
 }
 

@@ -1,26 +1,19 @@
-// scan.cuh -- K4 (filtered concatenation) and the ordered emit of the final
-// top-k, both built on one order-preserving compaction kernel.
+// scan.cuh -- ordered emit of the final top-k over a flat key array, the
+// merge copy, the stable radix sort of the answer and its write-out.
 //
-// Reference: pipeline.concatenate_filtered (pipeline.py:119-159) and the
-// tie rule of kernels._extract_exact (kernels.py:83-96): every element
-// strictly above the threshold first, then threshold-equal elements in scan
-// order until k slots are filled.
+// Reference: the tie rule of kernels._extract_exact (kernels.py:83-96) --
+// every element strictly above the k-th key first, then k-th-key ties in scan
+// order until k slots are filled -- and the final np.sort of dr_topk
+// (pipeline.py:215-218), here ordered (key desc, index asc).
 //
-// One tile = 8192 virtual elements = 8 warps x 1024; a warp loads 8 rounds of
+// scan_emit: one tile = 8192 keys = 8 warps x 1024; a warp loads 8 rounds of
 // 32 lanes x uint4 (512 contiguous bytes per instruction).  Phase 1 counts
 // (gt, eq) per thread; the tile publishes its aggregate on two decoupled
 // look-back chains; phase 2 re-derives the predicates from registers and
 // writes every selected element at its stable (index-ordered) position using
-// ballots, so no per-element atomics and no second read are needed.
-//
-// K4 (CAND=true) walks the ordered candidate-subrange list produced by K2 and
-//  * skips subranges whose max delegate is below theta,
-//  * reads subranges with max > theta (elements > theta -> pool P_gt),
-//  * reads tie-only subranges (max == theta) only while the tie buffer (first k
-//    ties in index order) is not yet full -- this keeps all-equal and
-//    few-distinct inputs at ~1 pass instead of the reference's 2-7 passes.
-// emit (CAND=false) walks a flat array (P_gt or the raw input) with the exact
-// k-th key tau and writes the answer's keys/indices into the sort buffer.
+// ballots, so no per-element atomics and no second read are needed.  It runs
+// over the pool P_gt when the pool exceeds k (and SMALL_POOL), and over the
+// raw input on the direct path (pipeline.py:184-191).
 #pragma once
 
 #include "common.cuh"
@@ -31,93 +24,63 @@ constexpr int SC_TILE = 8192;
 
 struct ScanArgs {
   const u32* keys;
-  u64 n;              // CAND: input length
-  const u64* idx_in;  // FLAT: explicit indices (null = position)
-  u64 m_host;         // FLAT: element count
+  const u64* idx_in;  // explicit indices (null = position)
+  u64 m_host;         // element count
   const ull* m_dev;
-  const u32* cand_sid;
-  const u32* cand_d1;
-  const u32* cand_dl;
-  int alpha;
-  const int64_t* theta_override;
-  u32 flags;
   Ctrl* ctrl;
   u64 k;
-  u32* gt_keys;
-  u64* gt_idx;
-  u32* eq_keys;
-  u64* eq_idx;
+  u32* out_keys;      // answer keys/indices (sort buffer A)
+  u64* out_idx;
   u64* lb_gt;
   u64* lb_eq;
   int check_path;
   int direct;
 };
 
-template <int MODE, bool CAND>
+__device__ __forceinline__ bool big_path_skip(const Ctrl* c) { return ld_volatile_u32(&c->small_done) != 0; }
+
+template <int MODE>
 __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
   __shared__ DigitResult r3s;
   __shared__ ull scratch[8];
   __shared__ u32 s_wgt[8], s_weq[8];
   __shared__ u64 s_tile, s_gtx, s_eqx;
-  __shared__ int s_skip;
-  __shared__ ull s_stat[3][8];
   __shared__ u32 s_max[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
-  if (a.check_path && ld_volatile_u32(&ctrl->res.path) != PATH_SELECT) return;
+  if (a.check_path && (ld_volatile_u32(&ctrl->res.path) != PATH_SELECT || big_path_skip(ctrl))) return;
 
-  u32 theta;
-  u64 eq_cap;
-  u32* eqk = a.eq_keys;
-  u64* eqi = a.eq_idx;
-  u32* ticket;
-  if constexpr (CAND) {
-    theta = ctrl->res.theta;  // exact kth(D), or max with an external theta (K3)
-    eq_cap = a.k;
-    ticket = &ctrl->k4_ticket;
-  } else {
-    const DigitResult r1 = ctrl->selP.r1, r2 = ctrl->selP.r2;
-    find_digit<NB3>(ctrl->selP.hist3, r2.rem, &r3s, scratch);
-    theta = (r1.digit << 21) | (r2.digit << 10) | r3s.digit;
-    eq_cap = r3s.rem;
-    const u64 ngt = a.k - eq_cap;
-    eqk += ngt;
-    eqi += ngt;
-    ticket = &ctrl->em_ticket;
-    if (blockIdx.x == 0 && tid == 0) {
-      ctrl->selP.r3 = r3s;
-      ctrl->selP.kth = theta;
-      ctrl->sort_lo = theta;
-      ctrl->res.k_out = a.k;
-      if (a.direct) {
-        ctrl->res.path = PATH_DIRECT;
-        ctrl->res.theta = theta;
-      }
-      atomicMax(&ctrl->maxkey, theta);
+  const DigitResult r1 = ctrl->selP.r1, r2 = ctrl->selP.r2;
+  find_digit<NB3>(ctrl->selP.hist3, r2.rem, &r3s, scratch);
+  const u32 theta = (r1.digit << 21) | (r2.digit << 10) | r3s.digit;
+  const u64 eq_cap = r3s.rem;  // ties needed
+  const u64 ngt = a.k - eq_cap;
+  u32* eqk = a.out_keys + ngt;
+  u64* eqi = a.out_idx + ngt;
+  if (blockIdx.x == 0 && tid == 0) {
+    ctrl->selP.r3 = r3s;
+    ctrl->selP.kth = theta;
+    ctrl->sort_lo = theta;
+    ctrl->res.k_out = a.k;
+    if (a.direct) {
+      ctrl->res.path = PATH_DIRECT;
+      ctrl->res.theta = theta;
+      ctrl->res.pool_gt = ngt;
     }
+    atomicMax(&ctrl->maxkey, theta);
   }
-  const u64 W = 1ull << a.alpha;
-  const u64 P = CAND ? (u64)ctrl->cand_count : 0;
-  const u64 total = CAND ? (P << a.alpha) : (a.m_dev ? (u64)*a.m_dev : a.m_host);
+  const u64 total = a.m_dev ? (u64)*a.m_dev : a.m_host;
   const u64 T = (total + SC_TILE - 1) / SC_TILE;
-  const bool exact = (a.flags & DTOPK_FLAG_EXACT_STATS) != 0;
-
   u32 bmax = 0;
-  ull st_concat = 0, st_skipfq = 0, st_reread = 0;
 
   for (;;) {
-    if (tid == 0) {
-      s_tile = atomicAdd(ticket, 1u);
-      s_skip = CAND && !exact ? (int)ld_volatile_u32(&ctrl->ties_full) : 0;
-    }
+    if (tid == 0) s_tile = atomicAdd(&ctrl->em_ticket, 1u);
     __syncthreads();
     const u64 tile = s_tile;
-    const bool skip_ties = s_skip != 0;
     if (tile >= T) break;
 
     // ---------------- phase 1: load + count
     u32 kv[8][4];
-    u64 pb[8];
     u32 vm[8];
     u32 cgt = 0, ceq = 0;
 #pragma unroll
@@ -125,84 +88,20 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
       const u64 v0 = tile * SC_TILE + (u64)warp * 1024 + (u64)j * 128 + (u64)lane * 4;
       u32 x[4] = {0u, 0u, 0u, 0u};
       u32 valid = 0;
-      u64 base = 0;
-      if constexpr (CAND) {
-        if (a.alpha >= 2) {
-          const u64 ci = v0 >> a.alpha;
-          if (ci < P) {
-            const u32 sid = a.cand_sid[ci];
-            const u32 d1 = a.cand_d1[ci];
-            const u64 off = v0 & (W - 1);
-            base = ((u64)sid << a.alpha) | off;
-            const bool fq = a.cand_dl[ci] >= theta;
-            const bool rd = d1 > theta || (d1 == theta && !skip_ties);
-            if (off == 0 && !rd && fq) st_skipfq++;
-            if (rd) {
-              if (base + 4 <= a.n) {
-                const uint4 q = ld_nc_v4(a.keys + base);
-                x[0] = to_key<MODE>(q.x);
-                x[1] = to_key<MODE>(q.y);
-                x[2] = to_key<MODE>(q.z);
-                x[3] = to_key<MODE>(q.w);
-                valid = 0xfu;
-              } else {
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                  if (base + c < a.n) {
-                    x[c] = to_key<MODE>(a.keys[base + c]);
-                    valid |= 1u << c;
-                  }
-              }
-              st_reread += __popc(valid);
-              if (fq) {
-#pragma unroll
-                for (int c = 0; c < 4; c++) st_concat += ((valid >> c) & 1u) && x[c] >= theta;
-              }
-            }
-          }
-        } else {
-          // alpha == 1: two elements per subrange, handled element-wise
-#pragma unroll
-          for (int c = 0; c < 4; c++) {
-            const u64 v = v0 + c;
-            const u64 ci = v >> 1;
-            if (ci < P) {
-              const u32 sid = a.cand_sid[ci];
-              const u32 d1 = a.cand_d1[ci];
-              const u64 off = v & 1;
-              const u64 phys = ((u64)sid << 1) | off;
-              const bool fq = a.cand_dl[ci] >= theta;
-              const bool rd = d1 > theta || (d1 == theta && !skip_ties);
-              if (off == 0 && !rd && fq) st_skipfq++;
-              if (rd && phys < a.n) {
-                x[c] = to_key<MODE>(a.keys[phys]);
-                valid |= 1u << c;
-                st_reread++;
-                if (fq && x[c] >= theta) st_concat++;
-              }
-              if (c == 0) base = phys;
-              // element-wise indices are rebuilt in phase 2 from the list
-            }
-          }
-        }
+      if (v0 + 4 <= total) {
+        const uint4 q = ld_nc_v4(a.keys + v0);
+        x[0] = to_key<MODE>(q.x);
+        x[1] = to_key<MODE>(q.y);
+        x[2] = to_key<MODE>(q.z);
+        x[3] = to_key<MODE>(q.w);
+        valid = 0xfu;
       } else {
-        const u64 m = total;
-        base = v0;
-        if (v0 + 4 <= m) {
-          const uint4 q = ld_nc_v4(a.keys + v0);
-          x[0] = to_key<MODE>(q.x);
-          x[1] = to_key<MODE>(q.y);
-          x[2] = to_key<MODE>(q.z);
-          x[3] = to_key<MODE>(q.w);
-          valid = 0xfu;
-        } else {
 #pragma unroll
-          for (int c = 0; c < 4; c++)
-            if (v0 + c < m) {
-              x[c] = to_key<MODE>(a.keys[v0 + c]);
-              valid |= 1u << c;
-            }
-        }
+        for (int c = 0; c < 4; c++)
+          if (v0 + c < total) {
+            x[c] = to_key<MODE>(a.keys[v0 + c]);
+            valid |= 1u << c;
+          }
       }
 #pragma unroll
       for (int c = 0; c < 4; c++) {
@@ -214,7 +113,6 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
         kv[j][c] = x[c];
       }
       vm[j] = valid;
-      pb[j] = base;
     }
     const u32 wg = __reduce_add_sync(FULL, cgt), we = __reduce_add_sync(FULL, ceq);
     if (lane == 0) {
@@ -235,26 +133,10 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
       const u64 xg = lb_warp_prefix(a.lb_gt, tile);
       const u64 xe = lb_warp_prefix(a.lb_eq, tile);
       if (lane == 0) {
-      lb_publish_prefix(a.lb_gt, tile, xg + ag);
-      lb_publish_prefix(a.lb_eq, tile, xe + ae);
-      s_gtx = xg;
-      s_eqx = xe;
-      if (CAND && xe + ae >= eq_cap) atomicExch(&ctrl->ties_full, 1u);
-      if (tile == T - 1) {
-        const u64 G = xg + ag, E = xe + ae;
-        if constexpr (CAND) {
-          ctrl->res.pool_gt = G;
-          ctrl->res.pool_eq = min(E, (u64)a.k);
-          if (G >= a.k) {
-            ctrl->res.path = PATH_SELECT;
-          } else {
-            ctrl->res.path = PATH_MERGE;
-            ctrl->res.k_out = min((u64)a.k, G + E);
-            ctrl->sort_lo = theta;
-            atomicMax(&ctrl->maxkey, theta);
-          }
-        }
-      }
+        lb_publish_prefix(a.lb_gt, tile, xg + ag);
+        lb_publish_prefix(a.lb_eq, tile, xe + ae);
+        s_gtx = xg;
+        s_eqx = xe;
       }
     }
     __syncthreads();
@@ -287,28 +169,19 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
           go += __popc(bg[c] & lt);
           eo += __popc(be[c] & lt);
         }
+        const u64 v0 = tile * SC_TILE + (u64)warp * 1024 + (u64)j * 128 + (u64)lane * 4;
 #pragma unroll
         for (int c = 0; c < 4; c++) {
           if (g[c] || e[c]) {
-            u64 idx;
-            if constexpr (CAND) {
-              if (a.alpha >= 2) {
-                idx = pb[j] + c;
-              } else {
-                const u64 v = tile * SC_TILE + (u64)warp * 1024 + (u64)j * 128 + (u64)lane * 4 + c;
-                idx = ((u64)a.cand_sid[v >> 1] << 1) | (v & 1);
-              }
-            } else {
-              idx = a.idx_in ? a.idx_in[pb[j] + c] : pb[j] + c;
-            }
+            const u64 idx = a.idx_in ? a.idx_in[v0 + c] : v0 + c;
             if (g[c]) {
-              a.gt_keys[go] = kv[j][c];
-              a.gt_idx[go] = idx;
+              a.out_keys[go] = kv[j][c];
+              a.out_idx[go] = idx;
               go++;
             }
             if (e[c]) {
               if (eo < eq_cap) {
-                if (eqk) eqk[eo] = kv[j][c];
+                eqk[eo] = kv[j][c];
                 eqi[eo] = idx;
               }
               eo++;
@@ -323,32 +196,13 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
       }
     }
   }
-
-  // ---------------- block-level stats and max
   bmax = __reduce_max_sync(FULL, bmax);
   if (lane == 0) s_max[warp] = bmax;
-  if constexpr (CAND) {
-    ull v[3] = {st_concat, st_skipfq, st_reread};
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(FULL, v[i], o);
-      if (lane == 0) s_stat[i][warp] = v[i];
-    }
-  }
   __syncthreads();
   if (tid == 0) {
     u32 m = 0;
     for (int w = 0; w < 8; w++) m = max(m, s_max[w]);
     if (m) atomicMax(&ctrl->maxkey, m);
-    if constexpr (CAND) {
-      ull t[3] = {0, 0, 0};
-      for (int i = 0; i < 3; i++)
-        for (int w = 0; w < 8; w++) t[i] += s_stat[i][w];
-      if (t[0]) atomicAdd((ull*)&ctrl->res.concatenated_len, t[0]);
-      if (t[1]) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, t[1]);
-      if (t[2]) atomicAdd((ull*)&ctrl->res.elements_reread, t[2]);
-    }
   }
 }
 
@@ -356,7 +210,7 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
 __global__ void __launch_bounds__(256) merge_copy(Ctrl* ctrl, const u32* __restrict__ gk, const u64* __restrict__ gi,
                                                   const u64* __restrict__ ties, u32* __restrict__ ok,
                                                   u64* __restrict__ oi) {
-  if (ld_volatile_u32(&ctrl->res.path) != PATH_MERGE) return;
+  if (ld_volatile_u32(&ctrl->res.path) != PATH_MERGE || big_path_skip(ctrl)) return;
   const u64 G = ctrl->res.pool_gt, kout = ctrl->res.k_out;
   const u32 theta = ctrl->res.theta;
   for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < kout; i += (u64)gridDim.x * 256) {
@@ -385,7 +239,7 @@ __device__ __forceinline__ int sort_bits(const Ctrl* c) {
 }
 
 __device__ __forceinline__ bool big_sort_skip(const Ctrl* c, int pass) {
-  return c->res.k_out <= (ull)SMALL_SORT || pass * 8 >= sort_bits(c);
+  return big_path_skip(c) || c->res.k_out <= (ull)SMALL_SORT || pass * 8 >= sort_bits(c);
 }
 
 __global__ void __launch_bounds__(256) sort_hist(Ctrl* ctrl, const u32* __restrict__ keys, int pass,
@@ -479,7 +333,7 @@ __global__ void __launch_bounds__(256) writeout(Ctrl* ctrl, const u32* __restric
                                                 const u32* __restrict__ kB, const u64* __restrict__ iB,
                                                 u32* __restrict__ ov, long long* __restrict__ oi, long long offset) {
   const u64 ko = ctrl->res.k_out;
-  if (ko <= (u64)SMALL_SORT) return;  // sort_small wrote the answer
+  if (ko <= (u64)SMALL_SORT || big_path_skip(ctrl)) return;  // sort_small / finish_small wrote it
   const int nb = sort_bits(ctrl);
   const int passes = (nb + 7) / 8;
   const u32* ks = (passes & 1) ? kB : kA;
@@ -501,7 +355,7 @@ __global__ void __launch_bounds__(1024) sort_small(Ctrl* ctrl, const u32* __rest
                                                    long long* __restrict__ oi, long long offset) {
   extern __shared__ unsigned long long sk[];  // SMALL_SORT entries (64 KiB, dynamic)
   const u64 ko = ctrl->res.k_out;
-  if (ko > (u64)SMALL_SORT || ko == 0) return;
+  if (ko > (u64)SMALL_SORT || ko == 0 || big_path_skip(ctrl)) return;
   const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
   u32 np = 1;
   while (np < ko) np <<= 1;

@@ -16,8 +16,7 @@
 
 namespace dtopk {
 
-constexpr int K2_TILE = 2048;  // subranges per tile of the delegate scan
-constexpr int K3_TILE = 2048;  // bitmap words (65536 subranges) per qualification tile
+constexpr int K2_TILE = 2048;  // subranges per tile of the delegate scan (256 threads x 8)
 
 struct K2Args {
   const u32* D;
@@ -26,7 +25,6 @@ struct K2Args {
   u64 k;
   Ctrl* ctrl;
   u32* selbuf;
-  u32* bitmap;  // one bit per subrange: max delegate can still reach theta
 };
 
 // Warp-aggregated append of `x` (where pred) to buf[*counter++].
@@ -41,175 +39,57 @@ __device__ __forceinline__ void warp_append(u32* buf, ull* counter, u32 x, bool 
   if (pred) buf[base + __popc(b & lanemask_lt())] = x;
 }
 
-// K2: one pass over D.
-//  * pass 2 of kth(D): histogram of digit 2 for delegates in theta's digit-1
-//    bucket, and compaction of that bucket into selbuf;
-//  * a bitmap of the subranges whose max delegate can still reach theta
-//    (digit1(d_1) >= digit1(theta)), consumed by K3 once theta is exact.
+// K2: pass 2 of kth(D) -- one read of D: histogram of digit 2 for the
+// delegates in theta's digit-1 bucket and compaction of that bucket into
+// selbuf (one global atomic per tile reserves the block's slots).
 __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
   __shared__ u32 shist[NB2];
   __shared__ DigitResult r1;
   __shared__ ull scratch[8];
+  __shared__ u32 s_wcnt[8];
+  __shared__ ull s_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < NB2; i += 256) shist[i] = 0;
   find_digit<NB1>(a.ctrl->selD.hist1, a.k, &r1, scratch);
   if (blockIdx.x == 0 && tid == 0) a.ctrl->selD.r1 = r1;
   const u32 b1 = r1.digit;
-  const u64 T = (a.S + K2_TILE - 1) / K2_TILE;
-  const int beta = a.beta;
-
+  const u64 nD = a.S * (u64)a.beta;
+  const u64 T = (nD + 256 * 16 - 1) / (256 * 16);
+  const u32 lt = lanemask_lt();
   for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
-    const u64 base = tile * K2_TILE + (u64)warp * 256;
-#pragma unroll 2
-    for (int j = 0; j < 8; j++) {
-      const u64 sid = base + (u64)j * 32 + lane;
-      const bool ok = sid < a.S;
-      u32 d1 = 0;
-      if (beta == 2) {
-        u32 dl = 0;
-        if (ok) {
-          const uint2 v = *reinterpret_cast<const uint2*>(a.D + sid * 2);
-          d1 = v.x;
-          dl = v.y;
-        }
-        const bool p1 = ok && dig1(d1) == b1, p2 = ok && dig1(dl) == b1;
-        if (p1) atomicAdd(&shist[dig2(d1)], 1u);
-        if (p2) atomicAdd(&shist[dig2(dl)], 1u);
-        warp_append(a.selbuf, &a.ctrl->selD.buf_count, d1, p1);
-        warp_append(a.selbuf, &a.ctrl->selD.buf_count, dl, p2);
-      } else {
-        for (int i = 0; i < beta; i++) {
-          const u32 d = ok ? a.D[sid * beta + i] : 0u;
-          if (i == 0) d1 = d;
-          const bool p = ok && dig1(d) == b1;
-          if (p) atomicAdd(&shist[dig2(d)], 1u);
-          warp_append(a.selbuf, &a.ctrl->selD.buf_count, d, p);
-        }
-      }
-      const u32 word = __ballot_sync(FULL, ok && dig1(d1) >= b1);
-      if (lane == 0 && base + (u64)j * 32 < a.S) a.bitmap[(base >> 5) + j] = word;
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < NB2; i += 256) {
-    const u32 v = shist[i];
-    if (v) atomicAdd(&a.ctrl->selD.hist2[i], (ull)v);
-  }
-}
-
-struct K3Args {
-  const u32* D;
-  u64 S;
-  int beta;
-  const u32* bitmap;
-  Ctrl* ctrl;
-  const int64_t* theta_override;
-  u32* q_sid;
-  u32* q_d1;
-  u32* q_dl;
-  u64* lb;
-};
-
-// K3 (qualification, pipeline.py:104-116 without bincount): with the exact
-// theta, keep the subranges whose max delegate d_1 >= theta, in subrange order
-// (ordered compaction with decoupled look-back); count fully qualified
-// (d_beta >= theta) and partially qualified (d_1 >= theta > d_beta) ones.
-__global__ void __launch_bounds__(256) k3_qualify(K3Args a) {
-  __shared__ u32 s_wcnt[8];
-  __shared__ u64 s_tile, s_prefix;
-  __shared__ ull s_stat[3][8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  Ctrl* ctrl = a.ctrl;
-  u32 theta = ctrl->selD.kth;
-  if (a.theta_override) {
-    const long long o = *a.theta_override;
-    const u32 ov = o < 0 ? 0u : (o > 0xffffffffll ? 0xffffffffu : (u32)o);
-    theta = max(theta, ov);
-  }
-  if (blockIdx.x == 0 && tid == 0) ctrl->res.theta = theta;
-  const u64 nwords = (a.S + 31) / 32;
-  const u64 T = (nwords + K3_TILE - 1) / K3_TILE;
-  const int beta = a.beta;
-  ull st_cand = 0, st_fq = 0, st_pq = 0;
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(&ctrl->k3_ticket, 1u);
-    __syncthreads();
-    const u64 tile = s_tile;
-    if (tile >= T) break;
-    const u64 wbase = tile * K3_TILE + (u64)warp * 256;
-    u32 q[8];
+    // each warp owns 512 consecutive delegates, read as 16 coalesced rounds
+    const u64 base = tile * (256 * 16) + (u64)warp * 512;
+    u32 v[16], bl[16];
     u32 cnt = 0;
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const u64 w = wbase + (u64)j * 32 + lane;
-      u32 bits = w < nwords ? a.bitmap[w] : 0u;
-      u32 keep = 0;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const u64 sid = w * 32 + b;
-        const u32 d1 = a.D[sid * beta];
-        if (d1 >= theta) {
-          keep |= 1u << b;
-          const u32 dl = a.D[sid * beta + beta - 1];
-          st_cand++;
-          if (dl >= theta) st_fq++; else st_pq++;
-        }
-      }
-      q[j] = keep;
-      cnt += __popc(keep);
+    for (int j = 0; j < 16; j++) {
+      const u64 i = base + (u64)j * 32 + lane;
+      v[j] = i < nD ? a.D[i] : 0u;
+      const bool p = i < nD && dig1(v[j]) == b1;
+      bl[j] = __ballot_sync(FULL, p);
+      cnt += __popc(bl[j]);
+      if (p) atomicAdd(&shist[dig2(v[j])], 1u);
     }
-    const u32 wsum = __reduce_add_sync(FULL, cnt);
-    if (lane == 0) s_wcnt[warp] = wsum;
+    if (lane == 0) s_wcnt[warp] = cnt;
     __syncthreads();
-    if (warp == 0) {
-      u64 agg = 0;
-      for (int w2 = 0; w2 < 8; w2++) agg += s_wcnt[w2];
-      if (lane == 0) lb_publish_agg(a.lb, tile, agg);
-      const u64 excl = lb_warp_prefix(a.lb, tile);
-      if (lane == 0) {
-        lb_publish_prefix(a.lb, tile, excl + agg);
-        s_prefix = excl;
-        if (tile == T - 1) ctrl->cand_count = excl + agg;
-      }
+    if (tid == 0) {
+      u32 tot = 0;
+      for (int w = 0; w < 8; w++) tot += s_wcnt[w];
+      s_base = tot ? atomicAdd(&a.ctrl->selD.buf_count, (ull)tot) : 0ull;
     }
     __syncthreads();
-    u64 pos = s_prefix;
-    for (int w2 = 0; w2 < warp; w2++) pos += s_wcnt[w2];
-    // order inside the warp: round j, then lane, then bit
+    u64 o = s_base;
+    for (int w = 0; w < warp; w++) o += s_wcnt[w];
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const u32 c = __popc(q[j]);
-      const u32 incl = warp_incl_scan<u32>(c);
-      u64 o = pos + incl - c;
-      u32 bits = q[j];
-      const u64 w = wbase + (u64)j * 32 + lane;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const u64 sid = w * 32 + b;
-        a.q_sid[o] = (u32)sid;
-        a.q_d1[o] = a.D[sid * beta];
-        a.q_dl[o] = a.D[sid * beta + beta - 1];
-        o++;
-      }
-      pos += __shfl_sync(FULL, incl, 31);
+    for (int j = 0; j < 16; j++) {
+      if ((bl[j] >> lane) & 1u) a.selbuf[o + __popc(bl[j] & lt)] = v[j];
+      o += __popc(bl[j]);
     }
+    __syncthreads();
   }
-  ull v[3] = {st_cand, st_fq, st_pq};
-#pragma unroll
-  for (int i = 0; i < 3; i++) {
-    v[i] = __reduce_add_sync(FULL, (u32)v[i]);
-    if (lane == 0) s_stat[i][warp] = v[i];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    ull t[3] = {0, 0, 0};
-    for (int i = 0; i < 3; i++)
-      for (int w2 = 0; w2 < 8; w2++) t[i] += s_stat[i][w2];
-    if (t[0]) atomicAdd((ull*)&ctrl->res.candidate_subranges, t[0]);
-    if (t[1]) atomicAdd((ull*)&ctrl->res.fully_qualified, t[1]);
-    if (t[2]) atomicAdd((ull*)&ctrl->res.partially_qualified, t[2]);
+  for (int i = tid; i < NB2; i += 256) {
+    const u32 c = shist[i];
+    if (c) atomicAdd(&a.ctrl->selD.hist2[i], (ull)c);
   }
 }
 
@@ -270,7 +150,8 @@ struct SelArgs {
 };
 
 __device__ __forceinline__ bool sel_skip(const SelArgs& a) {
-  return a.check_path && ld_volatile_u32(&a.ctrl->res.path) != PATH_SELECT;
+  return a.check_path &&
+         (ld_volatile_u32(&a.ctrl->res.path) != PATH_SELECT || ld_volatile_u32(&a.ctrl->small_done) != 0);
 }
 __device__ __forceinline__ u64 sel_count(const SelArgs& a) { return a.m_dev ? (u64)*a.m_dev : a.m_host; }
 
