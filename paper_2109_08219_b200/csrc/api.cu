@@ -31,12 +31,16 @@ inline void counted(int n = 1) { g_launches.fetch_add((unsigned long long)n, std
 constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
+int num_sms();
+
 struct Layout {
-  size_t ctrl, lb_k3, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
-  size_t D, meta, partial, pmeta, selbuf, rec_sid, rec_d1, rec_meta, rec_x, e_sid, t_sid, t_cnt, stg_key, stg_idx,
-      seg_gt, seg_eq, d_rec, d_pos, d_need, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts, total;
-  u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k2_tiles, k3_tiles, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len,
-      nseg;
+  size_t ctrl, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
+  size_t D, meta, partial, pmeta, selbuf, region_cnt, keepw, rec_sid, rec_d1, rec_meta, rec_x, e_sid, t_sid, t_cnt,
+      stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
+      digit_base, digit_tot, total;
+  u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
+      sort_cap;
+  u32 g2;
 };
 
 Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
@@ -61,14 +65,18 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   const int lseg = alpha < 13 ? alpha : 13;
   L.nseg = direct ? 0 : L.cap_e * (W >> lseg);
   L.m_emit = direct ? n : L.cap_gt;
-  L.k2_tiles = (L.D_len + 4095) / 4096;
-  L.k3_tiles = (L.S + K3_TILE - 1) / K3_TILE;
+  L.words = (L.S + 31) / 32;
+  // K2 regions: one contiguous range of D per CTA
+  const u64 g2 = std::max<u64>(1, std::min<u64>((u64)num_sms() * 4, (L.D_len + 4095) / 4096));
+  L.g2 = (u32)g2;
+  L.R2 = ((L.D_len + g2 - 1) / g2 + 511) / 512 * 512;
   L.k4_tiles = (L.cap_e * W + K4_TILE - 1) / K4_TILE;
-  L.k5_tiles = (L.S + K5_TILE - 1) / K5_TILE;
+  L.k5_tiles = (L.words + K5_TILE - 1) / K5_TILE;
   L.em_tiles = (L.m_emit + SC_TILE - 1) / SC_TILE;
-  L.sort_tiles = (k + ST_TILE - 1) / ST_TILE;
+  // largest sort: the answer (k), or a pool of up to 4k kept whole (BIG_SORT_POOL)
+  L.sort_cap = direct ? k : std::max<u64>(k, std::min<u64>(4 * k, L.cap_gt));
+  L.sort_tiles = (L.sort_cap + ST_TILE - 1) / ST_TILE;
   L.ctrl = take(sizeof(Ctrl));
-  L.lb_k3 = take(L.k3_tiles * 8);
   L.lb_k5g = take(L.k5_tiles * 8);
   L.lb_k5e = take(L.k5_tiles * 8);
   L.lb_emg = take(L.em_tiles * 8);
@@ -79,7 +87,9 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   const bool parts = !direct && alpha > K1_LOG_CHUNK;
   L.partial = take(parts ? (u64)beta * L.nch * 4 : 0);
   L.pmeta = take(parts ? 2 * L.nch * 4 : 0);
-  L.selbuf = take(std::max<u64>(L.D_len, L.m_emit) * 4);
+  L.selbuf = take(std::max<u64>((u64)L.g2 * L.R2, L.m_emit) * 4);
+  L.region_cnt = take((u64)L.g2 * 4);
+  L.keepw = take(L.words * 4);
   L.rec_sid = take(L.S * 4);
   L.rec_d1 = take(L.S * 4);
   L.rec_meta = take(L.S * 4);
@@ -91,20 +101,23 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.stg_idx = take(L.cap_e * W * 8);
   L.seg_gt = take(L.nseg * 4);
   L.seg_eq = take(L.nseg * 4);
-  L.d_rec = take(L.cap_d * 4);
+  L.d_sid = take(L.cap_d * 4);
   L.d_pos = take(L.cap_d * 8);
   L.d_need = take(L.cap_d * 4);
   L.gt_keys = take(L.cap_gt * 4);
   L.gt_idx = take(L.cap_gt * 8);
   L.ties = take(direct ? 0 : k * 8);
-  L.sak = take(k * 4);
-  L.sai = take(k * 8);
-  L.sbk = take(k * 4);
-  L.sbi = take(k * 8);
+  L.sak = take(direct ? k * 4 : 0);
+  L.sai = take(direct ? k * 8 : 0);
+  L.sbk = take(L.sort_cap * 4);
+  L.sbi = take(L.sort_cap * 8);
   L.counts = take(L.sort_tiles * 256 * 4);
+  L.digit_base = take(256 * 4);
+  L.digit_tot = take(256 * 4);
   L.total = off;
   return L;
 }
+
 
 int num_sms() {
   static int cache[64] = {0};
@@ -194,45 +207,58 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   u32* D = reinterpret_cast<u32*>(ws + L.D);
   stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm);
   rec(ev, 1, s);
-  K2Args k2{D, L.S, beta, k, ctrl, reinterpret_cast<u32*>(ws + L.selbuf)};
-  k2_scan_delegates<<<grid_for(L.k2_tiles, nsm * 4), 256, 0, s>>>(k2);
+  K2Args k2{D, L.D_len, k, ctrl, reinterpret_cast<u32*>(ws + L.selbuf), reinterpret_cast<u32*>(ws + L.region_cnt),
+            L.R2};
+  k2_scan_delegates<<<L.g2, 256, 0, s>>>(k2);
   counted();
-  k2_pass3<<<grid_for((L.D_len + 4095) / 4096, nsm * 2), 256, 0, s>>>(ctrl, k2.selbuf);
+  k2_pass3<<<grid_for(L.g2, nsm * 2), 256, 0, s>>>(ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2);
   counted();
   rec(ev, 2, s);
 }
 
-void run_sort(Ctrl* ctrl, char* ws, const Layout& L, cudaStream_t s, int nsm) {
-  u32* ka = reinterpret_cast<u32*>(ws + L.sak);
-  u64* ia = reinterpret_cast<u64*>(ws + L.sai);
-  u32* kb = reinterpret_cast<u32*>(ws + L.sbk);
-  u64* ib = reinterpret_cast<u64*>(ws + L.sbi);
-  u32* counts = reinterpret_cast<u32*>(ws + L.counts);
+SortBufs sort_bufs(char* ws, const Layout& L, bool direct) {
+  SortBufs b;
+  b.ka = reinterpret_cast<u32*>(ws + (direct ? L.sak : L.gt_keys));
+  b.ia = reinterpret_cast<u64*>(ws + (direct ? L.sai : L.gt_idx));
+  b.kb = reinterpret_cast<u32*>(ws + L.sbk);
+  b.ib = reinterpret_cast<u64*>(ws + L.sbi);
+  b.counts = reinterpret_cast<u32*>(ws + L.counts);
+  b.digit_base = reinterpret_cast<u32*>(ws + L.digit_base);
+  b.digit_tot = reinterpret_cast<u32*>(ws + L.digit_tot);
+  return b;
+}
+
+void run_sort(Ctrl* ctrl, const SortBufs& b, const Layout& L, cudaStream_t s, int nsm) {
   const int g = grid_for(L.sort_tiles, nsm * 4);
   for (int p = 0; p < 4; p++) {
-    const bool even = (p & 1) == 0;
-    sort_hist<<<g, 256, 0, s>>>(ctrl, even ? ka : kb, p, counts);
+    sort_hist<<<g, 256, 0, s>>>(ctrl, b, p);
     counted();
-    sort_scan<<<1, 256, 0, s>>>(ctrl, p, counts);
+    sort_scan<<<32, 256, 0, s>>>(ctrl, b, p);
     counted();
-    sort_scatter<<<g, 256, 0, s>>>(ctrl, p, even ? ka : kb, even ? ia : ib, even ? kb : ka, even ? ib : ia, counts);
+    sort_scatter<<<g, 256, 0, s>>>(ctrl, b, p);
     counted();
   }
 }
 
 template <int MODE>
-void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ull* m_dev, u64 m_host, int check_path,
-              int direct, void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L,
-              cudaStream_t s, int nsm) {
-  // SecondK for pools beyond SMALL_POOL (or the direct path): exact radix select,
-  // ordered emit into the sort buffer, sort, write-out.
+void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ull* m_dev, u64 m_host, int direct,
+              void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L, cudaStream_t s,
+              int nsm) {
+  // SecondK beyond SMALL_POOL (or the direct path): merge / sort the pool /
+  // exact radix select + ordered emit, then the stable sort and write-out.
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
-  u32* sak = reinterpret_cast<u32*>(ws + L.sak);
-  u64* sai = reinterpret_cast<u64*>(ws + L.sai);
+  const SortBufs sb = sort_bufs(ws, L, direct != 0);
   u32* selbuf = reinterpret_cast<u32*>(ws + L.selbuf);
+  if (!direct) {
+    tail_decide<<<1, 1, 0, s>>>(ctrl, k);
+    counted();
+    merge_append<<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(ctrl, sb.ka, sb.ia,
+                                                                     reinterpret_cast<u64*>(ws + L.ties));
+    counted();
+  }
   const u64 mcap = m_dev ? L.cap_gt : m_host;
   const int gs = grid_for((mcap + 2047) / 2048, nsm * 4);
-  SelArgs sp{keys_for_emit, m_host, m_dev, ctrl, &ctrl->selP, selbuf, k, check_path};
+  SelArgs sp{keys_for_emit, m_host, m_dev, ctrl, &ctrl->selP, selbuf, k, direct ? 0 : 1};
   if (direct) {
     sel_pass1<MODE><<<gs, 256, 0, s>>>(sp);
     counted();
@@ -253,36 +279,29 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
   em.m_dev = m_dev;
   em.ctrl = ctrl;
   em.k = k;
-  em.out_keys = sak;
-  em.out_idx = sai;
+  em.out_keys = direct ? sb.ka : sb.kb;
+  em.out_idx = direct ? sb.ia : sb.ib;
   em.lb_gt = reinterpret_cast<u64*>(ws + L.lb_emg);
   em.lb_eq = reinterpret_cast<u64*>(ws + L.lb_eme);
-  em.check_path = check_path;
+  em.check_path = direct ? 0 : 1;
   em.direct = direct;
   if (direct)
     scan_emit<MODE><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
   else
     scan_emit<KM_KEY><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
   counted();
-  if (!direct) {
-    merge_copy<<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
-        ctrl, reinterpret_cast<u32*>(ws + L.gt_keys), reinterpret_cast<u64*>(ws + L.gt_idx),
-        reinterpret_cast<u64*>(ws + L.ties), sak, sai);
-    counted();
-  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(sort_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SORT * 8);
     attr = true;
   }
-  sort_small<MODE><<<1, 1024, SMALL_SORT * 8, s>>>(ctrl, sak, sai, reinterpret_cast<u32*>(out_values),
+  sort_small<MODE><<<1, 1024, SMALL_SORT * 8, s>>>(ctrl, sb, reinterpret_cast<u32*>(out_values),
                                                    reinterpret_cast<long long*>(out_indices), (long long)offset);
   counted();
-  if (k > (u64)SMALL_SORT) {
-    run_sort(ctrl, ws, L, s, nsm);
+  if (L.sort_cap > (u64)SMALL_SORT) {
+    run_sort(ctrl, sb, L, s, nsm);
     writeout<MODE><<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
-        ctrl, sak, sai, reinterpret_cast<u32*>(ws + L.sbk), reinterpret_cast<u64*>(ws + L.sbi),
-        reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices), (long long)offset);
+        ctrl, sb, reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices), (long long)offset);
     counted();
   }
 }
@@ -298,10 +317,10 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
   u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);
   u32* t_cnt = reinterpret_cast<u32*>(ws + L.t_cnt);
+  u32* keepw = reinterpret_cast<u32*>(ws + L.keepw);
   K3Args k3{reinterpret_cast<const u32*>(ws + L.D), reinterpret_cast<const u32*>(ws + L.meta),
-            L.S, n, alpha, beta, ctrl, theta_override, rc, e_sid, t_sid, L.cap_e,
-            reinterpret_cast<u64*>(ws + L.lb_k3)};
-  k3_qualify<<<grid_for(L.k3_tiles, nsm * 4), 256, 0, s>>>(k3);
+            L.S, n, alpha, beta, ctrl, theta_override, rc, keepw, e_sid, t_sid, L.cap_e};
+  k3_classify<<<grid_for((L.words + 31) / 32, nsm * 8), 256, 0, s>>>(k3);
   counted();
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
             reinterpret_cast<u64*>(ws + L.stg_idx), reinterpret_cast<u32*>(ws + L.seg_gt),
@@ -312,6 +331,8 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   counted();
   K5Args k5{ctrl,
             rc,
+            keepw,
+            L.S,
             n,
             alpha,
             k,
@@ -323,15 +344,15 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
             reinterpret_cast<u32*>(ws + L.gt_keys),
             reinterpret_cast<u64*>(ws + L.gt_idx),
             reinterpret_cast<u64*>(ws + L.ties),
-            reinterpret_cast<u32*>(ws + L.d_rec),
+            reinterpret_cast<u32*>(ws + L.d_sid),
             reinterpret_cast<u64*>(ws + L.d_pos),
             reinterpret_cast<u32*>(ws + L.d_need),
             reinterpret_cast<u64*>(ws + L.lb_k5g),
             reinterpret_cast<u64*>(ws + L.lb_k5e)};
   k5_assemble<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
   counted();
-  k6_ties<MODE><<<grid_for((L.cap_d + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, keys, n, alpha, rc.sid, k5.d_rec,
-                                                                      k5.d_pos, k5.d_need, k5.ties);
+  k6_ties<MODE><<<grid_for((L.cap_d + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, keys, n, alpha, k5.d_sid, k5.d_pos,
+                                                                      k5.d_need, k5.ties);
   counted();
   rec(ev, 3, s);
   static bool attr = false;
@@ -345,7 +366,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   counted();
   // pools beyond SMALL_POOL are only possible when the caps allow them
   if (std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL)
-    big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 1, 0, out_values, out_indices,
+    big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices,
                    offset, ws, L, s, nsm);
   rec(ev, 4, s);
 }
@@ -355,7 +376,7 @@ void run_direct(const u32* keys, u64 n, u64 k, void* out_values, int64_t* out_in
                 const Layout& L, cudaStream_t s, int nsm, void* const* ev) {
   cudaMemsetAsync(ws, 0, L.zero_bytes, s);
   for (int i = 0; i < 4; i++) rec(ev, i, s);  // pipeline.py:185-186: only SecondK runs
-  big_tail<MODE>(k, keys, nullptr, nullptr, n, 0, 1, out_values, out_indices, offset, ws, L, s, nsm);
+  big_tail<MODE>(k, keys, nullptr, nullptr, n, 1, out_values, out_indices, offset, ws, L, s, nsm);
   rec(ev, 4, s);
 }
 

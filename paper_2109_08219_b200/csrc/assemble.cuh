@@ -19,13 +19,15 @@
 // qualified subranges), so the concatenation re-reads only the fully qualified
 // ones; all-equal keys make every candidate C and nothing is re-read.
 //
-//   K3  ordered compaction of the candidate records (decoupled look-back over
-//       tiles of 8192 subranges), class statistics (FQ / PQ).
+//   K3  classification, fully parallel: warp per 32 subranges; the records of
+//       the qualifying subranges of a 32-subrange word are stored compacted at
+//       the start of that word's 32 slots, plus the word's keep mask.
 //   K4  reads the E candidates; each candidate part (<= 8192 keys) writes its
 //       elements > theta and its ties, in index order, into a private staging
 //       slot -- no global ordering needed.
-//   K5  ordered scan over the records (gt, eq counts) -> positions in the pool
-//       P_gt (index order) and in the tie list (first k, index order).
+//   K5  ordered scan over the words (decoupled look-back over tiles of 2048
+//       words) -> positions in the pool P_gt (index order) and in the tie
+//       list (first k, index order).
 //   K6  locates the ties of class-D records that fall among the first k ties.
 #pragma once
 
@@ -35,11 +37,10 @@ namespace dtopk {
 
 enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4 };
 
-constexpr int K3_TILE = 8192;   // subranges per K3 tile (8 warps x 32 steps x 32 lanes)
 constexpr int K4_TILE = 8192;   // keys per K4 tile
-constexpr int K5_PER = 16;      // records per K5 thread
-constexpr int K5_TILE = 256 * K5_PER;
-constexpr int SMALL_POOL = 16384;  // pools up to this size are finished by one CTA
+constexpr int K5_WPT = 8;       // words (32 subranges each) per K5 thread
+constexpr int K5_TILE = 256 * K5_WPT;
+constexpr int SMALL_POOL = 8192;  // pools up to this size are finished by one CTA (8 keys per thread)
 
 struct Records {
   u32* sid;
@@ -58,10 +59,10 @@ struct K3Args {
   Ctrl* ctrl;
   const int64_t* theta_override;
   Records rec;
+  u32* keepw;  // [S/32] keep mask of every 32-subrange word
   u32* e_sid;  // [nE] subrange of each E candidate
   u32* t_sid;  // [nT] subrange of each T candidate
   u64 cap_e;
-  u64* lb;
 };
 
 __device__ __forceinline__ u64 sub_len(u64 sid, u64 n, int alpha) {
@@ -81,11 +82,10 @@ __device__ __forceinline__ u32 classify(u32 d1, u32 d2, u32 m, u32 theta, int be
   return meta_const(m) ? CLS_C : CLS_T;
 }
 
-// K3: qualification + ordered compaction of the candidate records.
-__global__ void __launch_bounds__(256) k3_qualify(K3Args a) {
-  __shared__ u32 s_wcnt[8];
-  __shared__ u64 s_tile, s_prefix;
-  __shared__ ull s_stat[5][8];
+// K3: qualification and classification.  Warp per 32-subrange word; the
+// loads of several words are in flight per warp.
+__global__ void __launch_bounds__(256) k3_classify(K3Args a) {
+  __shared__ ull s_stat[4][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
   u32 theta = ctrl->selD.kth;
@@ -95,104 +95,99 @@ __global__ void __launch_bounds__(256) k3_qualify(K3Args a) {
     theta = max(theta, ov);
   }
   if (blockIdx.x == 0 && tid == 0) ctrl->res.theta = theta;
-  const u64 T = (a.S + K3_TILE - 1) / K3_TILE;
   const int beta = a.beta;
-  ull st_cand = 0, st_fq = 0, st_pq = 0, st_a = 0, st_lastgt = 0;
-  u32 dmax = 0;  // largest key of the answer's pool (feeds the sort's key range)
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(&ctrl->k3_ticket, 1u);
-    __syncthreads();
-    const u64 tile = s_tile;
-    if (tile >= T) break;
-    const u64 wbase = tile * K3_TILE + (u64)warp * 1024;
-    // phase 1: keep masks (lane j of the warp remembers step j's ballot)
-    u32 myword = 0, wcnt = 0;
-#pragma unroll 8
-    for (int j = 0; j < 32; j++) {
-      const u64 sid = wbase + (u64)j * 32 + lane;
-      const u32 d1 = sid < a.S ? a.D[sid * beta] : 0u;
-      const u32 word = __ballot_sync(FULL, sid < a.S && d1 >= theta);
-      if (lane == j) myword = word;
-      wcnt += __popc(word);
-    }
-    if (lane == 0) s_wcnt[warp] = wcnt;
-    __syncthreads();
-    if (warp == 0) {
-      u64 agg = 0;
-      for (int w = 0; w < 8; w++) agg += s_wcnt[w];
-      if (lane == 0) lb_publish_agg(a.lb, tile, agg);
-      const u64 excl = lb_warp_prefix(a.lb, tile);
-      if (lane == 0) {
-        lb_publish_prefix(a.lb, tile, excl + agg);
-        s_prefix = excl;
-        if (tile == T - 1) ctrl->cand_count = excl + agg;
-      }
-    }
-    __syncthreads();
-    u64 pos = s_prefix;
-    for (int w = 0; w < warp; w++) pos += s_wcnt[w];
-    // phase 2: records of the kept subranges, in subrange order
-    for (int j = 0; j < 32; j++) {
-      const u32 word = __shfl_sync(FULL, myword, j);
-      if (!word) continue;
-      const u64 sid = wbase + (u64)j * 32 + lane;
-      if ((word >> lane) & 1u) {
-        const u32 d1 = a.D[sid * beta];
-        const u32 d2 = beta >= 2 ? a.D[sid * beta + 1] : d1;
-        const u32 dl = a.D[sid * beta + beta - 1];
-        const u32 m = a.meta[sid];
-        const u32 cls = classify(d1, d2, m, theta, beta);
-        const bool fq = dl >= theta;
-        const u64 o = pos + __popc(word & lanemask_lt());
-        u32 x = cls | (fq ? 8u : 0u);
-        if (cls == CLS_E) {
-          const u32 e = atomicAdd(&ctrl->nE, 1u);
-          if (e < a.cap_e) a.e_sid[e] = (u32)sid;
-          x |= e << 4;
-        } else if (cls == CLS_T) {
-          const u32 t = atomicAdd(&ctrl->nT, 1u);
-          a.t_sid[t] = (u32)sid;
-          x |= t << 4;
+  const u64 nwords = (a.S + 31) / 32;
+  const u64 gw = ((u64)blockIdx.x * 256 + tid) >> 5;
+  const u64 nw = ((u64)gridDim.x * 256) >> 5;
+  const u32 lt = lanemask_lt();
+  ull st_cand = 0, st_fq = 0, st_pq = 0, st_a = 0;
+  u32 dmax = 0, gt_word = 0;
+  constexpr int U = 4;
+  for (u64 w0 = gw * U; w0 < nwords; w0 += nw * U) {
+    u32 d1[U], d2[U], dl[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const u64 sid = (w0 + u) * 32 + lane;
+      d1[u] = d2[u] = dl[u] = 0;
+      if (sid < a.S) {
+        if (beta == 2) {
+          const uint2 v = *reinterpret_cast<const uint2*>(a.D + sid * 2);
+          d1[u] = v.x;
+          d2[u] = dl[u] = v.y;
+        } else {
+          d1[u] = a.D[sid * beta];
+          d2[u] = beta >= 2 ? a.D[sid * beta + 1] : d1[u];
+          dl[u] = a.D[sid * beta + beta - 1];
         }
-        a.rec.sid[o] = (u32)sid;
-        a.rec.d1[o] = d1;
-        a.rec.meta[o] = m;
-        a.rec.x[o] = x;
-        st_cand++;
-        dmax = max(dmax, d1);
-        if (fq) st_fq++; else st_pq++;
-        if (cls == CLS_A) st_a++;
-        if (cls == CLS_A || cls == CLS_E) st_lastgt = max(st_lastgt, (ull)o + 1);
       }
-      pos += __popc(word);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const u64 w = w0 + u;
+      if (w >= nwords) break;
+      const u64 sid = w * 32 + lane;
+      const bool keep = sid < a.S && d1[u] >= theta;
+      const u32 mask = __ballot_sync(FULL, keep);
+      if (lane == 0) a.keepw[w] = mask;
+      if (!keep) continue;
+      const u32 m = a.meta[sid];
+      const u32 cls = classify(d1[u], d2[u], m, theta, beta);
+      const bool fq = dl[u] >= theta;
+      u32 x = cls | (fq ? 8u : 0u);
+      // E / T list slots: one atomic per warp and list (kept lanes only here)
+      const u32 km = __activemask();
+      const u32 be = __ballot_sync(km, cls == CLS_E), bt = __ballot_sync(km, cls == CLS_T);
+      const int leader = __ffs(km) - 1;
+      u32 e0 = 0, t0 = 0;
+      if (lane == leader) {
+        if (be) e0 = atomicAdd(&ctrl->nE, (u32)__popc(be));
+        if (bt) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
+      }
+      e0 = __shfl_sync(km, e0, leader);
+      t0 = __shfl_sync(km, t0, leader);
+      if (cls == CLS_E) {
+        const u32 e = e0 + __popc(be & lt);
+        if (e < a.cap_e) a.e_sid[e] = (u32)sid;
+        x |= e << 4;
+      } else if (cls == CLS_T) {
+        const u32 t = t0 + __popc(bt & lt);
+        a.t_sid[t] = (u32)sid;
+        x |= t << 4;
+      }
+      const u64 slot = w * 32 + __popc(mask & lt);
+      a.rec.sid[slot] = (u32)sid;
+      a.rec.d1[slot] = d1[u];
+      a.rec.meta[slot] = m;
+      a.rec.x[slot] = x;
+      st_cand++;
+      dmax = max(dmax, d1[u]);
+      if (fq) st_fq++; else st_pq++;
+      if (cls == CLS_A) st_a++;
+      if (cls == CLS_A || cls == CLS_E) gt_word = max(gt_word, (u32)w + 1);
     }
   }
-  ull v[5] = {st_cand, st_fq, st_pq, st_a, st_lastgt};
+  ull v[4] = {st_cand, st_fq, st_pq, st_a};
 #pragma unroll
-  for (int i = 0; i < 5; i++) {
-    if (i < 4) {
+  for (int i = 0; i < 4; i++) {
 #pragma unroll
-      for (int o = 16; o; o >>= 1) v[i] += __shfl_xor_sync(FULL, v[i], o);
-    } else {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) v[i] = max(v[i], __shfl_xor_sync(FULL, v[i], o));
-    }
+    for (int o = 16; o; o >>= 1) v[i] += __shfl_xor_sync(FULL, v[i], o);
     if (lane == 0) s_stat[i][warp] = v[i];
   }
   dmax = __reduce_max_sync(FULL, dmax);
-  if (lane == 0 && dmax) atomicMax(&ctrl->maxkey, dmax);
+  gt_word = __reduce_max_sync(FULL, gt_word);
+  if (lane == 0) {
+    if (dmax) atomicMax(&ctrl->maxkey, dmax);
+    if (gt_word) atomicMax(&ctrl->gt_rec_end, (ull)gt_word);
+  }
   __syncthreads();
   if (tid == 0) {
-    ull t[5] = {0, 0, 0, 0, 0};
-    for (int w = 0; w < 8; w++) {
+    ull t[4] = {0, 0, 0, 0};
+    for (int w = 0; w < 8; w++)
       for (int i = 0; i < 4; i++) t[i] += s_stat[i][w];
-      t[4] = max(t[4], s_stat[4][w]);
-    }
     if (t[0]) atomicAdd((ull*)&ctrl->res.candidate_subranges, t[0]);
     if (t[1]) atomicAdd((ull*)&ctrl->res.fully_qualified, t[1]);
     if (t[2]) atomicAdd((ull*)&ctrl->res.partially_qualified, t[2]);
     if (t[3]) atomicAdd(&ctrl->nA, t[3]);
-    if (t[4]) atomicMax(&ctrl->gt_rec_end, t[4]);
   }
 }
 
@@ -437,7 +432,9 @@ __global__ void __launch_bounds__(256) k4t_count(const u32* __restrict__ keys, u
 // ---------------------------------------------------------------------------
 struct K5Args {
   Ctrl* ctrl;
-  Records rec;
+  Records rec;     // word-local record slots
+  const u32* keepw;
+  u64 S;
   u64 n;
   int alpha;
   u64 k;
@@ -446,18 +443,18 @@ struct K5Args {
   const u32* seg_gt;
   const u32* seg_eq;
   const u32* t_cnt;  // ties of each T candidate (K4T)
-  u32* gt_keys;  // P_gt, index order
+  u32* gt_keys;      // P_gt, index order
   u64* gt_idx;
-  u64* ties;     // first k ties, index order
-  u32* d_rec;    // K6 work list: record index
-  u64* d_pos;    //               tie position and count needed
+  u64* ties;         // first k ties, index order
+  u32* d_sid;        // K6 work list: subrange, first tie position, ties needed
+  u64* d_pos;
   u32* d_need;
   u64* lb_gt;
   u64* lb_eq;
 };
 
-__device__ __forceinline__ void rec_counts(const K5Args& a, u64 i, u32 theta, u64& g, u64& e) {
-  const u32 x = a.rec.x[i];
+__device__ __forceinline__ void rec_counts(const K5Args& a, u64 slot, u64& g, u64& e) {
+  const u32 x = a.rec.x[slot];
   const u32 cls = x & 7u;
   g = 0;
   e = 0;
@@ -466,7 +463,7 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, u64 i, u32 theta, u6
   } else if (cls == CLS_B) {
     e = 1;
   } else if (cls == CLS_C) {
-    e = sub_len(a.rec.sid[i], a.n, a.alpha);
+    e = sub_len(a.rec.sid[slot], a.n, a.alpha);
   } else if (cls == CLS_T) {
     e = a.t_cnt[x >> 4];
   } else {
@@ -478,10 +475,9 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, u64 i, u32 theta, u6
       e += a.seg_eq[eidx * ppc + p];
     }
   }
-  (void)theta;
 }
 
-// K5: ordered assembly of P_gt and of the first k ties.
+// K5: ordered assembly of P_gt and of the first k ties, over 32-subrange words.
 __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
   __shared__ u64 s_tile, s_gx, s_ex;
   __shared__ int s_skip;
@@ -490,13 +486,12 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
   const u32 theta = ctrl->res.theta;
-  const u64 P = ctrl->cand_count;
-  const u64 T = (P + K5_TILE - 1) / K5_TILE;
-  const u64 gt_end = ctrl->gt_rec_end;
-  const u64 W = 1ull << a.alpha;
+  const u64 nwords = (a.S + 31) / 32;
+  const u64 T = (nwords + K5_TILE - 1) / K5_TILE;
+  const u64 gt_end = ctrl->gt_rec_end;  // 1 + last word holding elements > theta
   const int lseg = a.alpha < 13 ? a.alpha : 13;
   const u64 seglen = 1ull << lseg;
-  const u64 ppc = W >> lseg;
+  const u64 ppc = (1ull << a.alpha) >> lseg;
   ull st_concat = 0;
   for (;;) {
     if (tid == 0) {
@@ -507,8 +502,8 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
     const u64 tile = s_tile;
     if (tile >= T) break;
     if (s_skip) {
-      // nothing > theta from here on and the first k ties are already placed:
-      // publish the final prefix without reading anything
+      // nothing > theta from here on and the first k ties are placed: publish
+      // the final prefix without reading anything
       if (tid == 0) {
         const u64 G = ctrl->nA + ctrl->sumEgt;
         st_release(&a.lb_gt[tile], LB_PRE | G);
@@ -527,15 +522,20 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
       __syncthreads();
       continue;
     }
-    const u64 i0 = tile * K5_TILE + (u64)tid * K5_PER;
+    const u64 w0 = tile * K5_TILE + (u64)tid * K5_WPT;
+    u32 masks[K5_WPT];
     u64 tg = 0, te = 0;
-    for (int r = 0; r < K5_PER; r++) {
-      const u64 i = i0 + r;
-      if (i >= P) break;
-      u64 g, e;
-      rec_counts(a, i, theta, g, e);
-      tg += g;
-      te += e;
+#pragma unroll
+    for (int r = 0; r < K5_WPT; r++) masks[r] = w0 + r < nwords ? a.keepw[w0 + r] : 0u;
+#pragma unroll
+    for (int r = 0; r < K5_WPT; r++) {
+      const u32 cnt = __popc(masks[r]);
+      for (u32 q = 0; q < cnt; q++) {
+        u64 g, e;
+        rec_counts(a, (w0 + r) * 32 + q, g, e);
+        tg += g;
+        te += e;
+      }
     }
     const u64 ig = block_incl_scan_256<u64>(tg, scratch_g);
     const u64 ie = block_incl_scan_256<u64>(te, scratch_e);
@@ -571,58 +571,60 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
     }
     __syncthreads();
     u64 gpos = s_gx + ig - tg, epos = s_ex + ie - te;
-    for (int r = 0; r < K5_PER; r++) {
-      const u64 i = i0 + r;
-      if (i >= P) break;
-      const u32 x = a.rec.x[i];
-      const u32 cls = x & 7u;
-      const bool fq = (x >> 3) & 1u;
-      const u64 sid = a.rec.sid[i];
-      const u32 m = a.rec.meta[i];
-      const u64 base = sid << a.alpha;
-      if (cls == CLS_A) {
-        a.gt_keys[gpos] = a.rec.d1[i];
-        a.gt_idx[gpos] = base + meta_p1(m);
-        gpos++;
-      } else if (cls == CLS_B) {
-        if (epos < a.k) a.ties[epos] = base + meta_p1(m);
-        epos++;
-      } else if (cls == CLS_C) {
-        const u64 len = sub_len(sid, a.n, a.alpha);
-        const u64 take = epos < a.k ? min(len, a.k - epos) : 0;
-        for (u64 q = 0; q < take; q++) a.ties[epos + q] = base + q;
-        if (fq) st_concat += len;
-        epos += len;
-      } else if (cls == CLS_T) {
-        const u64 c1 = a.t_cnt[x >> 4];
-        if (epos < a.k && c1) {
-          const u32 slot = atomicAdd(&ctrl->k6_count, 1u);
-          a.d_rec[slot] = (u32)i;
-          a.d_pos[slot] = epos;
-          a.d_need[slot] = (u32)min(c1, a.k - epos);
-        }
-        if (fq) st_concat += c1;
-        epos += c1;
-      } else {
-        const u64 eidx = x >> 4;
-        u64 eg = 0, ee = 0;
-        for (u64 p = 0; p < ppc; p++) {
-          const u64 sg = eidx * ppc + p;
-          const u32 ng = a.seg_gt[sg], ne = a.seg_eq[sg];
-          const u64 sb = sg << lseg;
-          for (u32 q = 0; q < ng; q++) {
-            a.gt_keys[gpos + q] = a.stg_key[sb + q];
-            a.gt_idx[gpos + q] = a.stg_idx[sb + q];
+#pragma unroll
+    for (int r = 0; r < K5_WPT; r++) {
+      const u32 cnt = __popc(masks[r]);
+      for (u32 q = 0; q < cnt; q++) {
+        const u64 slot = (w0 + r) * 32 + q;
+        const u32 x = a.rec.x[slot];
+        const u32 cls = x & 7u;
+        const bool fq = (x >> 3) & 1u;
+        const u64 sid = a.rec.sid[slot];
+        const u64 base = sid << a.alpha;
+        if (cls == CLS_A) {
+          a.gt_keys[gpos] = a.rec.d1[slot];
+          a.gt_idx[gpos] = base + meta_p1(a.rec.meta[slot]);
+          gpos++;
+        } else if (cls == CLS_B) {
+          if (epos < a.k) a.ties[epos] = base + meta_p1(a.rec.meta[slot]);
+          epos++;
+        } else if (cls == CLS_C) {
+          const u64 len = sub_len(sid, a.n, a.alpha);
+          const u64 take = epos < a.k ? min(len, a.k - epos) : 0;
+          for (u64 z = 0; z < take; z++) a.ties[epos + z] = base + z;
+          if (fq) st_concat += len;
+          epos += len;
+        } else if (cls == CLS_T) {
+          const u64 c1 = a.t_cnt[x >> 4];
+          if (epos < a.k && c1) {
+            const u32 wslot = atomicAdd(&ctrl->k6_count, 1u);
+            a.d_sid[wslot] = (u32)sid;
+            a.d_pos[wslot] = epos;
+            a.d_need[wslot] = (u32)min(c1, a.k - epos);
           }
-          gpos += ng;
-          eg += ng;
-          for (u32 q = 0; q < ne; q++) {
-            if (epos + q < a.k) a.ties[epos + q] = a.stg_idx[sb + seglen - 1 - q];
+          if (fq) st_concat += c1;
+          epos += c1;
+        } else {
+          const u64 eidx = x >> 4;
+          u64 eg = 0, ee = 0;
+          for (u64 p = 0; p < ppc; p++) {
+            const u64 sg = eidx * ppc + p;
+            const u32 ng = a.seg_gt[sg], ne = a.seg_eq[sg];
+            const u64 sb = sg << lseg;
+            for (u32 z = 0; z < ng; z++) {
+              a.gt_keys[gpos + z] = a.stg_key[sb + z];
+              a.gt_idx[gpos + z] = a.stg_idx[sb + z];
+            }
+            gpos += ng;
+            eg += ng;
+            for (u32 z = 0; z < ne; z++) {
+              if (epos + z < a.k) a.ties[epos + z] = a.stg_idx[sb + seglen - 1 - z];
+            }
+            epos += ne;
+            ee += ne;
           }
-          epos += ne;
-          ee += ne;
+          if (fq) st_concat += eg + ee;
         }
-        if (fq) st_concat += eg + ee;
       }
     }
     __syncthreads();
@@ -641,9 +643,8 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
 // (one warp per record; ballot-ordered within the subrange).
 template <int MODE>
 __global__ void __launch_bounds__(256) k6_ties(Ctrl* ctrl, const u32* __restrict__ keys, u64 n, int alpha,
-                                               const u32* __restrict__ rec_sid, const u32* __restrict__ d_rec,
-                                               const u64* __restrict__ d_pos, const u32* __restrict__ d_need,
-                                               u64* __restrict__ ties) {
+                                               const u32* __restrict__ d_sid, const u64* __restrict__ d_pos,
+                                               const u32* __restrict__ d_need, u64* __restrict__ ties) {
   const int lane = threadIdx.x & 31;
   const u32 theta = ctrl->res.theta;
   const u32 cnt = ctrl->k6_count;
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(256) k6_ties(Ctrl* ctrl, const u32* __restrict
   const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
   const u32 lt = lanemask_lt();
   for (u64 w = gw; w < cnt; w += nw) {
-    const u64 base = (u64)rec_sid[d_rec[w]] << alpha;
+    const u64 base = (u64)d_sid[w] << alpha;
     const u64 len = sub_len(base >> alpha, n, alpha);
     const u64 pos0 = d_pos[w];
     const u32 need = d_need[w];
@@ -663,6 +664,87 @@ __global__ void __launch_bounds__(256) k6_ties(Ctrl* ctrl, const u32* __restrict
       const u32 r = found + __popc(b & lt);
       if (t && r < need) ties[pos0 + r] = base + e;
       found += __popc(b);
+    }
+  }
+}
+
+// Bitonic sort (ascending) of R*1024 u64 values held as v[j] = element
+// j*1024 + threadIdx.x: strides < 32 exchange through shuffles, strides of
+// 32..512 through shared memory, strides >= 1024 stay inside the thread.
+template <int R>
+__device__ __forceinline__ void bitonic_1024(unsigned long long (&v)[R], unsigned long long* sm) {
+  const u32 tid = threadIdx.x;
+  constexpr u32 NP = R * 1024;
+  for (u32 size = 2; size <= NP; size <<= 1) {
+    // strides >= 1024: both elements live in this thread (compile-time slots)
+#pragma unroll
+    for (int js = R / 2; js >= 1; js >>= 1) {
+      if ((u32)js * 1024u <= (size >> 1)) {
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+          if ((j & js) == 0) {
+            const u32 i = (u32)j * 1024u + tid;
+            const bool up = (i & size) == 0;
+            const unsigned long long x = v[j], y = v[j | js];
+            const bool sw = (x > y) == up;
+            v[j] = sw ? y : x;
+            v[j | js] = sw ? x : y;
+          }
+        }
+      }
+    }
+    for (u32 stride = min(size >> 1, 512u); stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+#pragma unroll
+        for (int j = 0; j < R; j++) sm[j * 1024 + tid] = v[j];
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+          const u32 i = (u32)j * 1024u + tid;
+          const unsigned long long p = sm[i ^ stride];
+          const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
+          v[j] = keep_min ? min(v[j], p) : max(v[j], p);
+        }
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+          const u32 i = (u32)j * 1024u + tid;
+          const unsigned long long p = __shfl_xor_sync(FULL, v[j], (int)stride);
+          const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
+          v[j] = keep_min ? min(v[j], p) : max(v[j], p);
+        }
+      }
+    }
+  }
+}
+
+template <int MODE, int R>
+__device__ __forceinline__ void finish_small_r(Ctrl* ctrl, u64 m, u64 ko, u64 G, u32 theta, u32 hi,
+                                               const u32* __restrict__ gt_keys, const u64* __restrict__ gt_idx,
+                                               const u64* __restrict__ ties, u32* __restrict__ ov,
+                                               long long* __restrict__ oi, long long offset,
+                                               unsigned long long* sm) {
+  unsigned long long v[R];
+#pragma unroll
+  for (int j = 0; j < R; j++) {
+    const u32 i = (u32)j * 1024u + threadIdx.x;
+    v[j] = ~0ull;
+    if (i < m) {
+      const u32 key = i < G ? gt_keys[i] : theta;
+      v[j] = ((unsigned long long)(hi - key) << 32) | i;
+    }
+  }
+  bitonic_1024<R>(v, sm);
+#pragma unroll
+  for (int j = 0; j < R; j++) {
+    const u32 i = (u32)j * 1024u + threadIdx.x;
+    if (i < ko) {
+      const u32 pos = (u32)(v[j] & 0xffffffffu);
+      const u32 key = hi - (u32)(v[j] >> 32);
+      ov[i] = from_key<MODE>(key);
+      oi[i] = (long long)(pos < G ? gt_idx[pos] : ties[pos - G]) + offset;
+      if (i == ko - 1) ctrl->res.kth_key = key;
     }
   }
 }
@@ -684,39 +766,14 @@ __global__ void __launch_bounds__(1024) finish_small(Ctrl* ctrl, const u32* __re
   const u64 ko = ctrl->res.k_out;
   const u32 theta = ctrl->res.theta;
   const u32 hi = max(ctrl->maxkey, theta);
-  u32 np = 1;
-  while (np < m) np <<= 1;
-  for (u32 i = threadIdx.x; i < np; i += 1024) {
-    unsigned long long v = ~0ull;
-    if (i < m) {
-      const u32 key = i < G ? gt_keys[i] : theta;
-      v = ((unsigned long long)(hi - key) << 32) | i;
-    }
-    sk[i] = v;
-  }
-  __syncthreads();
-  for (u32 size = 2; size <= np; size <<= 1) {
-    for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
-      for (u32 t = threadIdx.x; t < np / 2; t += 1024) {
-        const u32 lo = 2 * t - (t & (stride - 1));
-        const u32 hi2 = lo + stride;
-        const bool up = (lo & size) == 0;
-        const unsigned long long x = sk[lo], y = sk[hi2];
-        if ((x > y) == up) {
-          sk[lo] = y;
-          sk[hi2] = x;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (u32 i = threadIdx.x; i < ko; i += 1024) {
-    const u32 pos = (u32)(sk[i] & 0xffffffffu);
-    const u32 key = hi - (u32)(sk[i] >> 32);
-    ov[i] = from_key<MODE>(key);
-    oi[i] = (long long)(pos < G ? gt_idx[pos] : ties[pos - G]) + offset;
-    if (i == ko - 1) ctrl->res.kth_key = key;
-  }
+  if (m <= 1024)
+    finish_small_r<MODE, 1>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+  else if (m <= 2048)
+    finish_small_r<MODE, 2>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+  else if (m <= 4096)
+    finish_small_r<MODE, 4>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+  else
+    finish_small_r<MODE, 8>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   if (threadIdx.x == 0) ctrl->small_done = 1;
 }
 

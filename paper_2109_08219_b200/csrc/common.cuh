@@ -96,12 +96,17 @@ struct Ctrl {
   u32 small_done;  // finish_small wrote the answer
   u32 nT;          // class-T records (tie-only, counted by K4T)
   u32 pad1;
-  // emit
+  // emit and sort of the answer
   u32 em_ticket;
   u32 maxkey;
   u32 sort_lo;
-  u32 sort_bits;
+  u32 sort_src;    // 0: sort buffer A holds the input, 1: buffer B
+  ull sort_m;      // elements to sort
+  u32 big_mode;    // 0 done by finish_small, 1 merge (append ties), 2 sort the pool, 3 radix select
+  u32 sort_done;   // last-block counter of sort_scan
 };
+
+enum BigMode : u32 { BIG_NONE = 0, BIG_MERGE = 1, BIG_SORT_POOL = 2, BIG_SELECT = 3 };
 
 // ---------------------------------------------------------------------------
 // PTX wrappers

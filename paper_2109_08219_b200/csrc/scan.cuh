@@ -37,7 +37,6 @@ struct ScanArgs {
   int direct;
 };
 
-__device__ __forceinline__ bool big_path_skip(const Ctrl* c) { return ld_volatile_u32(&c->small_done) != 0; }
 
 template <int MODE>
 __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
@@ -48,7 +47,7 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
   __shared__ u32 s_max[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
-  if (a.check_path && (ld_volatile_u32(&ctrl->res.path) != PATH_SELECT || big_path_skip(ctrl))) return;
+  if (a.check_path && ld_volatile_u32(&ctrl->big_mode) != BIG_SELECT) return;
 
   const DigitResult r1 = ctrl->selP.r1, r2 = ctrl->selP.r2;
   find_digit<NB3>(ctrl->selP.hist3, r2.rem, &r3s, scratch);
@@ -61,6 +60,8 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
     ctrl->selP.r3 = r3s;
     ctrl->selP.kth = theta;
     ctrl->sort_lo = theta;
+    ctrl->sort_m = a.k;
+    ctrl->sort_src = a.direct ? 0u : 1u;  // direct: emit into A; pool select: into B
     ctrl->res.k_out = a.k;
     if (a.direct) {
       ctrl->res.path = PATH_DIRECT;
@@ -206,28 +207,45 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
   }
 }
 
-// MERGE path: answer = P_gt (all keys > theta, index order) ++ first ties.
-__global__ void __launch_bounds__(256) merge_copy(Ctrl* ctrl, const u32* __restrict__ gk, const u64* __restrict__ gi,
-                                                  const u64* __restrict__ ties, u32* __restrict__ ok,
-                                                  u64* __restrict__ oi) {
-  if (ld_volatile_u32(&ctrl->res.path) != PATH_MERGE || big_path_skip(ctrl)) return;
+// Decide how the pool beyond SMALL_POOL is finished (one thread).
+__global__ void tail_decide(Ctrl* ctrl, u64 k) {
+  if (ctrl->small_done) {
+    ctrl->big_mode = BIG_NONE;
+    return;
+  }
+  const u64 G = ctrl->res.pool_gt;
+  ctrl->sort_lo = ctrl->res.theta;
+  if (ctrl->res.path == PATH_MERGE) {
+    ctrl->big_mode = BIG_MERGE;  // pool = P_gt ++ ties, sorted in place
+    ctrl->sort_src = 0;
+    ctrl->sort_m = ctrl->res.k_out;
+  } else if (G <= 4 * k) {
+    ctrl->big_mode = BIG_SORT_POOL;  // sort all of P_gt, keep the first k
+    ctrl->sort_src = 0;
+    ctrl->sort_m = G;
+  } else {
+    ctrl->big_mode = BIG_SELECT;  // radix select + ordered emit, then sort k
+  }
+}
+
+// BIG_MERGE: append the ties (key theta) after P_gt.
+__global__ void __launch_bounds__(256) merge_append(Ctrl* ctrl, u32* __restrict__ gk, u64* __restrict__ gi,
+                                                    const u64* __restrict__ ties) {
+  if (ld_volatile_u32(&ctrl->big_mode) != BIG_MERGE) return;
   const u64 G = ctrl->res.pool_gt, kout = ctrl->res.k_out;
   const u32 theta = ctrl->res.theta;
-  for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < kout; i += (u64)gridDim.x * 256) {
-    if (i < G) {
-      ok[i] = gk[i];
-      oi[i] = gi[i];
-    } else {
-      ok[i] = theta;
-      oi[i] = ties[i - G];
-    }
+  for (u64 i = G + (u64)blockIdx.x * 256 + threadIdx.x; i < kout; i += (u64)gridDim.x * 256) {
+    gk[i] = theta;
+    gi[i] = ties[i - G];
   }
 }
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort of the k answer pairs by key descending: digits of
-// (maxkey - key), only as many 8-bit passes as max - min needs.  Input order
+// Stable LSD radix sort of the answer candidates by key descending: digits of
+// (maxkey - key), only as many 8-bit passes as maxkey - lo needs.  Input order
 // is index order within equal keys, so stability yields (key desc, index asc).
+// The number of elements (ctrl->sort_m) and the buffer holding them
+// (ctrl->sort_src: 0 = A, 1 = B) are decided on the device.
 // ---------------------------------------------------------------------------
 constexpr int ST_TILE = 2048;
 constexpr int SMALL_SORT = 8192;  // answers up to this size are sorted by one CTA
@@ -239,52 +257,95 @@ __device__ __forceinline__ int sort_bits(const Ctrl* c) {
 }
 
 __device__ __forceinline__ bool big_sort_skip(const Ctrl* c, int pass) {
-  return big_path_skip(c) || c->res.k_out <= (ull)SMALL_SORT || pass * 8 >= sort_bits(c);
+  return c->sort_m <= (ull)SMALL_SORT || pass * 8 >= sort_bits(c) || c->small_done;
 }
 
-__global__ void __launch_bounds__(256) sort_hist(Ctrl* ctrl, const u32* __restrict__ keys, int pass,
-                                                 u32* __restrict__ counts) {
+struct SortBufs {
+  u32* ka;
+  u64* ia;
+  u32* kb;
+  u64* ib;
+  u32* counts;     // [256][T] digit-major
+  u32* digit_base; // [256]
+  u32* digit_tot;  // [256]
+};
+
+__device__ __forceinline__ void sort_io(const Ctrl* c, const SortBufs& b, int pass, const u32*& kin, const u64*& iin,
+                                        u32*& kout, u64*& iout) {
+  const bool from_b = ((c->sort_src + (u32)pass) & 1u) != 0;
+  kin = from_b ? b.kb : b.ka;
+  iin = from_b ? b.ib : b.ia;
+  kout = from_b ? b.ka : b.kb;
+  iout = from_b ? b.ia : b.ib;
+}
+
+__global__ void __launch_bounds__(256) sort_hist(Ctrl* ctrl, SortBufs b, int pass) {
   if (big_sort_skip(ctrl, pass)) return;
   __shared__ u32 h[256];
-  const u64 kout = ctrl->res.k_out;
+  const u32 *keys, *kx;
+  const u64 *ix;
+  u64* iy;
+  u32* ky;
+  sort_io(ctrl, b, pass, keys, ix, ky, iy);
+  (void)kx;
+  const u64 m = ctrl->sort_m;
   const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
-  const u64 T = (kout + ST_TILE - 1) / ST_TILE;
+  const u64 T = (m + ST_TILE - 1) / ST_TILE;
   for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
     h[threadIdx.x] = 0;
     __syncthreads();
     for (int r = 0; r < ST_TILE / 256; r++) {
       const u64 e = tile * ST_TILE + (u64)r * 256 + threadIdx.x;
-      if (e < kout) atomicAdd(&h[((hi - keys[e]) >> (8 * pass)) & 255u], 1u);
+      if (e < m) atomicAdd(&h[((hi - keys[e]) >> (8 * pass)) & 255u], 1u);
     }
     __syncthreads();
-    counts[tile * 256 + threadIdx.x] = h[threadIdx.x];
+    b.counts[(u64)threadIdx.x * T + tile] = h[threadIdx.x];  // digit-major
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(256) sort_scan(Ctrl* ctrl, int pass, u32* __restrict__ counts) {
+// One warp per digit: exclusive scan of its column over the tiles; the last
+// CTA scans the 256 digit totals into digit_base.
+__global__ void __launch_bounds__(256) sort_scan(Ctrl* ctrl, SortBufs b, int pass) {
   if (big_sort_skip(ctrl, pass)) return;
+  __shared__ int am_last;
   __shared__ u32 scratch[8];
-  const u64 T = (ctrl->res.k_out + ST_TILE - 1) / ST_TILE;
-  const int d = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const u32 d = blockIdx.x * 8 + (threadIdx.x >> 5);  // grid = 32 CTAs
+  const u64 T = (ctrl->sort_m + ST_TILE - 1) / ST_TILE;
+  u32* col = b.counts + (u64)d * T;
   u32 run = 0;
-  for (u64 t = 0; t < T; t++) {
-    const u32 v = counts[t * 256 + d];
-    counts[t * 256 + d] = run;
-    run += v;
+  for (u64 t0 = 0; t0 < T; t0 += 32) {
+    const u64 t = t0 + lane;
+    const u32 c = t < T ? col[t] : 0u;
+    const u32 incl = warp_incl_scan<u32>(c);
+    if (t < T) col[t] = run + incl - c;
+    run += __shfl_sync(FULL, incl, 31);
   }
-  const u32 incl = block_incl_scan_256<u32>(run, scratch);
-  const u32 base = incl - run;
-  for (u64 t = 0; t < T; t++) counts[t * 256 + d] += base;
+  if (lane == 0) b.digit_tot[d] = run;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) am_last = atomicAdd(&ctrl->sort_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    const u32 tot = __ldcg(&b.digit_tot[threadIdx.x]);
+    const u32 incl = block_incl_scan_256<u32>(tot, scratch);
+    b.digit_base[threadIdx.x] = incl - tot;
+    if (threadIdx.x == 0) ctrl->sort_done = 0;  // next pass
+  }
 }
 
-__global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, int pass, const u32* __restrict__ kin,
-                                                    const u64* __restrict__ iin, u32* __restrict__ kout,
-                                                    u64* __restrict__ iout, const u32* __restrict__ counts) {
+__global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, SortBufs b, int pass) {
   if (big_sort_skip(ctrl, pass)) return;
   __shared__ u32 wc[8][256];
+  const u32* kin;
+  const u64* iin;
+  u32* kout;
+  u64* iout;
+  sort_io(ctrl, b, pass, kin, iin, kout, iout);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const u64 ko = ctrl->res.k_out;
+  const u64 ko = ctrl->sort_m;
   const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
   const u64 T = (ko + ST_TILE - 1) / ST_TILE;
   const u32 lt = lanemask_lt();
@@ -295,8 +356,12 @@ __global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, int pass, const 
 #pragma unroll
     for (int r = 0; r < 8; r++) {
       const u64 e = tile * ST_TILE + (u64)warp * 256 + (u64)r * 32 + lane;
+      key[r] = e < ko ? kin[e] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const u64 e = tile * ST_TILE + (u64)warp * 256 + (u64)r * 32 + lane;
       const bool v = e < ko;
-      key[r] = v ? kin[e] : 0u;
       dg[r] = v ? ((hi - key[r]) >> (8 * pass)) & 255u : 256u;
       const u32 peers = __match_any_sync(FULL, dg[r]);
       const u32 leader = __ffs(peers) - 1;
@@ -319,7 +384,7 @@ __global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, int pass, const 
     for (int r = 0; r < 8; r++) {
       const u64 e = tile * ST_TILE + (u64)warp * 256 + (u64)r * 32 + lane;
       if (e < ko) {
-        const u64 pos = (u64)counts[tile * 256 + dg[r]] + wc[warp][dg[r]] + rk[r];
+        const u64 pos = (u64)b.digit_base[dg[r]] + b.counts[(u64)dg[r] * T + tile] + wc[warp][dg[r]] + rk[r];
         kout[pos] = key[r];
         iout[pos] = iin[e];
       }
@@ -328,16 +393,16 @@ __global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, int pass, const 
   }
 }
 
+// Write the first k_out sorted pairs in the input dtype (big sorts only).
 template <int MODE>
-__global__ void __launch_bounds__(256) writeout(Ctrl* ctrl, const u32* __restrict__ kA, const u64* __restrict__ iA,
-                                                const u32* __restrict__ kB, const u64* __restrict__ iB,
-                                                u32* __restrict__ ov, long long* __restrict__ oi, long long offset) {
+__global__ void __launch_bounds__(256) writeout(Ctrl* ctrl, SortBufs b, u32* __restrict__ ov,
+                                                long long* __restrict__ oi, long long offset) {
+  if (ctrl->sort_m <= (ull)SMALL_SORT || ctrl->small_done) return;
+  const int passes = (sort_bits(ctrl) + 7) / 8;
+  const bool in_b = ((ctrl->sort_src + (u32)passes) & 1u) != 0;
+  const u32* ks = in_b ? b.kb : b.ka;
+  const u64* is = in_b ? b.ib : b.ia;
   const u64 ko = ctrl->res.k_out;
-  if (ko <= (u64)SMALL_SORT || big_path_skip(ctrl)) return;  // sort_small / finish_small wrote it
-  const int nb = sort_bits(ctrl);
-  const int passes = (nb + 7) / 8;
-  const u32* ks = (passes & 1) ? kB : kA;
-  const u64* is = (passes & 1) ? iB : iA;
   for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < ko; i += (u64)gridDim.x * 256) {
     const u32 key = ks[i];
     ov[i] = from_key<MODE>(key);
@@ -346,21 +411,23 @@ __global__ void __launch_bounds__(256) writeout(Ctrl* ctrl, const u32* __restric
   }
 }
 
-// One CTA sorts answers of up to SMALL_SORT pairs in shared memory and writes
-// them out: bitonic sort of (maxkey - key) << 32 | position, so equal keys keep
+// One CTA sorts up to SMALL_SORT pairs in shared memory and writes the first
+// k_out: bitonic sort of (maxkey - key) << 32 | position, so equal keys keep
 // their (index-ordered) input positions -- a stable descending sort.
 template <int MODE>
-__global__ void __launch_bounds__(1024) sort_small(Ctrl* ctrl, const u32* __restrict__ kA,
-                                                   const u64* __restrict__ iA, u32* __restrict__ ov,
+__global__ void __launch_bounds__(1024) sort_small(Ctrl* ctrl, SortBufs b, u32* __restrict__ ov,
                                                    long long* __restrict__ oi, long long offset) {
   extern __shared__ unsigned long long sk[];  // SMALL_SORT entries (64 KiB, dynamic)
+  const u64 m = ctrl->sort_m;
+  if (m > (u64)SMALL_SORT || m == 0 || ctrl->small_done) return;
   const u64 ko = ctrl->res.k_out;
-  if (ko > (u64)SMALL_SORT || ko == 0 || big_path_skip(ctrl)) return;
+  const u32* kA = ctrl->sort_src ? b.kb : b.ka;
+  const u64* iA = ctrl->sort_src ? b.ib : b.ia;
   const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
   u32 np = 1;
-  while (np < ko) np <<= 1;
+  while (np < m) np <<= 1;
   for (u32 i = threadIdx.x; i < np; i += 1024)
-    sk[i] = i < ko ? ((unsigned long long)(hi - kA[i]) << 32) | i : ~0ull;
+    sk[i] = i < m ? ((unsigned long long)(hi - kA[i]) << 32) | i : ~0ull;
   __syncthreads();
   for (u32 size = 2; size <= np; size <<= 1) {
     for (u32 stride = size >> 1; stride > 0; stride >>= 1) {

@@ -16,15 +16,14 @@
 
 namespace dtopk {
 
-constexpr int K2_TILE = 2048;  // subranges per tile of the delegate scan (256 threads x 8)
-
 struct K2Args {
   const u32* D;
-  u64 S;
-  int beta;
+  u64 nD;      // beta * S delegates
   u64 k;
   Ctrl* ctrl;
-  u32* selbuf;
+  u32* selbuf;  // region of CTA c: [c * R, c * R + region_cnt[c])
+  u32* region_cnt;
+  u64 R;        // delegates per CTA region (multiple of 512)
 };
 
 // Warp-aggregated append of `x` (where pred) to buf[*counter++].
@@ -39,62 +38,64 @@ __device__ __forceinline__ void warp_append(u32* buf, ull* counter, u32 x, bool 
   if (pred) buf[base + __popc(b & lanemask_lt())] = x;
 }
 
-// K2: pass 2 of kth(D) -- one read of D: histogram of digit 2 for the
-// delegates in theta's digit-1 bucket and compaction of that bucket into
-// selbuf (one global atomic per tile reserves the block's slots).
+// K2: pass 2 of kth(D) -- one read of D.  CTA c owns the contiguous range
+// [c*R, (c+1)*R) of D; its warps histogram digit 2 of the delegates in
+// theta's digit-1 bucket and compact them into the CTA's own region of selbuf
+// through a shared-memory counter (no global atomics, no barriers in the loop).
 __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
   __shared__ u32 shist[NB2];
   __shared__ DigitResult r1;
   __shared__ ull scratch[8];
-  __shared__ u32 s_wcnt[8];
-  __shared__ ull s_base;
+  __shared__ u32 s_cnt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < NB2; i += 256) shist[i] = 0;
+  if (tid == 0) s_cnt = 0;
   find_digit<NB1>(a.ctrl->selD.hist1, a.k, &r1, scratch);
   if (blockIdx.x == 0 && tid == 0) a.ctrl->selD.r1 = r1;
   const u32 b1 = r1.digit;
-  const u64 nD = a.S * (u64)a.beta;
-  const u64 T = (nD + 256 * 16 - 1) / (256 * 16);
+  const u64 lo = (u64)blockIdx.x * a.R;
+  const u64 hi = min(a.nD, lo + a.R);
+  u32* region = a.selbuf + lo;
   const u32 lt = lanemask_lt();
-  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
-    // each warp owns 512 consecutive delegates, read as 16 coalesced rounds
-    const u64 base = tile * (256 * 16) + (u64)warp * 512;
-    u32 v[16], bl[16];
+  for (u64 base = lo + (u64)warp * 512; base < hi; base += 8 * 512) {
+    u32 v[16];
+    u32 bl[16];
     u32 cnt = 0;
 #pragma unroll
     for (int j = 0; j < 16; j++) {
       const u64 i = base + (u64)j * 32 + lane;
-      v[j] = i < nD ? a.D[i] : 0u;
-      const bool p = i < nD && dig1(v[j]) == b1;
+      v[j] = i < hi ? a.D[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const u64 i = base + (u64)j * 32 + lane;
+      const bool p = i < hi && dig1(v[j]) == b1;
       bl[j] = __ballot_sync(FULL, p);
       cnt += __popc(bl[j]);
       if (p) atomicAdd(&shist[dig2(v[j])], 1u);
     }
-    if (lane == 0) s_wcnt[warp] = cnt;
-    __syncthreads();
-    if (tid == 0) {
-      u32 tot = 0;
-      for (int w = 0; w < 8; w++) tot += s_wcnt[w];
-      s_base = tot ? atomicAdd(&a.ctrl->selD.buf_count, (ull)tot) : 0ull;
-    }
-    __syncthreads();
-    u64 o = s_base;
-    for (int w = 0; w < warp; w++) o += s_wcnt[w];
+    if (cnt) {
+      u32 o = 0;
+      if (lane == 0) o = atomicAdd(&s_cnt, cnt);
+      o = __shfl_sync(FULL, o, 0);
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-      if ((bl[j] >> lane) & 1u) a.selbuf[o + __popc(bl[j] & lt)] = v[j];
-      o += __popc(bl[j]);
+      for (int j = 0; j < 16; j++) {
+        if ((bl[j] >> lane) & 1u) region[o + __popc(bl[j] & lt)] = v[j];
+        o += __popc(bl[j]);
+      }
     }
-    __syncthreads();
   }
+  __syncthreads();
+  if (tid == 0) a.region_cnt[blockIdx.x] = s_cnt;
   for (int i = tid; i < NB2; i += 256) {
     const u32 c = shist[i];
     if (c) atomicAdd(&a.ctrl->selD.hist2[i], (ull)c);
   }
 }
 
-// Pass 3 of kth(D) over the compacted bucket; the last CTA resolves theta.
-__global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf) {
+// Pass 3 of kth(D) over the compacted bucket regions; the last CTA resolves theta.
+__global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
+                                                const u32* __restrict__ region_cnt, u32 nregions, u64 R) {
   __shared__ u32 shist[NB3];
   __shared__ DigitResult r2, r3;
   __shared__ ull scratch[8];
@@ -105,10 +106,13 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   find_digit<NB2>(ctrl->selD.hist2, r1.rem, &r2, scratch);
   if (blockIdx.x == 0 && tid == 0) ctrl->selD.r2 = r2;
   const u32 b2 = r2.digit;
-  const u64 m = r1.cnt;
-  for (u64 i = (u64)blockIdx.x * 256 + tid; i < m; i += (u64)gridDim.x * 256) {
-    const u32 x = selbuf[i];
-    if (dig2(x) == b2) atomicAdd(&shist[dig3(x)], 1u);
+  for (u32 g = blockIdx.x; g < nregions; g += gridDim.x) {
+    const u32 cnt = region_cnt[g];
+    const u32* reg = selbuf + (u64)g * R;
+    for (u32 i = tid; i < cnt; i += 256) {
+      const u32 x = reg[i];
+      if (dig2(x) == b2) atomicAdd(&shist[dig3(x)], 1u);
+    }
   }
   __syncthreads();
   for (int i = tid; i < NB3; i += 256) {
@@ -150,8 +154,7 @@ struct SelArgs {
 };
 
 __device__ __forceinline__ bool sel_skip(const SelArgs& a) {
-  return a.check_path &&
-         (ld_volatile_u32(&a.ctrl->res.path) != PATH_SELECT || ld_volatile_u32(&a.ctrl->small_done) != 0);
+  return a.check_path && ld_volatile_u32(&a.ctrl->big_mode) != BIG_SELECT;
 }
 __device__ __forceinline__ u64 sel_count(const SelArgs& a) { return a.m_dev ? (u64)*a.m_dev : a.m_host; }
 
@@ -187,20 +190,45 @@ __global__ void __launch_bounds__(256) sel_pass2(SelArgs a) {
   __shared__ u32 shist[NB2];
   __shared__ DigitResult r1;
   __shared__ ull scratch[8];
+  __shared__ u32 s_wcnt[8];
+  __shared__ ull s_base;
   for (int i = threadIdx.x; i < NB2; i += 256) shist[i] = 0;
   find_digit<NB1>(a.sel->hist1, a.k, &r1, scratch);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.sel->r1 = r1;
   const u32 b1 = r1.digit;
   const u64 m = sel_count(a);
-  const u64 stride = (u64)gridDim.x * 256;
-  const u64 m_pad = (m + 31) & ~31ull;  // whole warps for warp_append
-  for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < m_pad; i += stride) {
-    const u32 x = i < m ? to_key<MODE>(a.keys[i]) : 0u;
-    const bool p = i < m && dig1(x) == b1;
-    if (p) atomicAdd(&shist[dig2(x)], 1u);
-    warp_append(a.selbuf, &a.sel->buf_count, x, p);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 lt = lanemask_lt();
+  // tiles of 256 x 8 keys; one global atomic per tile reserves the slots
+  const u64 T = (m + 2047) / 2048;
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    u32 v[8], bl[8], cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const u64 i = tile * 2048 + (u64)warp * 256 + (u64)j * 32 + lane;
+      v[j] = i < m ? to_key<MODE>(a.keys[i]) : 0u;
+      const bool p = i < m && dig1(v[j]) == b1;
+      bl[j] = __ballot_sync(FULL, p);
+      cnt += __popc(bl[j]);
+      if (p) atomicAdd(&shist[dig2(v[j])], 1u);
+    }
+    if (lane == 0) s_wcnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u32 tot = 0;
+      for (int w = 0; w < 8; w++) tot += s_wcnt[w];
+      s_base = tot ? atomicAdd(&a.sel->buf_count, (ull)tot) : 0ull;
+    }
+    __syncthreads();
+    u64 o = s_base;
+    for (int w = 0; w < warp; w++) o += s_wcnt[w];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      if ((bl[j] >> lane) & 1u) a.selbuf[o + __popc(bl[j] & lt)] = v[j];
+      o += __popc(bl[j]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   for (int i = threadIdx.x; i < NB2; i += 256) {
     const u32 v = shist[i];
     if (v) atomicAdd(&a.sel->hist2[i], (ull)v);
