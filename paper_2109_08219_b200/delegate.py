@@ -50,6 +50,7 @@ def _check_args(n: int, alpha: int, beta: int) -> int:
 def extract_delegates(v, alpha: int, beta: int, *, stats: WorkloadStats | None = None,
                       largest: bool = True) -> DelegateVector:
     """Top-beta delegates of every 2**alpha subrange (delegate.py:142-155)."""
+    _native.load()
     dv = _device.to_device(v)
     _check_args(dv.n, alpha, beta)
     lib = _native.load()

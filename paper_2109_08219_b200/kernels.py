@@ -60,6 +60,7 @@ def radix_topk(values, k, *, skip_last=False, digit_bits=RADIX_BITS, tags=None, 
     if digit_bits < 1 or 32 % digit_bits:
         raise ValueError(f"digit_bits={digit_bits} must divide 32")
     del states
+    _native.load()
     dv = _device.to_device(values)
     if not 1 <= k <= dv.n:
         raise InvalidK(f"k={k} outside [1, {dv.n}]")

@@ -153,6 +153,7 @@ def dr_topk(v, cfg: PipelineConfig, *, stats: WorkloadStats | None = None, exact
     ``cfg.largest``), int64 indices with ties broken by lowest index,
     ``threshold == values[-1]`` and the work counters.
     """
+    _native.load()  # fails loudly (NativeUnavailable) without libdtopk.so or a CUDA device
     dv = _device.to_device(v)
     stats = stats if stats is not None else WorkloadStats()
     plan = DrTopK(dv.n, cfg, dv.code, dv.out_dtype, dv.device, exact_stats=exact_stats)

@@ -15,13 +15,9 @@ import pytest
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
 
-# The reference's 16-element worked example (pkg/tests/conftest.py:10-18):
-# four subranges of four; subrange 2's top two are {3210, 3000}.
-FIGURE_VECTOR = np.array(
-    [101, 2001, 3012, 1323, 2313, 878, 1500, 450, 3000, 1002, 3210, 2500, 2321, 700, 1900, 1100],
-    dtype=np.uint32,
-)
+from dtopk_testlib import FIGURE_VECTOR  # noqa: E402
 
 GOLDEN = ROOT / "tests" / "golden" / "golden.npz"
 

@@ -1,0 +1,185 @@
+"""CPU: host-side drop-in logic and the C-ABI boundary (no GPU compute).
+
+Config semantics restate the reference's pkg/tests/test_core.py and
+test_tuning.py anchors; the boundary tests check that libdtopk.so loads and
+exports every symbol include/dtopk.h declares.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+import paper_2109_08219_b200 as dtopk
+from paper_2109_08219_b200 import _native
+from paper_2109_08219_b200.core import (
+    EmptyInput,
+    InvalidBeta,
+    InvalidK,
+    PipelineConfig,
+    WorkloadStats,
+    delegate_vector_len,
+    effective_beta,
+    validate_config,
+)
+from dtopk_testlib import ROOT
+
+
+class TestValidateConfig:
+    def test_auto_alpha_anchors(self):
+        # test_core.py:22-30, test_tuning.py:67-91
+        assert validate_config(PipelineConfig(k=2**24), 2**30).alpha == 4
+        assert validate_config(PipelineConfig(k=2**19), 2**30).alpha == 7
+        assert dtopk.auto_alpha(2**30, 2**24) == 4
+        assert dtopk.auto_alpha(2**30, 2**19) == 7
+        assert dtopk.auto_alpha(2**24, 2**10) == 8
+        # the bench sweep
+        for k, a in [(1, 16), (2**7, 13), (2**10, 11), (2**13, 10), (2**16, 8), (2**18, 7), (2**20, 6)]:
+            assert validate_config(PipelineConfig(k=k), 2**30).alpha == a
+
+    def test_alpha_ignored_unless_auto_alpha_false(self):
+        # core.py:165 quirk kept: PipelineConfig(k=5, alpha=3) re-tunes
+        assert validate_config(PipelineConfig(k=5, alpha=3), 1000).alpha == 5
+        assert validate_config(PipelineConfig(k=5, alpha=3, auto_alpha=False), 1000).alpha == 3
+
+    def test_fallbacks(self):
+        assert validate_config(PipelineConfig(k=1, alpha=0, auto_alpha=False), 1).direct_fallback
+        assert validate_config(PipelineConfig(k=2**10), 2**10).direct_fallback
+        assert validate_config(PipelineConfig(k=100, alpha=6, beta=2, auto_alpha=False), 1024).direct_fallback
+
+    def test_clamps(self):
+        assert validate_config(PipelineConfig(k=4, alpha=2, beta=9, auto_alpha=False), 64).beta == 3
+        assert validate_config(PipelineConfig(k=2, alpha=30, auto_alpha=False), 64).alpha == 6
+        assert effective_beta(2, 0) == 1 and effective_beta(2, 1) == 1 and effective_beta(9, 3) == 7
+
+    def test_idempotent(self):
+        for k, n, alpha, auto in [(7, 500, None, True), (3, 64, 4, False), (64, 64, 1, False)]:
+            once = validate_config(PipelineConfig(k=k, alpha=alpha, auto_alpha=auto), n)
+            assert validate_config(once, n) == once
+
+    def test_errors(self):
+        with pytest.raises(InvalidK):
+            validate_config(PipelineConfig(k=0), 10)
+        with pytest.raises(InvalidK):
+            validate_config(PipelineConfig(k=11), 10)
+        with pytest.raises(EmptyInput):
+            validate_config(PipelineConfig(k=1), 0)
+        with pytest.raises(InvalidBeta):
+            validate_config(PipelineConfig(k=1, beta=0), 10)
+        with pytest.raises(InvalidK):
+            validate_config(PipelineConfig(k=100, backend="bitonic"), 1024)
+        with pytest.raises(ValueError):
+            validate_config(PipelineConfig(k=1, backend="quick"), 10)
+        validate_config(PipelineConfig(k=128, backend="bitonic"), 1024)
+
+    def test_matches_reference_formula_against_oracle(self, oracle_mod, rng):
+        for _ in range(300):
+            n = int(rng.integers(1, 2**31))
+            k = int(rng.integers(1, n + 1))
+            beta = int(rng.integers(1, 5))
+            assert dtopk.auto_alpha(n, k, beta=beta) == oracle_mod.auto_alpha(n, k, 3.0, beta)
+
+
+def test_delegate_len_formula(rng):
+    for _ in range(50):
+        n = int(rng.integers(1, 10_000))
+        alpha = int(rng.integers(0, n.bit_length()))
+        beta = int(rng.integers(1, 5))
+        assert delegate_vector_len(n, alpha, beta) == beta * -(-n // (1 << alpha))
+
+
+def test_stats_thread_safe():
+    import threading
+
+    stats = WorkloadStats()
+
+    def bump():
+        for _ in range(10_000):
+            stats.add_read(1)
+            stats.add_written(2)
+            stats.add_stage_nanos("FirstK", 3)
+
+    ts = [threading.Thread(target=bump) for _ in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert stats.elements_read == 40_000 and stats.elements_written == 80_000
+    assert stats.total_nanos() == 120_000
+
+
+def test_public_names_match_reference_surface():
+    # the drop-in exports the reference's hot-path names (pkg/src/dtopk/__init__.py)
+    for name in ["PipelineConfig", "TopKResult", "WorkloadStats", "DtopkError", "InvalidK", "EmptyInput",
+                 "InvalidBeta", "validate_config", "dr_topk", "first_topk", "concatenate_filtered",
+                 "extract_delegates", "extract_delegates_blocked", "DelegateVector", "radix_topk",
+                 "auto_alpha", "plan", "WorkerFailed", "BACKENDS", "ELEMENT_DTYPE", "KeyedEntry",
+                 "QualificationReport", "PartitionPlan"]:
+        assert hasattr(dtopk, name), name
+
+
+# ---------------------------------------------------------------- C-ABI boundary
+def _header_symbols():
+    text = (ROOT / "include" / "dtopk.h").read_text()
+    return sorted(set(re.findall(r"\b(dtopk_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(str(_native.LIB_PATH))
+    syms = _header_symbols()
+    assert "dtopk_select" in syms and len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) <= set(_native.EXPORTS), set(syms) - set(_native.EXPORTS)
+
+
+def test_library_host_only_entry_points():
+    lib = _native.load(require_cuda=False)
+    assert lib.dtopk_version().startswith(b"dtopk-b200")
+    assert lib.dtopk_result_offset() == 0
+    assert ctypes.sizeof(_native.DtopkResult) == 104
+    # workspace sizing is host arithmetic
+    ws1 = lib.dtopk_workspace_bytes(1 << 30, 1024, 11, 2, 0)
+    ws2 = lib.dtopk_workspace_bytes(1 << 30, 1 << 20, 6, 2, 0)
+    assert 0 < ws1 < ws2 < 8 * 2**30
+    assert lib.dtopk_workspace_bytes(1 << 20, 600, 0, 1, 1) > 0
+
+
+def test_status_codes_raise_reference_exceptions():
+    with pytest.raises(EmptyInput):
+        _native.check(_native.EMPTY_INPUT, "x")
+    with pytest.raises(InvalidK):
+        _native.check(_native.INVALID_K, "x")
+    with pytest.raises(InvalidBeta):
+        _native.check(_native.INVALID_BETA, "x")
+    with pytest.raises(ValueError):
+        _native.check(_native.INVALID_ARG, "x")
+    with pytest.raises(RuntimeError):
+        _native.check(_native.CUDA_ERROR, "x")
+    _native.check(_native.OK, "x")
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(_native.NativeUnavailable):
+        dtopk.dr_topk(np.arange(100, dtype=np.uint32), PipelineConfig(k=5))
+
+
+def test_plan_arithmetic():
+    # pkg/tests/test_distributed.py:17-52
+    p = dtopk.plan(2**26, 128, workers=4, max_resident=2**26)
+    assert len(p.partitions) == 4 and p.partition_len == 2**24
+    assert all(x.resident for x in p.partitions)
+    p = dtopk.plan(2**28, 128, workers=2, max_resident=2**26)
+    assert p.assignments == {0: [0, 2], 1: [1, 3]}
+    assert [x.resident for x in p.partitions] == [True, True, False, False]
+    with pytest.raises(InvalidK):
+        dtopk.plan(2**20, 2**19, workers=8, max_resident=2**26)
+    assert dtopk.shard_bounds(10, 3, 2) == (8, 2)
+    assert sum(dtopk.shard_bounds(1_000_003, 7, r)[1] for r in range(7)) == 1_000_003
