@@ -35,7 +35,7 @@ int num_sms();
 
 struct Layout {
   size_t ctrl, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
-  size_t D, meta, partial, pmeta, selbuf, region_cnt, keepw, rec_sid, rec_d1, rec_meta, rec_x, e_sid, t_sid, t_cnt,
+  size_t D, meta, partial, pmeta, selbuf, region_cnt, keepw, rec, e_sid, t_sid, t_cnt,
       stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
       digit_base, digit_tot, total;
   u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
@@ -90,10 +90,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.selbuf = take(std::max<u64>((u64)L.g2 * L.R2, L.m_emit) * 4);
   L.region_cnt = take((u64)L.g2 * 4);
   L.keepw = take(L.words * 4);
-  L.rec_sid = take(L.S * 4);
-  L.rec_d1 = take(L.S * 4);
-  L.rec_meta = take(L.S * 4);
-  L.rec_x = take(L.S * 4);
+  L.rec = take(L.words * 32 * 16);
   L.e_sid = take(L.cap_e * 4);
   L.t_sid = take(L.S * 4);
   L.t_cnt = take(L.S * 4);
@@ -312,8 +309,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
                 int nsm, void* const* ev) {
   (void)flags;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
-  Records rc{reinterpret_cast<u32*>(ws + L.rec_sid), reinterpret_cast<u32*>(ws + L.rec_d1),
-              reinterpret_cast<u32*>(ws + L.rec_meta), reinterpret_cast<u32*>(ws + L.rec_x)};
+  Records rc{reinterpret_cast<uint4*>(ws + L.rec)};
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
   u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);
   u32* t_cnt = reinterpret_cast<u32*>(ws + L.t_cnt);

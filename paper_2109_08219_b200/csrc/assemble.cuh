@@ -38,15 +38,14 @@ namespace dtopk {
 enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4 };
 
 constexpr int K4_TILE = 8192;   // keys per K4 tile
-constexpr int K5_WPT = 8;       // words (32 subranges each) per K5 thread
+constexpr int K5_WPT = 1;       // words (32 subranges each) per K5 thread
 constexpr int K5_TILE = 256 * K5_WPT;
 constexpr int SMALL_POOL = 8192;  // pools up to this size are finished by one CTA (8 keys per thread)
 
+// One 16-byte record per qualifying subrange: x = sid, y = d_1,
+// z = K1 meta (constant << 31 | p1), w = cls | fq << 3 | (E or T index) << 4.
 struct Records {
-  u32* sid;
-  u32* d1;
-  u32* meta;  // K1 meta: constant << 31 | p1
-  u32* x;     // cls | fq << 3 | (E or T list index) << 4
+  uint4* r;
 };
 
 struct K3Args {
@@ -102,7 +101,7 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
   const u32 lt = lanemask_lt();
   ull st_cand = 0, st_fq = 0, st_pq = 0, st_a = 0;
   u32 dmax = 0, gt_word = 0;
-  constexpr int U = 4;
+  constexpr int U = 8;
   for (u64 w0 = gw * U; w0 < nwords; w0 += nw * U) {
     u32 d1[U], d2[U], dl[U];
 #pragma unroll
@@ -155,10 +154,7 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
         x |= t << 4;
       }
       const u64 slot = w * 32 + __popc(mask & lt);
-      a.rec.sid[slot] = (u32)sid;
-      a.rec.d1[slot] = d1[u];
-      a.rec.meta[slot] = m;
-      a.rec.x[slot] = x;
+      a.rec.r[slot] = make_uint4((u32)sid, d1[u], m, x);
       st_cand++;
       dmax = max(dmax, d1[u]);
       if (fq) st_fq++; else st_pq++;
@@ -453,8 +449,8 @@ struct K5Args {
   u64* lb_eq;
 };
 
-__device__ __forceinline__ void rec_counts(const K5Args& a, u64 slot, u64& g, u64& e) {
-  const u32 x = a.rec.x[slot];
+__device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64& g, u64& e) {
+  const u32 x = rc.w;
   const u32 cls = x & 7u;
   g = 0;
   e = 0;
@@ -463,7 +459,7 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, u64 slot, u64& g, u6
   } else if (cls == CLS_B) {
     e = 1;
   } else if (cls == CLS_C) {
-    e = sub_len(a.rec.sid[slot], a.n, a.alpha);
+    e = sub_len(rc.x, a.n, a.alpha);
   } else if (cls == CLS_T) {
     e = a.t_cnt[x >> 4];
   } else {
@@ -530,9 +526,10 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
 #pragma unroll
     for (int r = 0; r < K5_WPT; r++) {
       const u32 cnt = __popc(masks[r]);
+      const uint4* wr = a.rec.r + (w0 + r) * 32;
       for (u32 q = 0; q < cnt; q++) {
         u64 g, e;
-        rec_counts(a, (w0 + r) * 32 + q, g, e);
+        rec_counts(a, wr[q], g, e);
         tg += g;
         te += e;
       }
@@ -574,19 +571,20 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
 #pragma unroll
     for (int r = 0; r < K5_WPT; r++) {
       const u32 cnt = __popc(masks[r]);
+      const uint4* wr = a.rec.r + (w0 + r) * 32;
       for (u32 q = 0; q < cnt; q++) {
-        const u64 slot = (w0 + r) * 32 + q;
-        const u32 x = a.rec.x[slot];
+        const uint4 rc = wr[q];
+        const u32 x = rc.w;
         const u32 cls = x & 7u;
         const bool fq = (x >> 3) & 1u;
-        const u64 sid = a.rec.sid[slot];
+        const u64 sid = rc.x;
         const u64 base = sid << a.alpha;
         if (cls == CLS_A) {
-          a.gt_keys[gpos] = a.rec.d1[slot];
-          a.gt_idx[gpos] = base + meta_p1(a.rec.meta[slot]);
+          a.gt_keys[gpos] = rc.y;
+          a.gt_idx[gpos] = base + meta_p1(rc.z);
           gpos++;
         } else if (cls == CLS_B) {
-          if (epos < a.k) a.ties[epos] = base + meta_p1(a.rec.meta[slot]);
+          if (epos < a.k) a.ties[epos] = base + meta_p1(rc.z);
           epos++;
         } else if (cls == CLS_C) {
           const u64 len = sub_len(sid, a.n, a.alpha);
