@@ -32,6 +32,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SMALL_POOL = 8192
 METRIC = "top-k keys/sec (N=2^30 u32, k=1..2^20) and % of HBM roofline at 1/2/4/8 B200"
 UNIT = "keys/s"
 
@@ -41,6 +42,23 @@ def _dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of K1 from the committed
+    ncu --set full capture (profiles/<round>/k1_delegates_ncu_full_raw.txt)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "k1_delegates_ncu_full_raw.txt")))
+    if not files:
+        return None
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for line in open(files[-1]):
+        parts = line.split()
+        if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(parts[1]) * units.get(parts[2], 1)
+    return {"bytes": tot, "source": os.path.relpath(files[-1], ROOT)}
 
 
 def _measured_peak():
@@ -203,7 +221,7 @@ def run_ours(args):
         return float(t.item())
 
     cfg = dtopk.PipelineConfig(k=k)
-    plan = DrTopK(n, cfg, _native.DTYPE_U32, torch.uint32, dev, timed=False)
+    plan = DrTopK(n, cfg, _native.DTYPE_U32, torch.uint32, dev, timed=False, use_graph=not args.no_graph)
     stream = torch.cuda.current_stream(dev)
 
     if world == 1:
@@ -229,15 +247,38 @@ def run_ours(args):
         barrier()
         t_start.record(stream)
         for i in range(args.steps):
-            step(ev_arrays[i] if world == 1 else None)
+            step()
         t_end.record(stream)
         barrier()
     launches = lib.dtopk_launch_count() - launches0
     ms = t_start.elapsed_time(t_end) / args.steps
     ms = max_over_ranks(ms)
     value = n * world / (ms * 1e-3)
-
     hdr = plan.header()
+    graph_info = None
+    if world == 1 and plan.use_graph:
+        main_k, tail_k = plan.plan_kernels(v)
+        pool = int(hdr.pool_gt) if hdr.path == _native.PATH_SELECT else int(hdr.k_out)
+        tail_ran = pool > SMALL_POOL  # finish_small handles pools up to SMALL_POOL (csrc/assemble.cuh)
+        launches += args.steps * tail_k if tail_ran else 0
+        graph_info = {"graph_kernels": main_k, "conditional_tail_kernels": tail_k, "tail_ran": tail_ran}
+
+    # timed region B: eager launches with per-step stage events on the launch
+    # stream -> the live duration of K1 (Delegate stage) for the roofline
+    eager_ms = None
+    if world == 1:
+        for _ in range(2):
+            plan.launch(v, stream, events=ev_arrays[0])
+        torch.cuda.synchronize()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for i in range(args.steps):
+            plan.launch(v, stream, events=ev_arrays[i])
+        b1.record(stream)
+        torch.cuda.synchronize()
+        eager_ms = b0.elapsed_time(b1) / args.steps
+
     peak, peak_src = _measured_peak()
     roof = None
     if world == 1:
@@ -252,7 +293,12 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": n * 4, "kernel_ms": k1, "peak_source": peak_src,
             "stage_ms": stage_ms,
             "step_frac": (n * 4 / (ms * 1e-3) / 1e9) / peak,
+            "eager_ms_per_step": eager_ms,
         }
+        traffic = _ncu_traffic()
+        if traffic:
+            roof["traffic"] = traffic["bytes"]
+            roof["traffic_source"] = traffic["source"]
     out = None
     if rank == 0:
         out = {
@@ -269,6 +315,7 @@ def run_ours(args):
             },
             "roofline": roof,
             "gpu_launches": int(launches),
+            "graph": graph_info,
             "clocks": clk.summary(),
             "device_header": {"path": int(hdr.path), "pool_gt": int(hdr.pool_gt),
                               "candidate_subranges": int(hdr.candidate_subranges),
@@ -280,7 +327,8 @@ def run_ours(args):
         sweep = []
         for e in range(0, 21, args.sweep_stride):
             kk = 1 << e
-            p = DrTopK(n, dtopk.PipelineConfig(k=kk), _native.DTYPE_U32, torch.uint32, dev, timed=False)
+            p = DrTopK(n, dtopk.PipelineConfig(k=kk), _native.DTYPE_U32, torch.uint32, dev, timed=False,
+                       use_graph=not args.no_graph)
             for _ in range(3):
                 p.launch(v, stream)
             torch.cuda.synchronize()
@@ -351,6 +399,7 @@ def main():
     ap.add_argument("--sweep-stride", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA-graph plan")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

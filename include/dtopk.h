@@ -104,6 +104,21 @@ dtopk_status dtopk_select(const void* keys, uint64_t n, int dtype, uint64_t k, i
                           void* out_values, int64_t* out_indices, int64_t index_offset,
                           void* ws, size_t ws_bytes, void* stream, void* const* stage_events);
 
+/* A plan fixes every argument of dtopk_select (input, outputs, workspace) and
+ * captures the whole launch sequence into a CUDA graph.  The large-pool tail
+ * sits behind a device-side conditional node that finish_small sets, so for
+ * pools of <= 8192 pairs its kernels are not launched at all.  Replaying the
+ * plan is equivalent to calling dtopk_select with the same arguments. */
+typedef struct dtopk_plan_s* dtopk_plan;
+dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t k, int largest,
+                               int alpha, int beta, int direct, uint32_t flags,
+                               void* out_values, int64_t* out_indices, int64_t index_offset,
+                               void* ws, size_t ws_bytes, dtopk_plan* out_plan);
+dtopk_status dtopk_plan_launch(dtopk_plan plan, void* stream);
+/* kernels in the always-executed part and in the conditional tail */
+void dtopk_plan_kernels(dtopk_plan plan, unsigned long long* main_kernels, unsigned long long* tail_kernels);
+void dtopk_plan_destroy(dtopk_plan plan);
+
 /* First half of dtopk_select (delegate path only): delegates, theta = kth(D).
  * Afterwards dtopk_result.theta_slot holds theta (int64) in device memory. */
 dtopk_status dtopk_select_begin(const void* keys, uint64_t n, int dtype, uint64_t k, int largest,

@@ -11,7 +11,10 @@ import ctypes
 import pathlib
 import threading
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libdtopk.so"
+import os
+
+# DTOPK_LIB overrides the library path (used to A/B kernel variants in profiling runs)
+LIB_PATH = pathlib.Path(os.environ.get("DTOPK_LIB") or pathlib.Path(__file__).resolve().parent / "_lib" / "libdtopk.so")
 
 OK = 0
 EMPTY_INPUT = 1
@@ -87,6 +90,15 @@ EXPORTS = {
         [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
          ctypes.c_void_p],
     ),
+    "dtopk_plan_create": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+         ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+         ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)],
+    ),
+    "dtopk_plan_launch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "dtopk_plan_kernels": (None, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_ulonglong), ctypes.POINTER(ctypes.c_ulonglong)]),
+    "dtopk_plan_destroy": (None, [ctypes.c_void_p]),
     "dtopk_event_create": (ctypes.c_void_p, []),
     "dtopk_event_destroy": (None, [ctypes.c_void_p]),
     "dtopk_event_elapsed_ms": (ctypes.c_float, [ctypes.c_void_p, ctypes.c_void_p]),

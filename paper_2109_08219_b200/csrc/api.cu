@@ -26,7 +26,12 @@ using namespace dtopk;
 namespace {
 
 std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library
-inline void counted(int n = 1) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+thread_local unsigned long long t_launches = 0;  // kernels launched (or captured) by this thread
+inline void counted(int n = 1) {
+  g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed);
+  t_launches += (unsigned long long)n;
+}
+inline unsigned long long dtopk_launch_count_internal() { return t_launches; }
 
 constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
@@ -303,10 +308,20 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
   }
 }
 
+// Graph capture context: when `graph` is set, run_finish ends the main
+// capture after finish_small, adds a conditional IF node set by finish_small
+// and captures the large-pool tail into its body.
+struct GraphCtx {
+  cudaGraph_t graph = nullptr;
+  cudaGraphConditionalHandle cond{};
+  unsigned long long main_kernels = 0, body_kernels = 0;
+  bool ok = true;
+};
+
 template <int MODE>
 void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, const int64_t* theta_override,
                 void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L, cudaStream_t s,
-                int nsm, void* const* ev) {
+                int nsm, void* const* ev, GraphCtx* gc = nullptr) {
   (void)flags;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
   Records rc{reinterpret_cast<uint4*>(ws + L.rec)};
@@ -356,15 +371,48 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
     cudaFuncSetAttribute(finish_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_POOL * 8);
     attr = true;
   }
+  const bool need_tail = std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL;  // pools beyond SMALL_POOL possible
+  const bool cond = gc && need_tail;
   finish_small<MODE><<<1, 1024, SMALL_POOL * 8, s>>>(ctrl, k5.gt_keys, k5.gt_idx, k5.ties,
                                                      reinterpret_cast<u32*>(out_values),
-                                                     reinterpret_cast<long long*>(out_indices), (long long)offset);
+                                                     reinterpret_cast<long long*>(out_indices), (long long)offset,
+                                                     cond ? gc->cond : cudaGraphConditionalHandle{}, cond ? 1 : 0);
   counted();
-  // pools beyond SMALL_POOL are only possible when the caps allow them
-  if (std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL)
+  if (!need_tail) {
+    rec(ev, 4, s);
+    return;
+  }
+  if (!gc) {
     big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices,
                    offset, ws, L, s, nsm);
-  rec(ev, 4, s);
+    rec(ev, 4, s);
+    return;
+  }
+  // graph mode: finish the main capture with a conditional node; capture the tail into its body
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t cg = nullptr;
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = gc->cond;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  gc->ok = gc->ok && cudaStreamGetCaptureInfo(s, &cst, nullptr, &cg, &deps, &ndeps) == cudaSuccess;
+  gc->ok = gc->ok && cudaGraphAddNode(&cnode, gc->graph, deps, ndeps, &cp) == cudaSuccess;
+  gc->ok = gc->ok && cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies) == cudaSuccess;
+  cudaGraph_t done = nullptr;
+  gc->ok = gc->ok && cudaStreamEndCapture(s, &done) == cudaSuccess;
+  gc->main_kernels = dtopk_launch_count_internal();
+  gc->ok = gc->ok &&
+           cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed) == cudaSuccess;
+  big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices, offset,
+                 ws, L, s, nsm);
+  cudaGraph_t body = nullptr;
+  gc->ok = gc->ok && cudaStreamEndCapture(s, &body) == cudaSuccess;
+  gc->body_kernels = dtopk_launch_count_internal() - gc->main_kernels;
 }
 
 template <int MODE>
@@ -410,6 +458,95 @@ size_t dtopk_workspace_bytes(uint64_t n, uint64_t k, int alpha, int beta, int di
 }
 
 size_t dtopk_result_offset(void) { return 0; }
+
+struct dtopk_plan_s {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  unsigned long long main_kernels = 0, body_kernels = 0;
+};
+
+dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha, int beta,
+                               int direct, uint32_t flags, void* out_values, int64_t* out_indices,
+                               int64_t index_offset, void* ws, size_t ws_bytes, dtopk_plan* out_plan) {
+  if (out_plan == nullptr) return DTOPK_INVALID_ARG;
+  *out_plan = nullptr;
+  dtopk_status st = check_common(keys, n, dtype, k);
+  if (st != DTOPK_OK) return st;
+  if (out_values == nullptr || out_indices == nullptr) return DTOPK_INVALID_ARG;
+  if (!direct) {
+    if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
+    if ((u64)beta * ((n + (1ull << alpha) - 1) >> alpha) < k) return DTOPK_INVALID_K;
+  }
+  const Layout L = direct ? make_layout(n, k, 0, 1, 1) : make_layout(n, k, alpha, beta, 0);
+  if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+  // run once eagerly: sets kernel attributes and validates the configuration
+  st = dtopk_select(keys, n, dtype, k, largest, alpha, beta, direct, flags, out_values, out_indices, index_offset, ws,
+                    ws_bytes, nullptr, nullptr);
+  if (st != DTOPK_OK) return st;
+  if (cudaStreamSynchronize(nullptr) != cudaSuccess) return cuda_status();
+  dtopk_plan_s* p = new dtopk_plan_s();
+  GraphCtx gc;
+  bool ok = cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaGraphCreate(&p->graph, 0) == cudaSuccess &&
+            cudaGraphConditionalHandleCreate(&gc.cond, p->graph, 0, cudaGraphCondAssignDefault) == cudaSuccess &&
+            cudaStreamBeginCaptureToGraph(p->cap, p->graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
+                cudaSuccess;
+  if (ok) {
+    gc.graph = p->graph;
+    t_launches = 0;
+    const int nsm = num_sms();
+    const u32* kp = reinterpret_cast<const u32*>(keys);
+    char* w = reinterpret_cast<char*>(ws);
+    cudaStream_t s = p->cap;
+    bool captured_tail = false;
+    if (direct) {
+      DISPATCH_MODE(key_mode(dtype, largest), run_direct, kp, n, k, out_values, out_indices, index_offset, w, L, s,
+                    nsm, nullptr);
+    } else {
+      DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, nullptr);
+      DISPATCH_MODE(key_mode(dtype, largest), run_finish, kp, n, k, alpha, beta, flags, nullptr, out_values,
+                    out_indices, index_offset, w, L, s, nsm, nullptr, &gc);
+      captured_tail = gc.main_kernels != 0;
+    }
+    if (!captured_tail) {
+      cudaGraph_t g = nullptr;
+      ok = cudaStreamEndCapture(s, &g) == cudaSuccess;
+      gc.main_kernels = t_launches;
+    }
+    ok = ok && gc.ok && cudaGraphInstantiate(&p->exec, p->graph, 0) == cudaSuccess;
+    p->main_kernels = gc.main_kernels;
+    p->body_kernels = gc.body_kernels;
+  }
+  if (!ok) {
+    cudaGetLastError();
+    dtopk_plan_destroy(p);
+    return DTOPK_CUDA_ERROR;
+  }
+  *out_plan = p;
+  return DTOPK_OK;
+}
+
+dtopk_status dtopk_plan_launch(dtopk_plan plan, void* stream) {
+  if (plan == nullptr || plan->exec == nullptr) return DTOPK_INVALID_ARG;
+  if (cudaGraphLaunch(plan->exec, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess) return cuda_status();
+  counted((int)plan->main_kernels);
+  return DTOPK_OK;
+}
+
+void dtopk_plan_kernels(dtopk_plan plan, unsigned long long* main_kernels, unsigned long long* tail_kernels) {
+  if (plan == nullptr) return;
+  if (main_kernels) *main_kernels = plan->main_kernels;
+  if (tail_kernels) *tail_kernels = plan->body_kernels;
+}
+
+void dtopk_plan_destroy(dtopk_plan plan) {
+  if (plan == nullptr) return;
+  if (plan->exec) cudaGraphExecDestroy(plan->exec);
+  if (plan->graph) cudaGraphDestroy(plan->graph);
+  if (plan->cap) cudaStreamDestroy(plan->cap);
+  delete plan;
+}
 
 int dtopk_num_sms(void) { return num_sms(); }
 

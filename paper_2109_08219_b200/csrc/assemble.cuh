@@ -751,15 +751,19 @@ __device__ __forceinline__ void finish_small_r(Ctrl* ctrl, u64 m, u64 ko, u64 G,
 // (P_gt, plus the ties on the merge path) by (key desc, position asc) and
 // writes the first k_out pairs in the input dtype.  Positions follow index
 // order, so this is the (key desc, index asc) order of the reference tie rule.
+// In a CUDA graph (use_cond != 0) it also sets the conditional that gates the
+// large-pool tail, so that tail's kernels are not even launched when unneeded.
 template <int MODE>
 __global__ void __launch_bounds__(1024) finish_small(Ctrl* ctrl, const u32* __restrict__ gt_keys,
                                                      const u64* __restrict__ gt_idx, const u64* __restrict__ ties,
                                                      u32* __restrict__ ov, long long* __restrict__ oi,
-                                                     long long offset) {
+                                                     long long offset, cudaGraphConditionalHandle cond,
+                                                     int use_cond) {
   extern __shared__ unsigned long long sk[];
   const u32 path = ctrl->res.path;
   const u64 G = ctrl->res.pool_gt;
   const u64 m = path == PATH_SELECT ? G : ctrl->res.k_out;
+  if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(cond, m > (u64)SMALL_POOL ? 1u : 0u);
   if (m > (u64)SMALL_POOL || m == 0) return;
   const u64 ko = ctrl->res.k_out;
   const u32 theta = ctrl->res.theta;

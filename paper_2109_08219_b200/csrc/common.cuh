@@ -153,6 +153,11 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, u32 byte
       : "memory");
 }
 
+// Bulk prefetch of global memory into L2 (no shared-memory destination).
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, u32 bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ u64 ld_acquire(const u64* p) {
   u64 v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

@@ -23,7 +23,14 @@ namespace dtopk {
 constexpr int K1_CHUNK = 2048;    // keys per stage = one warp's unit of work (8 KiB)
 constexpr int K1_LOG_CHUNK = 11;
 constexpr int K1_CWARPS = 8;      // consumer warps
-constexpr int K1_STAGES = 16;     // two stages in flight per consumer warp
+#ifndef DTOPK_K1_STAGES
+#define DTOPK_K1_STAGES 16
+#endif
+#ifndef DTOPK_K1_PREFETCH
+#define DTOPK_K1_PREFETCH 0
+#endif
+constexpr int K1_STAGES = DTOPK_K1_STAGES;  // stages in flight (a multiple of the consumer warps)
+constexpr int K1_PREFETCH = DTOPK_K1_PREFETCH;  // chunks prefetched into L2 ahead of the TMA ring
 constexpr int K1_THREADS = (K1_CWARPS + 1) * 32;
 constexpr size_t K1_SMEM = (size_t)K1_STAGES * K1_CHUNK * 4 + 2 * K1_STAGES * 8 + NB1 * 4;
 
@@ -322,6 +329,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_delegates(K1Args a) {
         const u64 start = c << K1_LOG_CHUNK;
         const u64 cnt = min((u64)K1_CHUNK, a.n - start);
         const u32 bytes = (u32)(cnt * 4u) & ~15u;
+        if constexpr (K1_PREFETCH > 0) {
+          const u64 cp = c + (u64)K1_PREFETCH * gridDim.x;
+          if (cp < nch && ((cp + 1) << K1_LOG_CHUNK) <= a.n) l2_prefetch_bulk(a.keys + (cp << K1_LOG_CHUNK), K1_CHUNK * 4u);
+        }
         if (bytes) {
           mbar_arrive_expect_tx(&full[s], bytes);
           tma_load_1d(stages + (size_t)s * K1_CHUNK, a.keys + start, bytes, &full[s]);

@@ -74,7 +74,7 @@ class DrTopK:
     """
 
     def __init__(self, n: int, cfg: PipelineConfig, code: int, out_dtype: torch.dtype, device, *,
-                 exact_stats: bool = False, timed: bool = True):
+                 exact_stats: bool = False, timed: bool = True, use_graph: bool = False):
         self.lib = _native.load()
         self.n = int(n)
         self.cfg = validate_config(cfg, self.n)
@@ -87,11 +87,44 @@ class DrTopK:
         self.values = torch.empty(c.k, dtype=out_dtype, device=self.device)
         self.indices = torch.empty(c.k, dtype=torch.int64, device=self.device)
         self.events = _stage_events() if timed else None
+        self.use_graph = use_graph
+        self._plans = {}  # (keys ptr, index offset) -> dtopk_plan (CUDA graph)
+
+    def _plan(self, keys: torch.Tensor, index_offset: int):
+        key = (keys.data_ptr(), int(index_offset))
+        h = self._plans.get(key)
+        if h is None:
+            c = self.cfg
+            out = ctypes.c_void_p()
+            with torch.cuda.device(self.device):
+                st = self.lib.dtopk_plan_create(
+                    keys.data_ptr(), self.n, self.code, c.k, int(c.largest), c.alpha, c.beta,
+                    int(c.direct_fallback), self.flags, self.values.data_ptr(), self.indices.data_ptr(),
+                    int(index_offset), self.ws.data_ptr(), self.ws_bytes, ctypes.byref(out))
+            _native.check(st, "dtopk_plan_create")
+            h = out.value
+            self._plans[key] = h
+        return h
+
+    def plan_kernels(self, keys: torch.Tensor, index_offset: int = 0) -> tuple[int, int]:
+        main, tail = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+        self.lib.dtopk_plan_kernels(self._plan(keys, index_offset), ctypes.byref(main), ctypes.byref(tail))
+        return int(main.value), int(tail.value)
+
+    def __del__(self):
+        lib = getattr(self, "lib", None)
+        for h in getattr(self, "_plans", {}).values():
+            if lib is not None and h:
+                lib.dtopk_plan_destroy(h)
 
     def launch(self, keys: torch.Tensor, stream: torch.cuda.Stream | None = None, index_offset: int = 0,
                events=None) -> None:
         c = self.cfg
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self.use_graph and events is None:
+            _native.check(self.lib.dtopk_plan_launch(self._plan(keys, index_offset), s.cuda_stream),
+                          "dtopk_plan_launch")
+            return
         st = self.lib.dtopk_select(
             keys.data_ptr(), self.n, self.code, c.k, int(c.largest), c.alpha, c.beta, int(c.direct_fallback),
             self.flags, self.values.data_ptr(), self.indices.data_ptr(), int(index_offset), self.ws.data_ptr(),
