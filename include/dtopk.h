@@ -63,7 +63,7 @@ typedef struct {
   uint64_t fully_qualified;       /* beta-th delegate >= theta     (pipeline.py:104-108) */
   uint64_t partially_qualified;   /* max >= theta > beta-th delegate (pipeline.py:109,205) */
   uint64_t concatenated_len;      /* |C|: elements >= theta of fully qualified subranges */
-  uint64_t concat_skipped_fq;     /* FQ subranges not re-read (ties already satisfied);
+  uint64_t concat_skipped_fq;     /* work skipped because the first k ties were already placed;
                                      concatenated_len is exact iff this is 0          */
   uint64_t elements_reread;       /* input elements re-read by the concatenation stage */
   uint64_t pool_gt;               /* G: elements strictly above theta                  */

@@ -40,8 +40,8 @@ int num_sms();
 
 struct Layout {
   size_t ctrl, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
-  size_t D, meta, partial, pmeta, selbuf, region_cnt, keepw, rec, e_sid, t_sid, t_cnt,
-      stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
+  size_t D, meta, partial, pmeta, selbuf, region_cnt, keepw, wsum, rec, e_sid, t_sid, t_cnt,
+      stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, e_gpos, e_epos, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
       digit_base, digit_tot, total;
   u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
       sort_cap;
@@ -95,6 +95,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.selbuf = take(std::max<u64>((u64)L.g2 * L.R2, L.m_emit) * 4);
   L.region_cnt = take((u64)L.g2 * 4);
   L.keepw = take(L.words * 4);
+  L.wsum = take(L.words * 8);
   L.rec = take(L.words * 32 * 16);
   L.e_sid = take(L.cap_e * 4);
   L.t_sid = take(L.S * 4);
@@ -104,6 +105,8 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.seg_gt = take(L.nseg * 4);
   L.seg_eq = take(L.nseg * 4);
   L.d_sid = take(L.cap_d * 4);
+  L.e_gpos = take(L.cap_e * 8);
+  L.e_epos = take(L.cap_e * 8);
   L.d_pos = take(L.cap_d * 8);
   L.d_need = take(L.cap_d * 4);
   L.gt_keys = take(L.cap_gt * 4);
@@ -322,15 +325,15 @@ template <int MODE>
 void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, const int64_t* theta_override,
                 void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L, cudaStream_t s,
                 int nsm, void* const* ev, GraphCtx* gc = nullptr) {
-  (void)flags;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
   Records rc{reinterpret_cast<uint4*>(ws + L.rec)};
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
   u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);
   u32* t_cnt = reinterpret_cast<u32*>(ws + L.t_cnt);
   u32* keepw = reinterpret_cast<u32*>(ws + L.keepw);
+  uint2* wsum = reinterpret_cast<uint2*>(ws + L.wsum);
   K3Args k3{reinterpret_cast<const u32*>(ws + L.D), reinterpret_cast<const u32*>(ws + L.meta),
-            L.S, n, alpha, beta, ctrl, theta_override, rc, keepw, e_sid, t_sid, L.cap_e};
+            L.S, n, alpha, beta, ctrl, theta_override, rc, keepw, wsum, e_sid, t_sid, t_cnt, L.cap_e};
   k3_classify<<<grid_for((L.words + 31) / 32, nsm * 8), 256, 0, s>>>(k3);
   counted();
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
@@ -338,11 +341,15 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
             reinterpret_cast<u32*>(ws + L.seg_eq), L.cap_e};
   k4_read<MODE><<<grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4), 256, 0, s>>>(k4);
   counted();
-  k4t_count<MODE><<<grid_for((L.S + 7) / 8, nsm * 4), 256, 0, s>>>(keys, n, alpha, ctrl, t_sid, t_cnt);
+  const int exact = (flags & DTOPK_FLAG_EXACT_STATS) ? 1 : 0;
+  K4TArgs k4t{keys, n,  L.S,   alpha, k, ctrl, t_sid, t_cnt, keepw, wsum, rc.r, reinterpret_cast<const u32*>(ws + L.seg_eq),
+              exact};
+  k4t_count<MODE><<<grid_for((L.S + 7) / 8, nsm * 4), 256, 0, s>>>(k4t);
   counted();
   K5Args k5{ctrl,
             rc,
             keepw,
+            wsum,
             L.S,
             n,
             alpha,
@@ -358,9 +365,16 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
             reinterpret_cast<u32*>(ws + L.d_sid),
             reinterpret_cast<u64*>(ws + L.d_pos),
             reinterpret_cast<u32*>(ws + L.d_need),
+            reinterpret_cast<u64*>(ws + L.e_gpos),
+            reinterpret_cast<u64*>(ws + L.e_epos),
             reinterpret_cast<u64*>(ws + L.lb_k5g),
-            reinterpret_cast<u64*>(ws + L.lb_k5e)};
+            reinterpret_cast<u64*>(ws + L.lb_k5e),
+            exact};
   k5_assemble<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
+  counted();
+  k5b_copy<<<grid_for((L.nseg + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, alpha, k, k5.stg_key, k5.stg_idx, k5.seg_gt,
+                                                               k5.seg_eq, k5.e_gpos, k5.e_epos, L.cap_e,
+                                                               k5.gt_keys, k5.gt_idx, k5.ties);
   counted();
   k6_ties<MODE><<<grid_for((L.cap_d + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, keys, n, alpha, k5.d_sid, k5.d_pos,
                                                                       k5.d_need, k5.ties);

@@ -59,10 +59,14 @@ struct K3Args {
   const int64_t* theta_override;
   Records rec;
   u32* keepw;  // [S/32] keep mask of every 32-subrange word
+  uint2* wsum; // [S/32] per word: x = keys > theta, y = ties | 1 << 31 if an E/T record needs K4/K4T counts
   u32* e_sid;  // [nE] subrange of each E candidate
   u32* t_sid;  // [nT] subrange of each T candidate
+  u32* t_cnt;  // [nT] ties of each T candidate (zeroed here, filled by K4T)
   u64 cap_e;
 };
+
+__device__ __forceinline__ u32 sat_add31(u32 a, u64 b) { return (u32)min((u64)a + b, (u64)0x7fffffffu); }
 
 __device__ __forceinline__ u64 sub_len(u64 sid, u64 n, int alpha) {
   const u64 W = 1ull << alpha;
@@ -128,6 +132,29 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
       const bool keep = sid < a.S && d1[u] >= theta;
       const u32 mask = __ballot_sync(FULL, keep);
       if (lane == 0) a.keepw[w] = mask;
+      if (!mask) {
+        if (lane == 0) a.wsum[w] = make_uint2(0u, 0u);
+        continue;
+      }
+      // per-word known counts: A -> 1 key > theta, B -> 1 tie, C -> len ties;
+      // E / T set the "needs records" flag (counts come from K4 / K4T)
+      u32 kg = 0, ke = 0, kf = 0;
+      if (keep) {
+        const u32 m0 = a.meta[sid];
+        const u32 c0 = classify(d1[u], d2[u], m0, theta, beta);
+        if (c0 == CLS_A) kg = 1;
+        else if (c0 == CLS_B) ke = 1;
+        else if (c0 == CLS_C) ke = (u32)min(sub_len(sid, a.n, a.alpha), (u64)0x7fffffffu);
+        else kf = 1;
+      }
+      kg = __reduce_add_sync(FULL, kg);
+      kf = __reduce_or_sync(FULL, kf);
+      {
+        u64 ew = ke;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ew += __shfl_xor_sync(FULL, ew, o);
+        if (lane == 0) a.wsum[w] = make_uint2(kg, sat_add31(0, ew) | (kf << 31));
+      }
       if (!keep) continue;
       const u32 m = a.meta[sid];
       const u32 cls = classify(d1[u], d2[u], m, theta, beta);
@@ -151,6 +178,7 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
       } else if (cls == CLS_T) {
         const u32 t = t0 + __popc(bt & lt);
         a.t_sid[t] = (u32)sid;
+        a.t_cnt[t] = 0;
         x |= t << 4;
       }
       const u64 slot = w * 32 + __popc(mask & lt);
@@ -391,37 +419,104 @@ __global__ void __launch_bounds__(256) k4_read(K4Args a) {
   if (lane == 0 && st_gt) atomicAdd(&ctrl->sumEgt, st_gt);
 }
 
-// K4T: count the ties of every T candidate (d_1 == theta, max not unique,
-// subrange not constant): one warp per candidate (one thread when W < 64).
+// K4T: count the ties of T candidates (d_1 == theta, max not unique,
+// subrange not constant).  Few T candidates: count them all in parallel (one
+// warp each).  Many (tie-heavy inputs): walk the 32-subrange words in index
+// order in chunks taken by ticket, and stop taking chunks once the completed
+// chunks already hold k ties -- every later tie lands beyond position k, so
+// its count is never needed (it stays 0; concatenated_len is then a lower
+// bound, flagged through concat_skipped_fq).
+constexpr u32 K4T_PARALLEL_MAX = 4096;
+constexpr u32 K4T_WORDS_PER_TICKET = 8;
+
 template <int MODE>
-__global__ void __launch_bounds__(256) k4t_count(const u32* __restrict__ keys, u64 n, int alpha, Ctrl* ctrl,
-                                                 const u32* __restrict__ t_sid, u32* __restrict__ t_cnt) {
+__device__ __forceinline__ u32 count_ties_warp(const u32* __restrict__ keys, u64 n, int alpha, u64 sid, u32 theta) {
+  const int lane = threadIdx.x & 31;
+  const u64 b = sid << alpha;
+  const u64 len = min((u64)(1ull << alpha), (u64)(n - b));
+  u32 c = 0;
+  for (u64 e = lane; e < len; e += 32) c += to_key<MODE>(keys[b + e]) == theta;
+  return __reduce_add_sync(FULL, c);
+}
+
+struct K4TArgs {
+  const u32* keys;
+  u64 n;
+  u64 S;
+  int alpha;
+  u64 k;
+  Ctrl* ctrl;
+  const u32* t_sid;
+  u32* t_cnt;
+  const u32* keepw;
+  const uint2* wsum;
+  const uint4* rec;
+  const u32* seg_eq;
+  int exact;  // DTOPK_FLAG_EXACT_STATS: count every T candidate
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
+  __shared__ u64 s_chunk;
+  __shared__ u32 s_eq[8];
+  Ctrl* ctrl = a.ctrl;
   const u32 theta = ctrl->res.theta;
   const u64 nT = ctrl->nT;
-  const u64 W = 1ull << alpha;
-  const int lane = threadIdx.x & 31;
-  if (W < 64) {
-    for (u64 t = (u64)blockIdx.x * 256 + threadIdx.x; t < nT; t += (u64)gridDim.x * 256) {
-      const u64 b = (u64)t_sid[t] << alpha;
-      u32 c = 0;
-      for (u64 e = 0; e < W && b + e < n; e++) c += to_key<MODE>(keys[b + e]) == theta;
-      t_cnt[t] = c;
+  if (nT == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 gw = ((u64)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const u64 nw = ((u64)gridDim.x * 256) >> 5;
+  if (nT <= K4T_PARALLEL_MAX || a.exact) {
+    for (u64 t = gw; t < nT; t += nw) {
+      const u32 c = count_ties_warp<MODE>(a.keys, a.n, a.alpha, a.t_sid[t], theta);
+      if (lane == 0) a.t_cnt[t] = c;
     }
     return;
   }
-  const u64 gw = ((u64)blockIdx.x * 256 + threadIdx.x) >> 5;
-  const u64 nw = ((u64)gridDim.x * 256) >> 5;
-  for (u64 t = gw; t < nT; t += nw) {
-    const u64 b = (u64)t_sid[t] << alpha;
-    const u64 len = min(W, n - b);
-    u32 c = 0;
-    for (u64 e = (u64)lane * 2; e < len; e += 64) {
-      const u32 k0 = to_key<MODE>(keys[b + e]);
-      c += k0 == theta;
-      if (e + 1 < len) c += to_key<MODE>(keys[b + e + 1]) == theta;
+  const u64 nwords = (a.S + 31) / 32;
+  const int lseg = a.alpha < 13 ? a.alpha : 13;
+  const u64 ppc = (1ull << a.alpha) >> lseg;
+  for (;;) {
+    if (threadIdx.x == 0)
+      s_chunk = ld_volatile_u32((const u32*)&ctrl->k4t_eq_done) >= a.k ? ~0ull
+                                                                          : (u64)atomicAdd(&ctrl->k4t_ticket, 1u);
+    __syncthreads();
+    const u64 chunk = s_chunk;
+    if (chunk == ~0ull) {
+      if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, 1ull);
+      break;
     }
-    c = __reduce_add_sync(FULL, c);
-    if (lane == 0) t_cnt[t] = c;
+    if (chunk * K4T_WORDS_PER_TICKET >= nwords) break;
+    // one word per warp: ties of its B/C/E/T records
+    u32 eq = 0;
+    const u64 w = chunk * K4T_WORDS_PER_TICKET + warp;
+    if (w < nwords) {
+      const uint2 sm = a.wsum[w];
+      eq = sm.y & 0x7fffffffu;
+      if (sm.y >> 31) {
+        const u32 cnt = __popc(a.keepw[w]);
+        for (u32 q = 0; q < cnt; q++) {
+          const uint4 rc = a.rec[w * 32 + q];
+          const u32 cls = rc.w & 7u;
+          if (cls == CLS_T) {
+            const u32 c = count_ties_warp<MODE>(a.keys, a.n, a.alpha, rc.x, theta);
+            if (lane == 0) a.t_cnt[rc.w >> 4] = c;
+            eq = (u32)min((u64)eq + c, (u64)0x7fffffffu);
+          } else if (cls == CLS_E) {
+            const u64 e = rc.w >> 4;
+            for (u64 p = 0; p < ppc; p++) eq = (u32)min((u64)eq + a.seg_eq[e * ppc + p], (u64)0x7fffffffu);
+          }
+        }
+      }
+    }
+    if (lane == 0) s_eq[warp] = eq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u64 tot = 0;
+      for (int i = 0; i < 8; i++) tot += s_eq[i];
+      if (tot) atomicAdd(&ctrl->k4t_eq_done, (ull)min(tot, (u64)0xffffffffull));
+    }
+    __syncthreads();
   }
 }
 
@@ -430,6 +525,7 @@ struct K5Args {
   Ctrl* ctrl;
   Records rec;     // word-local record slots
   const u32* keepw;
+  const uint2* wsum;
   u64 S;
   u64 n;
   int alpha;
@@ -445,8 +541,11 @@ struct K5Args {
   u32* d_sid;        // K6 work list: subrange, first tie position, ties needed
   u64* d_pos;
   u32* d_need;
+  u64* e_gpos;       // per E candidate: first slot in P_gt / in the tie list (K5b copies)
+  u64* e_epos;
   u64* lb_gt;
   u64* lb_eq;
+  int exact;         // DTOPK_FLAG_EXACT_STATS: never skip (exact concatenated_len)
 };
 
 __device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64& g, u64& e) {
@@ -486,13 +585,12 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
   const u64 T = (nwords + K5_TILE - 1) / K5_TILE;
   const u64 gt_end = ctrl->gt_rec_end;  // 1 + last word holding elements > theta
   const int lseg = a.alpha < 13 ? a.alpha : 13;
-  const u64 seglen = 1ull << lseg;
   const u64 ppc = (1ull << a.alpha) >> lseg;
-  ull st_concat = 0;
+  ull st_concat = 0, st_skipw = 0;
   for (;;) {
     if (tid == 0) {
       s_tile = atomicAdd(&ctrl->k5_ticket, 1u);
-      s_skip = ld_volatile_u32(&ctrl->ties_full) && s_tile * K5_TILE >= gt_end;
+      s_skip = !a.exact && ld_volatile_u32(&ctrl->ties_full) && s_tile * K5_TILE >= gt_end;
     }
     __syncthreads();
     const u64 tile = s_tile;
@@ -502,6 +600,7 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
       // the final prefix without reading anything
       if (tid == 0) {
         const u64 G = ctrl->nA + ctrl->sumEgt;
+        atomicAdd((ull*)&ctrl->res.concat_skipped_fq, 1ull);  // concatenated_len becomes a lower bound
         st_release(&a.lb_gt[tile], LB_PRE | G);
         st_release(&a.lb_eq[tile], LB_PRE | a.k);
         if (tile == T - 1) {
@@ -522,16 +621,25 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
     u32 masks[K5_WPT];
     u64 tg = 0, te = 0;
 #pragma unroll
-    for (int r = 0; r < K5_WPT; r++) masks[r] = w0 + r < nwords ? a.keepw[w0 + r] : 0u;
-#pragma unroll
     for (int r = 0; r < K5_WPT; r++) {
-      const u32 cnt = __popc(masks[r]);
-      const uint4* wr = a.rec.r + (w0 + r) * 32;
-      for (u32 q = 0; q < cnt; q++) {
-        u64 g, e;
-        rec_counts(a, wr[q], g, e);
-        tg += g;
-        te += e;
+      masks[r] = 0;
+      if (w0 + r < nwords) {
+        const uint2 sm = a.wsum[w0 + r];
+        if (sm.y >> 31) {  // E / T records: exact counts from K4 / K4T
+          masks[r] = a.keepw[w0 + r];
+          const u32 cnt = __popc(masks[r]);
+          const uint4* wr = a.rec.r + (w0 + r) * 32;
+          for (u32 q = 0; q < cnt; q++) {
+            u64 g, e;
+            rec_counts(a, wr[q], g, e);
+            tg += g;
+            te += e;
+          }
+        } else {
+          tg += sm.x;
+          te += sm.y;
+          if (sm.x | sm.y) masks[r] = 0xffffffffu;  // records fetched in phase 2 only if they emit
+        }
       }
     }
     const u64 ig = block_incl_scan_256<u64>(tg, scratch_g);
@@ -570,7 +678,14 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
     u64 gpos = s_gx + ig - tg, epos = s_ex + ie - te;
 #pragma unroll
     for (int r = 0; r < K5_WPT; r++) {
-      const u32 cnt = __popc(masks[r]);
+      if (!masks[r]) continue;
+      const uint2 sm = a.wsum[w0 + r];
+      if (!a.exact && !(sm.y >> 31) && sm.x == 0 && epos >= a.k) {
+        epos += sm.y;  // ties only, all beyond position k: nothing to place
+        st_skipw++;
+        continue;
+      }
+      const u32 cnt = __popc(a.keepw[w0 + r]);
       const uint4* wr = a.rec.r + (w0 + r) * 32;
       for (u32 q = 0; q < cnt; q++) {
         const uint4 rc = wr[q];
@@ -603,24 +718,17 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
           if (fq) st_concat += c1;
           epos += c1;
         } else {
+          // the staged keys of E candidates are copied in parallel by K5b
           const u64 eidx = x >> 4;
           u64 eg = 0, ee = 0;
           for (u64 p = 0; p < ppc; p++) {
-            const u64 sg = eidx * ppc + p;
-            const u32 ng = a.seg_gt[sg], ne = a.seg_eq[sg];
-            const u64 sb = sg << lseg;
-            for (u32 z = 0; z < ng; z++) {
-              a.gt_keys[gpos + z] = a.stg_key[sb + z];
-              a.gt_idx[gpos + z] = a.stg_idx[sb + z];
-            }
-            gpos += ng;
-            eg += ng;
-            for (u32 z = 0; z < ne; z++) {
-              if (epos + z < a.k) a.ties[epos + z] = a.stg_idx[sb + seglen - 1 - z];
-            }
-            epos += ne;
-            ee += ne;
+            eg += a.seg_gt[eidx * ppc + p];
+            ee += a.seg_eq[eidx * ppc + p];
           }
+          a.e_gpos[eidx] = gpos;
+          a.e_epos[eidx] = epos;
+          gpos += eg;
+          epos += ee;
           if (fq) st_concat += eg + ee;
         }
       }
@@ -628,12 +736,45 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
     __syncthreads();
   }
   for (int o = 16; o; o >>= 1) st_concat += __shfl_xor_sync(FULL, st_concat, o);
+  st_skipw = __reduce_add_sync(FULL, (u32)st_skipw);
   if (lane == 0) s_cc[warp] = st_concat;
+  if (lane == 0 && st_skipw) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, st_skipw);
   __syncthreads();
   if (tid == 0) {
     ull t = 0;
     for (int w = 0; w < 8; w++) t += s_cc[w];
     if (t) atomicAdd((ull*)&ctrl->res.concatenated_len, t);
+  }
+}
+
+// K5b: copy the staged keys > theta and ties of every E candidate part to
+// its place in P_gt / the tie list (one warp per part).
+__global__ void __launch_bounds__(256) k5b_copy(Ctrl* ctrl, int alpha, u64 k, const u32* __restrict__ stg_key,
+                                                const u64* __restrict__ stg_idx, const u32* __restrict__ seg_gt,
+                                                const u32* __restrict__ seg_eq, const u64* __restrict__ e_gpos,
+                                                const u64* __restrict__ e_epos, u64 cap_e, u32* __restrict__ gt_keys,
+                                                u64* __restrict__ gt_idx, u64* __restrict__ ties) {
+  const int lane = threadIdx.x & 31;
+  const u64 nE = min((u64)ctrl->nE, cap_e);
+  const int lseg = alpha < 13 ? alpha : 13;
+  const u64 seglen = 1ull << lseg;
+  const u64 ppc = (1ull << alpha) >> lseg;
+  const u64 gw = ((u64)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const u64 nw = ((u64)gridDim.x * 256) >> 5;
+  for (u64 sg = gw; sg < nE * ppc; sg += nw) {
+    const u64 e = sg / ppc, part = sg - e * ppc;
+    u64 go = e_gpos[e], eo = e_epos[e];
+    for (u64 p = 0; p < part; p++) {
+      go += seg_gt[e * ppc + p];
+      eo += seg_eq[e * ppc + p];
+    }
+    const u32 ng = seg_gt[sg], ne = seg_eq[sg];
+    const u64 sb = sg << lseg;
+    for (u32 z = lane; z < ng; z += 32) {
+      gt_keys[go + z] = stg_key[sb + z];
+      gt_idx[go + z] = stg_idx[sb + z];
+    }
+    for (u32 z = lane; z < ne && eo + z < k; z += 32) ties[eo + z] = stg_idx[sb + seglen - 1 - z];
   }
 }
 

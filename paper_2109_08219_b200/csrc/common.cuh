@@ -95,7 +95,8 @@ struct Ctrl {
   u32 k6_count;
   u32 small_done;  // finish_small wrote the answer
   u32 nT;          // class-T records (tie-only, counted by K4T)
-  u32 pad1;
+  u32 k4t_ticket;
+  ull k4t_eq_done; // ties of the word chunks K4T has completed
   // emit and sort of the answer
   u32 em_ticket;
   u32 maxkey;

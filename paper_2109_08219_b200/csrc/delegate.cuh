@@ -81,6 +81,28 @@ __device__ __forceinline__ void acc_keys(Acc<B>& A, const u32 (&x)[4], const u32
     const u32 n2 = max(max(min(A.L[0], t1), A.L[1]), t2);
     A.L[0] = n1;
     A.L[1] = n2;
+  } else if constexpr (B == 3 || B == 4) {
+    // sort the four keys (t1 >= t2 >= t3 >= t4), then merge the two sorted
+    // lists: top-B of L u t without per-key insertion chains
+    const u32 h1 = max(x[0], x[1]), l1 = min(x[0], x[1]);
+    const u32 h2 = max(x[2], x[3]), l2 = min(x[2], x[3]);
+    const u32 t1 = max(h1, h2), m = min(h1, h2), M = max(l1, l2), t4 = min(l1, l2);
+    const u32 t2 = max(m, M), t3 = min(m, M);
+    A.p = t1 > A.L[0] ? q : A.p;
+    if constexpr (B == 3) {
+      const u32 a0 = A.L[0], a1 = A.L[1], a2 = A.L[2];
+      A.L[0] = max(a0, t1);
+      A.L[1] = max(min(a0, t1), max(a1, t2));
+      A.L[2] = max(max(a2, t3), max(min(a0, t2), min(a1, t1)));
+    } else {
+      // bitonic: r_i = max(a_i, t_{3-i}) is bitonic and holds the top 4; sort it
+      const u32 r0 = max(A.L[0], t4), r1 = max(A.L[1], t3), r2 = max(A.L[2], t2), r3 = max(A.L[3], t1);
+      const u32 s0 = max(r0, r2), s2 = min(r0, r2), s1 = max(r1, r3), s3 = min(r1, r3);
+      A.L[0] = max(s0, s1);
+      A.L[1] = min(s0, s1);
+      A.L[2] = max(s2, s3);
+      A.L[3] = min(s2, s3);
+    }
   } else {
     const u32 t1 = max(max(x[0], x[1]), max(x[2], x[3]));
     A.p = t1 > A.L[0] ? q : A.p;

@@ -261,3 +261,31 @@ def test_theta_override_split_path(oracle_mod, cuda):
     ek, ei = oracle_mod.topk_with_indices(v.cpu().numpy(), k)
     np.testing.assert_array_equal(fi.cpu().numpy(), ei)
     np.testing.assert_array_equal(fv.cpu().numpy(), ek)
+
+
+@pytest.mark.parametrize("dist", ["few_distinct", "all_equal", "nd_u32", "ascending"])
+@pytest.mark.parametrize("k", [1, 1000, 1 << 15])
+def test_tie_heavy_default_stats_mode(dist, k, oracle_mod, cuda):
+    """Default mode (no exact stats): K4T's ordered early stop and K5's
+    word skipping must not change values or indices."""
+    v = data.generate(dist, (1 << 22) + 77, seed=3, device=cuda)
+    r = dtopk.dr_topk(v, dtopk.PipelineConfig(k=k))
+    ek, ei = oracle_mod.topk_with_indices(v.cpu().numpy(), k)
+    np.testing.assert_array_equal(r.indices.cpu().numpy(), ei)
+    np.testing.assert_array_equal(r.values.cpu().numpy(), ek)
+
+
+@pytest.mark.parametrize("k", [7, 5000, 70000])
+def test_graph_plan_replay_matches_eager(k, oracle_mod, cuda):
+    from paper_2109_08219_b200 import _native
+    from paper_2109_08219_b200.pipeline import DrTopK
+
+    v = data.generate("uniform", 1 << 22, seed=k, device=cuda)
+    p = DrTopK(v.numel(), dtopk.PipelineConfig(k=k), _native.DTYPE_U32, torch.uint32, cuda, use_graph=True)
+    for _ in range(3):
+        p.launch(v)
+        torch.cuda.synchronize()
+        ek, ei = oracle_mod.topk_with_indices(v.cpu().numpy(), k)
+        np.testing.assert_array_equal(p.indices.cpu().numpy(), ei)
+        np.testing.assert_array_equal(p.values.cpu().numpy(), ek)
+        v.view(torch.int32)[::97] += 1  # new data, same buffer: the plan re-reads it
