@@ -42,7 +42,7 @@ struct Layout {
   size_t ctrl, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
   size_t D, meta, partial, pmeta, selbuf, region_cnt, keepw, wsum, rec, e_sid, t_sid, t_cnt,
       stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, e_gpos, e_epos, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
-      digit_base, digit_tot, total;
+      digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, total;
   u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
       sort_cap;
   u32 g2;
@@ -82,6 +82,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.sort_cap = direct ? k : std::max<u64>(k, std::min<u64>(4 * k, L.cap_gt));
   L.sort_tiles = (L.sort_cap + ST_TILE - 1) / ST_TILE;
   L.ctrl = take(sizeof(Ctrl));
+  L.bk_total = take(L.sort_cap > (u64)SMALL_SORT ? BK_MAX * 4 : 0);
   L.lb_k5g = take(L.k5_tiles * 8);
   L.lb_k5e = take(L.k5_tiles * 8);
   L.lb_emg = take(L.em_tiles * 8);
@@ -119,6 +120,11 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.counts = take(L.sort_tiles * 256 * 4);
   L.digit_base = take(256 * 4);
   L.digit_tot = take(256 * 4);
+  const bool bk = L.sort_cap > (u64)SMALL_SORT;
+  L.bk_count = take(bk ? (u64)BK_CHUNKS * BK_MAX * 4 : 0);
+  L.bk_start = take(bk ? (BK_MAX + 1) * 4 : 0);
+  L.bk_info = take(4 * 4);
+  L.bk_comp = take(bk ? L.sort_cap * 8 : 0);
   L.total = off;
   return L;
 }
@@ -304,6 +310,16 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
                                                    reinterpret_cast<long long*>(out_indices), (long long)offset);
   counted();
   if (L.sort_cap > (u64)SMALL_SORT) {
+    BucketBufs bb{reinterpret_cast<u32*>(ws + L.bk_total), reinterpret_cast<u32*>(ws + L.bk_count), reinterpret_cast<u32*>(ws + L.bk_start),
+                  reinterpret_cast<unsigned long long*>(ws + L.bk_comp), reinterpret_cast<u32*>(ws + L.bk_info)};
+    bucket_count<<<BK_CHUNKS, 512, 0, s>>>(ctrl, sb, bb);
+    counted();
+    bucket_scatter<<<BK_CHUNKS, 512, 0, s>>>(ctrl, sb, bb);
+    counted();
+    bucket_sort<MODE><<<grid_for(BK_MAX, nsm * 6), 256, 0, s>>>(
+        ctrl, sb, bb, reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices),
+        (long long)offset);
+    counted();
     run_sort(ctrl, sb, L, s, nsm);
     writeout<MODE><<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
         ctrl, sb, reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices), (long long)offset);

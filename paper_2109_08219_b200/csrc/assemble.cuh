@@ -38,7 +38,7 @@ namespace dtopk {
 enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4 };
 
 constexpr int K4_TILE = 8192;   // keys per K4 tile
-constexpr int K5_WPT = 1;       // words (32 subranges each) per K5 thread
+constexpr int K5_WPT = 4;       // words (32 subranges each) per K5 thread
 constexpr int K5_TILE = 256 * K5_WPT;
 constexpr int SMALL_POOL = 8192;  // pools up to this size are finished by one CTA (8 keys per thread)
 
@@ -138,49 +138,47 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
       }
       // per-word known counts: A -> 1 key > theta, B -> 1 tie, C -> len ties;
       // E / T set the "needs records" flag (counts come from K4 / K4T)
-      u32 kg = 0, ke = 0, kf = 0;
-      if (keep) {
-        const u32 m0 = a.meta[sid];
-        const u32 c0 = classify(d1[u], d2[u], m0, theta, beta);
-        if (c0 == CLS_A) kg = 1;
-        else if (c0 == CLS_B) ke = 1;
-        else if (c0 == CLS_C) ke = (u32)min(sub_len(sid, a.n, a.alpha), (u64)0x7fffffffu);
+      // per-word known counts: A -> 1 key > theta, B -> 1 tie, C -> len ties;
+      // E / T set the "needs records" flag (counts come from K4 / K4T).
+      // 32-bit sums: a word holds at most 32 * 2^alpha ties; above alpha 26
+      // the flag is set instead so K5 counts from the records in 64 bits.
+      const u32 m = keep ? a.meta[sid] : 0u;
+      const u32 cls = keep ? classify(d1[u], d2[u], m, theta, beta) : CLS_A;
+      u32 kg = keep && cls == CLS_A ? 1u : 0u;
+      u32 ke = 0, kf = keep && cls >= CLS_T ? 1u : 0u;
+      if (keep && cls == CLS_B) ke = 1;
+      if (keep && cls == CLS_C) {
+        if (a.alpha <= 26) ke = (u32)sub_len(sid, a.n, a.alpha);
         else kf = 1;
       }
       kg = __reduce_add_sync(FULL, kg);
-      kf = __reduce_or_sync(FULL, kf);
-      {
-        u64 ew = ke;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) ew += __shfl_xor_sync(FULL, ew, o);
-        if (lane == 0) a.wsum[w] = make_uint2(kg, sat_add31(0, ew) | (kf << 31));
+      ke = __reduce_add_sync(FULL, ke);
+      const u32 flag = __ballot_sync(FULL, kf);
+      if (lane == 0) a.wsum[w] = make_uint2(kg, ke | (flag ? 0x80000000u : 0u));
+      // E / T list slots: one atomic per warp and list, only when present
+      u32 x = cls | (dl[u] >= theta ? 8u : 0u);
+      if (flag) {
+        const u32 be = __ballot_sync(FULL, keep && cls == CLS_E), bt = __ballot_sync(FULL, keep && cls == CLS_T);
+        u32 e0 = 0, t0 = 0;
+        if (lane == 0) {
+          if (be) e0 = atomicAdd(&ctrl->nE, (u32)__popc(be));
+          if (bt) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
+        }
+        e0 = __shfl_sync(FULL, e0, 0);
+        t0 = __shfl_sync(FULL, t0, 0);
+        if (keep && cls == CLS_E) {
+          const u32 e = e0 + __popc(be & lt);
+          if (e < a.cap_e) a.e_sid[e] = (u32)sid;
+          x |= e << 4;
+        } else if (keep && cls == CLS_T) {
+          const u32 t = t0 + __popc(bt & lt);
+          a.t_sid[t] = (u32)sid;
+          a.t_cnt[t] = 0;
+          x |= t << 4;
+        }
       }
       if (!keep) continue;
-      const u32 m = a.meta[sid];
-      const u32 cls = classify(d1[u], d2[u], m, theta, beta);
       const bool fq = dl[u] >= theta;
-      u32 x = cls | (fq ? 8u : 0u);
-      // E / T list slots: one atomic per warp and list (kept lanes only here)
-      const u32 km = __activemask();
-      const u32 be = __ballot_sync(km, cls == CLS_E), bt = __ballot_sync(km, cls == CLS_T);
-      const int leader = __ffs(km) - 1;
-      u32 e0 = 0, t0 = 0;
-      if (lane == leader) {
-        if (be) e0 = atomicAdd(&ctrl->nE, (u32)__popc(be));
-        if (bt) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
-      }
-      e0 = __shfl_sync(km, e0, leader);
-      t0 = __shfl_sync(km, t0, leader);
-      if (cls == CLS_E) {
-        const u32 e = e0 + __popc(be & lt);
-        if (e < a.cap_e) a.e_sid[e] = (u32)sid;
-        x |= e << 4;
-      } else if (cls == CLS_T) {
-        const u32 t = t0 + __popc(bt & lt);
-        a.t_sid[t] = (u32)sid;
-        a.t_cnt[t] = 0;
-        x |= t << 4;
-      }
       const u64 slot = w * 32 + __popc(mask & lt);
       a.rec.r[slot] = make_uint4((u32)sid, d1[u], m, x);
       st_cand++;
@@ -703,8 +701,12 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
           epos++;
         } else if (cls == CLS_C) {
           const u64 len = sub_len(sid, a.n, a.alpha);
-          const u64 take = epos < a.k ? min(len, a.k - epos) : 0;
-          for (u64 z = 0; z < take; z++) a.ties[epos + z] = base + z;
+          if (epos < a.k) {  // a run of ties: K6 writes it (one warp per run)
+            const u32 wslot = atomicAdd(&ctrl->k6_count, 1u);
+            a.d_sid[wslot] = (u32)sid;
+            a.d_pos[wslot] = epos;
+            a.d_need[wslot] = (u32)min(len, a.k - epos) | 0x80000000u;
+          }
           if (fq) st_concat += len;
           epos += len;
         } else if (cls == CLS_T) {
@@ -794,7 +796,11 @@ __global__ void __launch_bounds__(256) k6_ties(Ctrl* ctrl, const u32* __restrict
     const u64 base = (u64)d_sid[w] << alpha;
     const u64 len = sub_len(base >> alpha, n, alpha);
     const u64 pos0 = d_pos[w];
-    const u32 need = d_need[w];
+    const u32 need = d_need[w] & 0x7fffffffu;
+    if (d_need[w] >> 31) {  // constant subrange: its first `need` positions
+      for (u32 z = lane; z < need; z += 32) ties[pos0 + z] = base + z;
+      continue;
+    }
     u32 found = 0;
     for (u64 off = 0; off < len && found < need; off += 32) {
       const u64 e = off + lane;
@@ -807,22 +813,22 @@ __global__ void __launch_bounds__(256) k6_ties(Ctrl* ctrl, const u32* __restrict
   }
 }
 
-// Bitonic sort (ascending) of R*1024 u64 values held as v[j] = element
-// j*1024 + threadIdx.x: strides < 32 exchange through shuffles, strides of
-// 32..512 through shared memory, strides >= 1024 stay inside the thread.
-template <int R>
-__device__ __forceinline__ void bitonic_1024(unsigned long long (&v)[R], unsigned long long* sm) {
+// Bitonic sort (ascending) of R*T u64 values held by a T-thread block as
+// v[j] = element j*T + threadIdx.x: strides < 32 exchange through shuffles,
+// strides of 32..T/2 through shared memory, strides >= T stay in the thread.
+template <int R, int T>
+__device__ __forceinline__ void bitonic_block(unsigned long long (&v)[R], unsigned long long* sm) {
   const u32 tid = threadIdx.x;
-  constexpr u32 NP = R * 1024;
+  constexpr u32 NP = R * T;
   for (u32 size = 2; size <= NP; size <<= 1) {
-    // strides >= 1024: both elements live in this thread (compile-time slots)
+    // strides >= T: both elements live in this thread (compile-time slots)
 #pragma unroll
     for (int js = R / 2; js >= 1; js >>= 1) {
-      if ((u32)js * 1024u <= (size >> 1)) {
+      if ((u32)js * (u32)T <= (size >> 1)) {
 #pragma unroll
         for (int j = 0; j < R; j++) {
           if ((j & js) == 0) {
-            const u32 i = (u32)j * 1024u + tid;
+            const u32 i = (u32)j * (u32)T + tid;
             const bool up = (i & size) == 0;
             const unsigned long long x = v[j], y = v[j | js];
             const bool sw = (x > y) == up;
@@ -832,14 +838,14 @@ __device__ __forceinline__ void bitonic_1024(unsigned long long (&v)[R], unsigne
         }
       }
     }
-    for (u32 stride = min(size >> 1, 512u); stride > 0; stride >>= 1) {
+    for (u32 stride = min(size >> 1, (u32)T / 2); stride > 0; stride >>= 1) {
       if (stride >= 32) {
 #pragma unroll
-        for (int j = 0; j < R; j++) sm[j * 1024 + tid] = v[j];
+        for (int j = 0; j < R; j++) sm[j * T + tid] = v[j];
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < R; j++) {
-          const u32 i = (u32)j * 1024u + tid;
+          const u32 i = (u32)j * (u32)T + tid;
           const unsigned long long p = sm[i ^ stride];
           const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
           v[j] = keep_min ? min(v[j], p) : max(v[j], p);
@@ -848,7 +854,7 @@ __device__ __forceinline__ void bitonic_1024(unsigned long long (&v)[R], unsigne
       } else {
 #pragma unroll
         for (int j = 0; j < R; j++) {
-          const u32 i = (u32)j * 1024u + tid;
+          const u32 i = (u32)j * (u32)T + tid;
           const unsigned long long p = __shfl_xor_sync(FULL, v[j], (int)stride);
           const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
           v[j] = keep_min ? min(v[j], p) : max(v[j], p);
@@ -856,6 +862,11 @@ __device__ __forceinline__ void bitonic_1024(unsigned long long (&v)[R], unsigne
       }
     }
   }
+}
+
+template <int R>
+__device__ __forceinline__ void bitonic_1024(unsigned long long (&v)[R], unsigned long long* sm) {
+  bitonic_block<R, 1024>(v, sm);
 }
 
 template <int MODE, int R>

@@ -105,6 +105,8 @@ struct Ctrl {
   ull sort_m;      // elements to sort
   u32 big_mode;    // 0 done by finish_small, 1 merge (append ties), 2 sort the pool, 3 radix select
   u32 sort_done;   // last-block counter of sort_scan
+  u32 lsd_fallback;
+  u32 bk_ticket;     // last-block counter of bucket_scan  // large answer too skewed for the bucket sort: LSD radix sort instead
 };
 
 enum BigMode : u32 { BIG_NONE = 0, BIG_MERGE = 1, BIG_SORT_POOL = 2, BIG_SELECT = 3 };

@@ -257,7 +257,7 @@ __device__ __forceinline__ int sort_bits(const Ctrl* c) {
 }
 
 __device__ __forceinline__ bool big_sort_skip(const Ctrl* c, int pass) {
-  return c->sort_m <= (ull)SMALL_SORT || pass * 8 >= sort_bits(c) || c->small_done;
+  return c->sort_m <= (ull)SMALL_SORT || pass * 8 >= sort_bits(c) || c->small_done || !c->lsd_fallback;
 }
 
 struct SortBufs {
@@ -393,11 +393,246 @@ __global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, SortBufs b, int 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bucket sort of large answers.  Elements go to up to BK_MAX buckets by the
+// high bits of d = maxkey - key and carry their input position; (d << 32 |
+// position) orders a bucket as (key desc, index asc) whatever order the
+// scatter wrote it in.  BK_CHUNKS CTAs own contiguous chunks of the input:
+//   bucket_count   per-chunk bucket counts; an atomicAdd on the bucket total
+//                  hands each chunk its base inside the bucket
+//   bucket_scatter scan of the totals (bucket starts), then composites to
+//                  their bucket through shared-memory cursors
+//   bucket_sort    CTA per bucket: counting sort on the next BK_SUB_BITS bits
+//                  of d in shared memory, then rank inside each sub-bin by
+//                  comparison (sub-bins hold ~1 element unless keys repeat),
+//                  and write the answer slice directly.
+// A bucket above BK_CAP (skewed keys) sends the sort to the LSD radix sort.
+// ---------------------------------------------------------------------------
+constexpr int BK_MAX = 4096;      // buckets
+constexpr int BK_CHUNKS = 64;     // count / scatter CTAs
+constexpr int BK_TARGET = 1024;   // elements per bucket aimed for
+constexpr int BK_CAP = 4096;      // largest bucket bucket_sort takes (16 per thread)
+constexpr int BK_SUB_BITS = 11;   // sub-bins of the in-bucket counting sort
+constexpr int BK_SUB = 1 << BK_SUB_BITS;
+
+struct BucketBufs {
+  u32* total;   // [BK_MAX] bucket sizes (zeroed per run)
+  u32* counts;  // [BK_CHUNKS][BK_MAX] each chunk's base inside its bucket
+  u32* start;   // [BK_MAX + 1] bucket starts
+  unsigned long long* comp;  // [sort cap] scattered composites
+  u32* info;    // [0] shift, [1] buckets, [2] fallback flag
+};
+
+__device__ __forceinline__ bool bucket_skip(const Ctrl* c) {
+  return c->sort_m <= (ull)SMALL_SORT || c->small_done;
+}
+
+__device__ __forceinline__ void bucket_geometry(const Ctrl* c, u32& shift, u32& nb) {
+  const u64 m = c->sort_m;
+  const u32 hi = max(c->maxkey, c->sort_lo);
+  const u32 range = hi - c->sort_lo;
+  u32 want = 1;
+  while (want < BK_MAX && (u64)want * BK_TARGET < m) want <<= 1;
+  const int bits = range ? 32 - __clz(range) : 0;  // d < 2^bits
+  const int lb = 31 - __clz(want);
+  shift = bits > lb ? (u32)(bits - lb) : 0u;
+  nb = (u32)min((ull)want, range ? ((ull)range >> shift) + 1ull : 1ull);
+}
+
+__device__ __forceinline__ void bucket_chunk(u64 m, u64& lo, u64& hi) {
+  const u64 per = (m + BK_CHUNKS - 1) / BK_CHUNKS;
+  lo = min(m, (u64)blockIdx.x * per);
+  hi = min(m, lo + per);
+}
+
+__global__ void __launch_bounds__(512) bucket_count(Ctrl* ctrl, SortBufs b, BucketBufs bb) {
+  if (bucket_skip(ctrl)) return;
+  __shared__ u32 h[BK_MAX];
+  u32 shift, nb;
+  bucket_geometry(ctrl, shift, nb);
+  for (int i = threadIdx.x; i < (int)nb; i += 512) h[i] = 0;
+  __syncthreads();
+  const u32* keys = ctrl->sort_src ? b.kb : b.ka;
+  const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
+  u64 lo, end;
+  bucket_chunk(ctrl->sort_m, lo, end);
+  u64 i = lo + threadIdx.x;
+  for (; i + 3 * 512 < end; i += 4 * 512) {
+    u32 d[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) d[q] = hi - keys[i + q * 512];
+#pragma unroll
+    for (int q = 0; q < 4; q++) atomicAdd(&h[d[q] >> shift], 1u);
+  }
+  for (; i < end; i += 512) atomicAdd(&h[(hi - keys[i]) >> shift], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < (int)nb; i += 512)
+    bb.counts[(u64)blockIdx.x * BK_MAX + i] = h[i] ? atomicAdd(&bb.total[i], h[i]) : 0u;
+}
+
+// Bucket starts = exclusive scan of the bucket totals (every scatter CTA
+// does it in shared memory; CTA 0 publishes it).  Decides the fallback.
+__device__ __forceinline__ bool bucket_starts(Ctrl* ctrl, const BucketBufs& bb, u32 nb, u32 shift, u32* st) {
+  __shared__ u32 wsum[16];
+  __shared__ u32 s_max;
+  constexpr int PER = BK_MAX / 512;
+  if (threadIdx.x == 0) s_max = 0;
+  u32 loc[PER], sum = 0, mx = 0;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const u32 i = threadIdx.x * PER + q;
+    loc[q] = i < nb ? bb.total[i] : 0u;
+    sum += loc[q];
+    mx = max(mx, loc[q]);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const u32 incl = warp_incl_scan<u32>(sum);
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  atomicMax(&s_max, mx);
+  if (w == 0) {
+    const u32 x = lane < 16 ? wsum[lane] : 0u;
+    const u32 y = warp_incl_scan<u32>(x);
+    if (lane < 16) wsum[lane] = y - x;
+  }
+  __syncthreads();
+  u32 run = wsum[w] + incl - sum;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const u32 i = threadIdx.x * PER + q;
+    if (i < nb) {
+      st[i] = run;
+      if (blockIdx.x == 0) bb.start[i] = run;
+      if (i + 1 == nb) {
+        st[nb] = run + loc[q];
+        if (blockIdx.x == 0) bb.start[nb] = run + loc[q];
+      }
+    }
+    run += loc[q];
+  }
+  __syncthreads();
+  const bool fb = s_max > (u32)BK_CAP || ctrl->sort_m >= (1ull << 32);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    bb.info[0] = shift;
+    bb.info[1] = nb;
+    bb.info[2] = fb ? 1u : 0u;
+    ctrl->lsd_fallback = fb ? 1u : 0u;
+  }
+  return fb;
+}
+
+__global__ void __launch_bounds__(512) bucket_scatter(Ctrl* ctrl, SortBufs b, BucketBufs bb) {
+  if (bucket_skip(ctrl)) return;
+  __shared__ u32 cur[BK_MAX + 1];
+  u32 shift, nb;
+  bucket_geometry(ctrl, shift, nb);
+  if (bucket_starts(ctrl, bb, nb, shift, cur)) return;
+  for (int i = threadIdx.x; i < (int)nb; i += 512) cur[i] += bb.counts[(u64)blockIdx.x * BK_MAX + i];
+  __syncthreads();
+  const u32* keys = ctrl->sort_src ? b.kb : b.ka;
+  const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
+  u64 lo, end;
+  bucket_chunk(ctrl->sort_m, lo, end);
+  u64 i = lo + threadIdx.x;
+  for (; i + 3 * 512 < end; i += 4 * 512) {
+    u32 d[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) d[q] = hi - keys[i + q * 512];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const u32 pos = atomicAdd(&cur[d[q] >> shift], 1u);
+      bb.comp[pos] = ((unsigned long long)d[q] << 32) | (u32)(i + q * 512);
+    }
+  }
+  for (; i < end; i += 512) {
+    const u32 d = hi - keys[i];
+    const u32 pos = atomicAdd(&cur[d >> shift], 1u);
+    bb.comp[pos] = ((unsigned long long)d << 32) | (u32)i;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) bucket_sort(Ctrl* ctrl, SortBufs b, BucketBufs bb, u32* __restrict__ ov,
+                                                      long long* __restrict__ oi, long long offset) {
+  if (bucket_skip(ctrl) || bb.info[2]) return;
+  constexpr int PER = BK_CAP / 256;
+  __shared__ unsigned long long tmp[BK_CAP];
+  __shared__ u32 hs[BK_SUB + 1];
+  __shared__ u32 scr[8];
+  const u32 shift = bb.info[0], nb = bb.info[1];
+  const u32 s2 = shift > (u32)BK_SUB_BITS ? shift - BK_SUB_BITS : 0u;
+  const u64 ko = ctrl->res.k_out;
+  const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
+  const u64* idx = ctrl->sort_src ? b.ib : b.ia;
+  const u32* dhi = reinterpret_cast<const u32*>(bb.comp) + 1;  // d of composite j at dhi[2 j]
+  for (u32 bk = blockIdx.x; bk < nb; bk += gridDim.x) {
+    const u32 lo = bb.start[bk], cnt = bb.start[bk + 1] - lo;
+    if ((u64)lo >= ko || cnt == 0) continue;  // uniform across the CTA
+    for (int i = threadIdx.x; i < BK_SUB; i += 256) hs[i] = 0;
+    __syncthreads();
+    u32 ss[PER];  // sub << 16 | slot in the sub-bin, then sub << 16 | place in tmp
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+      const u32 i = r * 256 + threadIdx.x;
+      if (i < cnt) {
+        const u32 sub = (dhi[2 * (u64)(lo + i)] >> s2) & (BK_SUB - 1);
+        ss[r] = sub << 16 | atomicAdd(&hs[sub], 1u);
+      }
+    }
+    __syncthreads();
+    u32 loc[BK_SUB / 256], sum = 0;
+#pragma unroll
+    for (int q = 0; q < BK_SUB / 256; q++) {
+      loc[q] = hs[threadIdx.x * (BK_SUB / 256) + q];
+      sum += loc[q];
+    }
+    u32 run = block_incl_scan_256<u32>(sum, scr) - sum;
+#pragma unroll
+    for (int q = 0; q < BK_SUB / 256; q++) {
+      hs[threadIdx.x * (BK_SUB / 256) + q] = run;
+      run += loc[q];
+    }
+    if (threadIdx.x == 255) hs[BK_SUB] = run;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+      const u32 i = r * 256 + threadIdx.x;
+      if (i < cnt) {
+        const u32 sub = ss[r] >> 16;
+        const u32 place = hs[sub] + (ss[r] & 0xffffu);
+        tmp[place] = bb.comp[lo + i];
+        ss[r] = sub << 16 | place;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+      const u32 i = r * 256 + threadIdx.x;
+      if (i < cnt) {
+        const u32 sub = ss[r] >> 16;
+        const unsigned long long e = tmp[ss[r] & 0xffffu];
+        const u32 b0 = hs[sub], b1 = hs[sub + 1];
+        u32 rank = b0;
+        if (b1 - b0 > 1)
+          for (u32 q = b0; q < b1; q++) rank += tmp[q] < e ? 1u : 0u;
+        const u64 pos = (u64)lo + rank;
+        if (pos < ko) {
+          const u32 key = hi - (u32)(e >> 32);
+          ov[pos] = from_key<MODE>(key);
+          oi[pos] = (long long)idx[(u32)e] + offset;
+          if (pos == ko - 1) ctrl->res.kth_key = key;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Write the first k_out sorted pairs in the input dtype (big sorts only).
 template <int MODE>
 __global__ void __launch_bounds__(256) writeout(Ctrl* ctrl, SortBufs b, u32* __restrict__ ov,
                                                 long long* __restrict__ oi, long long offset) {
-  if (ctrl->sort_m <= (ull)SMALL_SORT || ctrl->small_done) return;
+  if (ctrl->sort_m <= (ull)SMALL_SORT || ctrl->small_done || !ctrl->lsd_fallback) return;
   const int passes = (sort_bits(ctrl) + 7) / 8;
   const bool in_b = ((ctrl->sort_src + (u32)passes) & 1u) != 0;
   const u32* ks = in_b ? b.kb : b.ka;

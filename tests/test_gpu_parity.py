@@ -106,6 +106,27 @@ def test_dr_topk_adversarial(dist, k, oracle_mod, cuda):
     check_topk(v, k, oracle_mod)
 
 
+@pytest.mark.parametrize("k", [20_000, 300_000])
+@pytest.mark.parametrize("case", ["uniform", "normal_f32_smallest", "skewed_bucket", "two_values"])
+def test_big_answer_sorts(case, k, oracle_mod, cuda):
+    """Large answers: bucket sort (uniform, float) and its LSD fallback (a
+    bucket above BK_CAP: a block of near-equal keys; two values only)."""
+    largest = True
+    if case == "uniform":
+        v = data.generate("uniform", 1 << 22, seed=k, device=cuda)
+    elif case == "normal_f32_smallest":
+        v = data.generate("normal_f32", 1 << 22, seed=k, device=cuda)
+        largest = False
+    elif case == "skewed_bucket":
+        v = data.generate("uniform", 1 << 22, seed=k, device=cuda)
+        hot = data.generate("uniform", 1 << 22, seed=k + 1, device=cuda).view(torch.int32) & 0xFFF
+        v.view(torch.int32)[::5] = (0x7FFFF000 + hot[::5]).to(torch.int32) | torch.iinfo(torch.int32).min
+    else:
+        v = data.generate("uniform", 1 << 22, seed=k, device=cuda).view(torch.int32) & 1
+        v = (v + 7).view(torch.uint32)
+    check_topk(v, k, oracle_mod, largest=largest)
+
+
 @pytest.mark.parametrize("largest", [True, False])
 @pytest.mark.parametrize("dist", ["normal_f32", "pareto_f32"])
 @pytest.mark.parametrize("beta", [1, 2, 3])
