@@ -170,7 +170,7 @@ void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch) {
     cudaFuncSetAttribute(k1_delegates<MODE, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1_SMEM);
     attr = true;
   }
-  k1_delegates<MODE, B><<<grid_for(nch, nsm), K1_THREADS, K1_SMEM, s>>>(a);
+  k1_delegates<MODE, B><<<grid_for(nch, nsm * K1_CPS), K1_THREADS, K1_SMEM, s>>>(a);
   counted();
   if (a.alpha > K1_LOG_CHUNK) {
     k1_merge<B><<<grid_for((a.S + 255) / 256, nsm * 4), 256, 0, s>>>(a.partial, a.pmeta, nch, a.alpha, a.S, a.D,

@@ -22,9 +22,19 @@ namespace dtopk {
 
 constexpr int K1_CHUNK = 2048;    // keys per stage = one warp's unit of work (8 KiB)
 constexpr int K1_LOG_CHUNK = 11;
-constexpr int K1_CWARPS = 8;      // consumer warps
+#ifndef DTOPK_K1_CWARPS
+#define DTOPK_K1_CWARPS 8
+#endif
+#ifndef DTOPK_K1_CPS
+#define DTOPK_K1_CPS 1
+#endif
+constexpr int K1_CWARPS = DTOPK_K1_CWARPS;  // consumer warps
+constexpr int K1_CPS = DTOPK_K1_CPS;        // resident CTAs per SM
 #ifndef DTOPK_K1_STAGES
 #define DTOPK_K1_STAGES 16
+#endif
+#ifndef DTOPK_K1_EXP
+#define DTOPK_K1_EXP 0  // profiling experiments only (tools/k1_exp.cu): 1 = no consumer work, 2 = no emit
 #endif
 #ifndef DTOPK_K1_PREFETCH
 #define DTOPK_K1_PREFETCH 0
@@ -157,15 +167,22 @@ __device__ __forceinline__ void store_delegates(u32* D, u64 sid, const u32 (&L)[
 // warp must call (warp-aggregated histogram).
 template <int B>
 __device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 sid, bool leader,
-                                              const u32 (&L)[B], u32 meta) {
+                                              const u32 (&L)[B], u32 meta, bool one_writer = false) {
   const bool w = leader && sid < a.S;
   if (w) {
     store_delegates<B>(a.D, sid, L);
     a.meta[sid] = meta;
   }
-  if (a.do_hist) {
+  if (a.do_hist && DTOPK_K1_EXP != 3) {
+    if (one_writer) {  // a single emitting lane: no aggregation needed
+      if (w) {
 #pragma unroll
-    for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, w);
+        for (int i = 0; i < B; i++) atomicAdd(&shist[L[i] >> 21], 1u);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, w);
+    }
   }
 }
 
@@ -214,8 +231,12 @@ __device__ __forceinline__ u32 finalize_meta(const K1Args& a, const uint4* st4, 
 
 // One warp reduces one staged chunk of 2048 keys.  No CTA-wide barrier: the
 // eight consumer warps run decoupled, each on its own stages.
+// `rel`: the stage's empty barrier.  The lane-contiguous path (alpha >= 6,
+// full chunks) releases the stage as soon as its last shared-memory read is
+// done -- before the subrange butterflies and the delegate stores -- and then
+// returns true; otherwise the caller releases it.
 template <int MODE, int B, bool TAIL>
-__device__ __forceinline__ void k1_warp_chunk(const K1Args& a, const u32* stage, u64 c, u32* shist) {
+__device__ __forceinline__ bool k1_warp_chunk(const K1Args& a, const u32* stage, u64 c, u32* shist, u64* rel) {
   const int lane = threadIdx.x & 31;
   const u64 start = c << K1_LOG_CHUNK;
   const u32 cnt = TAIL ? (u32)min((u64)K1_CHUNK, a.n - start) : (u32)K1_CHUNK;
@@ -251,7 +272,7 @@ __device__ __forceinline__ void k1_warp_chunk(const K1Args& a, const u32* stage,
         emit_subrange<B>(a, shist, (start + q * 4u) >> alpha, (lane & (G - 1)) == 0, A.L, meta);
       }
     }
-    return;
+    return false;
   }
 
   // ---- lane-contiguous: lane owns keys [lane*64, lane*64+64).  LDS.128 order
@@ -276,7 +297,7 @@ __device__ __forceinline__ void k1_warp_chunk(const K1Args& a, const u32* stage,
       const u32 meta = finalize_meta<MODE, B, TAIL>(a, st4, start, cnt, tcnt, A0);
       emit_subrange<B>(a, shist, (start + (q0 + h * 8) * 4u) >> 5, true, A0.L, meta);
     }
-    return;
+    return false;
   }
   Acc<B> A0, A1;
   A0.init(q0);
@@ -289,38 +310,55 @@ __device__ __forceinline__ void k1_warp_chunk(const K1Args& a, const u32* stage,
     acc_keys<B>((jj & 1) ? A1 : A0, x, y, q);
   }
   acc_merge<B>(A0, A1.L, A1.p, A1.mn);
-  const int G = alpha >= K1_LOG_CHUNK ? 32 : 1 << (alpha - 6);  // lanes per subrange (alpha == 6: 1)
-  for (int off = 1; off < G; off <<= 1) acc_shfl<B>(A0, off);
-  if (alpha <= K1_LOG_CHUNK) {
-    const u32 meta = finalize_meta<MODE, B, TAIL>(a, st4, start, cnt, tcnt, A0);
-    emit_subrange<B>(a, shist, (start + q0 * 4u) >> alpha, (lane & (G - 1)) == 0, A0.L, meta);
-  } else {
-    // W > 2048: this chunk is one part of a subrange -> partial ladder + the
-    // exact offset of its max inside the subrange + its minimum
+  if constexpr (DTOPK_K1_EXP == 2) {
+    if (A0.L[0] == 0x12345678u && A0.p == 7u) a.D[c] = A0.mn;
+    return false;
+  }
+  // exact chunk offset of this lane's maximum (first occurrence inside its
+  // uint4), read while the stage is still owned; then hand the stage back
+  {
     u32 x[4], y[4];
     load_keys<MODE, TAIL>(a, start, A0.p * 4u, cnt, tcnt, st4[A0.p], x, y);
     u32 cc = 3;
 #pragma unroll
     for (int i = 3; i >= 0; i--)
       if (x[i] == A0.L[0]) cc = (u32)i;
+    A0.p = A0.p * 4u + cc;
+  }
+  bool released = false;
+  if (!TAIL && rel != nullptr) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(rel);
+    released = true;
+  }
+  const int G = alpha >= K1_LOG_CHUNK ? 32 : 1 << (alpha - 6);  // lanes per subrange (alpha == 6: 1)
+  for (int off = 1; off < G; off <<= 1) acc_shfl<B>(A0, off);
+  const u64 wmask = (1ull << alpha) - 1;
+  if (alpha <= K1_LOG_CHUNK) {
+    const u32 meta = pack_meta(A0.mn == A0.L[0], (u32)((start + A0.p) & wmask));
+    emit_subrange<B>(a, shist, (start + q0 * 4u) >> alpha, (lane & (G - 1)) == 0, A0.L, meta, G == 32);
+  } else {
+    // W > 2048: this chunk is one part of a subrange -> partial ladder + the
+    // exact offset of its max inside the subrange + its minimum
     if (lane == 0) {
 #pragma unroll
       for (int i = 0; i < B; i++) a.partial[c * B + i] = A0.L[i];
-      a.pmeta[2 * c] = (u32)((start + A0.p * 4u + cc) & ((1ull << alpha) - 1));
+      a.pmeta[2 * c] = (u32)((start + A0.p) & wmask);
       a.pmeta[2 * c + 1] = A0.mn;
     }
   }
+  return released;
 }
 
 // The (single) ragged last chunk goes through an out-of-line copy so the bounds
 // checks do not inflate the register budget of the steady-state loop.
 template <int MODE, int B>
 __device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stage, u64 c, u32* shist) {
-  k1_warp_chunk<MODE, B, true>(a, stage, c, shist);
+  k1_warp_chunk<MODE, B, true>(a, stage, c, shist, nullptr);
 }
 
 template <int MODE, int B>
-__global__ void __launch_bounds__(K1_THREADS, 1) k1_delegates(K1Args a) {
+__global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   u32* stages = reinterpret_cast<u32*>(smem_raw);
   u64* full = reinterpret_cast<u64*>(smem_raw + (size_t)K1_STAGES * K1_CHUNK * 4);
@@ -370,12 +408,20 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_delegates(K1Args a) {
       const u32 ph = (u32)(i / K1_STAGES) & 1u;
       mbar_wait(&full[s], ph);
       const u32* st = stages + (size_t)s * K1_CHUNK;
+      if constexpr (DTOPK_K1_EXP == 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      }
+      bool released = false;
       if (((c + 1) << K1_LOG_CHUNK) <= a.n)
-        k1_warp_chunk<MODE, B, false>(a, st, c, shist);
+        released = k1_warp_chunk<MODE, B, false>(a, st, c, shist, &empty[s]);
       else
         k1_warp_chunk_tail<MODE, B>(a, st, c, shist);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (!released) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
     }
   }
   __syncthreads();
