@@ -31,6 +31,8 @@
 //   K6  locates the ties of class-D records that fall among the first k ties.
 #pragma once
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "common.cuh"
 
 namespace dtopk {
@@ -899,6 +901,42 @@ __device__ __forceinline__ void finish_small_r(Ctrl* ctrl, u64 m, u64 ko, u64 G,
   }
 }
 
+// Pools of 2049..SMALL_POOL pairs: one CTA, stable LSD radix sort (CUB block
+// primitive, 1024 threads x 8 items in shared memory) of d = hi - key over
+// only the bits d can occupy, with the pool position as the value.  The input
+// is in position order, so stability yields (key desc, position asc).
+// Padding slots (>= m) carry the largest d and come last by stability.
+template <int MODE>
+__device__ __forceinline__ void finish_small_radix(Ctrl* ctrl, u64 m, u64 ko, u64 G, u32 theta, u32 hi,
+                                                   const u32* __restrict__ gt_keys, const u64* __restrict__ gt_idx,
+                                                   const u64* __restrict__ ties, u32* __restrict__ ov,
+                                                   long long* __restrict__ oi, long long offset, void* smem) {
+  typedef cub::BlockRadixSort<u32, 1024, 8, u32> Sorter;
+  static_assert(sizeof(typename Sorter::TempStorage) <= SMALL_POOL * 8, "finish_small shared memory");
+  const u32 range = hi - theta;
+  const int nbits = range ? 32 - __clz(range) : 0;
+  const u32 pad = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
+  u32 d[8], pos[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const u32 i = threadIdx.x * 8u + (u32)j;
+    pos[j] = i;
+    d[j] = pad;
+    if (i < m) d[j] = hi - (i < G ? gt_keys[i] : theta);
+  }
+  if (nbits) Sorter(*reinterpret_cast<typename Sorter::TempStorage*>(smem)).Sort(d, pos, 0, nbits);
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const u32 r = threadIdx.x * 8u + (u32)j;
+    if (r < ko) {
+      const u32 key = hi - d[j];
+      ov[r] = from_key<MODE>(key);
+      oi[r] = (long long)(pos[j] < G ? gt_idx[pos[j]] : ties[pos[j] - G]) + offset;
+      if (r == ko - 1) ctrl->res.kth_key = key;
+    }
+  }
+}
+
 // Fused finish for pools of at most SMALL_POOL pairs: one CTA sorts the pool
 // (P_gt, plus the ties on the merge path) by (key desc, position asc) and
 // writes the first k_out pairs in the input dtype.  Positions follow index
@@ -924,10 +962,8 @@ __global__ void __launch_bounds__(1024) finish_small(Ctrl* ctrl, const u32* __re
     finish_small_r<MODE, 1>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   else if (m <= 2048)
     finish_small_r<MODE, 2>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
-  else if (m <= 4096)
-    finish_small_r<MODE, 4>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   else
-    finish_small_r<MODE, 8>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+    finish_small_radix<MODE>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   if (threadIdx.x == 0) ctrl->small_done = 1;
 }
 

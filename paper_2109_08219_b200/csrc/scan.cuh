@@ -16,6 +16,8 @@
 // raw input on the direct path (pipeline.py:184-191).
 #pragma once
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "common.cuh"
 
 namespace dtopk {
@@ -658,33 +660,50 @@ __global__ void __launch_bounds__(1024) sort_small(Ctrl* ctrl, SortBufs b, u32* 
   const u64 ko = ctrl->res.k_out;
   const u32* kA = ctrl->sort_src ? b.kb : b.ka;
   const u64* iA = ctrl->sort_src ? b.ib : b.ia;
-  const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
-  u32 np = 1;
-  while (np < m) np <<= 1;
-  for (u32 i = threadIdx.x; i < np; i += 1024)
-    sk[i] = i < m ? ((unsigned long long)(hi - kA[i]) << 32) | i : ~0ull;
-  __syncthreads();
-  for (u32 size = 2; size <= np; size <<= 1) {
-    for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
-      for (u32 t = threadIdx.x; t < np / 2; t += 1024) {
-        const u32 lo = 2 * t - (t & (stride - 1));
-        const u32 hi2 = lo + stride;
-        const bool up = (lo & size) == 0;
-        const unsigned long long x = sk[lo], y = sk[hi2];
-        if ((x > y) == up) {
-          sk[lo] = y;
-          sk[hi2] = x;
-        }
-      }
-      __syncthreads();
-    }
+  // stable LSD radix sort of d = hi - key over the bits d can occupy (CUB
+  // block primitive, 1024 threads x 8 items); input order is index order
+  // within equal keys, so the result is (key desc, index asc)
+  typedef cub::BlockRadixSort<u32, 1024, 8, u32> Sorter;
+  static_assert(sizeof(typename Sorter::TempStorage) <= SMALL_SORT * 8, "sort_small shared memory");
+  __shared__ u32 s_lo[32], s_hi[32];
+  u32 key_in[8], lo = 0xffffffffu, hi = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const u32 i = threadIdx.x * 8u + (u32)j;
+    key_in[j] = i < m ? kA[i] : kA[0];
+    lo = min(lo, key_in[j]);
+    hi = max(hi, key_in[j]);
   }
-  for (u32 i = threadIdx.x; i < ko; i += 1024) {
-    const u32 pos = (u32)(sk[i] & 0xffffffffu);
-    const u32 key = hi - (u32)(sk[i] >> 32);
-    ov[i] = from_key<MODE>(key);
-    oi[i] = (long long)iA[pos] + offset;
-    if (i == ko - 1) ctrl->res.kth_key = key;
+  lo = __reduce_min_sync(FULL, lo);
+  hi = __reduce_max_sync(FULL, hi);
+  if ((threadIdx.x & 31) == 0) {
+    s_lo[threadIdx.x >> 5] = lo;
+    s_hi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  lo = __reduce_min_sync(FULL, s_lo[threadIdx.x & 31]);
+  hi = __reduce_max_sync(FULL, s_hi[threadIdx.x & 31]);
+  const u32 dmax = hi - lo;  // every key lies in [lo, hi]
+  const int nbits = dmax ? 32 - __clz(dmax) : 0;
+  const u32 pad = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
+  u32 d[8], pos[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const u32 i = threadIdx.x * 8u + (u32)j;
+    pos[j] = i;
+    d[j] = i < m ? hi - key_in[j] : pad;
+  }
+  __syncthreads();  // s_lo reads done before the sort reuses shared memory
+  if (nbits) Sorter(*reinterpret_cast<typename Sorter::TempStorage*>(sk)).Sort(d, pos, 0, nbits);
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const u32 r = threadIdx.x * 8u + (u32)j;
+    if (r < ko) {
+      const u32 key = hi - d[j];
+      ov[r] = from_key<MODE>(key);
+      oi[r] = (long long)iA[pos[j]] + offset;
+      if (r == ko - 1) ctrl->res.kth_key = key;
+    }
   }
 }
 
