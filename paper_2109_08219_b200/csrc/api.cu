@@ -251,37 +251,96 @@ void run_sort(Ctrl* ctrl, const SortBufs& b, const Layout& L, cudaStream_t s, in
   }
 }
 
+// Graph capture context: when `graph` is set, run_finish ends the main
+// capture after finish_small, adds a conditional IF node set by finish_small
+// and captures the large-pool tail into its body; inside the tail, nested IF
+// nodes (captured on s2 / s3) gate the select kernels, the bucket sort and the
+// LSD fallback sort, so only the stages a run needs are launched.
+struct GraphCtx {
+  cudaGraph_t graph = nullptr;
+  cudaGraphConditionalHandle cond{};
+  cudaStream_t s2 = nullptr, s3 = nullptr;
+  unsigned long long main_kernels = 0, body_kernels = 0;
+  bool ok = true;
+};
+
+inline bool cap_ok(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  fprintf(stderr, "dtopk: graph capture step %s failed: %s\n", what, cudaGetErrorString(e));
+  return false;
+}
+
+// Conditional handle for a node anywhere in the plan's graph (handles belong
+// to the root graph; the node may sit in a nested conditional body).
+bool cond_handle(cudaGraph_t root, cudaGraphConditionalHandle* h) {
+  return cap_ok(cudaGraphConditionalHandleCreate(h, root, 0, cudaGraphCondAssignDefault), "handle create");
+}
+
+// Append an IF node on handle h at the capture point of s; capture its body on `inner`.
+bool cond_begin(cudaStream_t s, cudaGraphConditionalHandle h, cudaStream_t inner) {
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t g = nullptr;
+  if (!cap_ok(cudaStreamGetCaptureInfo(s, &cst, nullptr, &g, &deps, &ndeps), "capture info")) return false;
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  return cap_ok(cudaGraphAddNode(&node, g, deps, ndeps, &cp), "add conditional node") &&
+         cap_ok(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies), "update deps") &&
+         cap_ok(cudaStreamBeginCaptureToGraph(inner, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeRelaxed), "begin body capture");
+}
+
+bool cond_end(cudaStream_t inner) {
+  cudaGraph_t g = nullptr;
+  return cap_ok(cudaStreamEndCapture(inner, &g), "end body capture");
+}
+
 template <int MODE>
 void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ull* m_dev, u64 m_host, int direct,
               void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L, cudaStream_t s,
-              int nsm) {
+              int nsm, GraphCtx* gc = nullptr) {
   // SecondK beyond SMALL_POOL (or the direct path): merge / sort the pool /
   // exact radix select + ordered emit, then the stable sort and write-out.
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
   const SortBufs sb = sort_bufs(ws, L, direct != 0);
   u32* selbuf = reinterpret_cast<u32*>(ws + L.selbuf);
+  const bool g = gc != nullptr && !direct;
+  cudaGraphConditionalHandle h_sel{}, h_bucket{}, h_lsd{};
+  // a handle must belong to a conditional node: h_bucket only when the bucket stage exists
+  const bool bucket_stage = L.sort_cap > (u64)SMALL_SORT;
+  if (g) gc->ok = gc->ok && cond_handle(gc->graph, &h_sel) && (!bucket_stage || cond_handle(gc->graph, &h_bucket));
   if (!direct) {
-    tail_decide<<<1, 1, 0, s>>>(ctrl, k);
+    tail_decide<<<1, 1, 0, s>>>(ctrl, k, h_sel, h_bucket, g ? (bucket_stage ? 3 : 1) : 0);
     counted();
     merge_append<<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(ctrl, sb.ka, sb.ia,
                                                                      reinterpret_cast<u64*>(ws + L.ties));
     counted();
   }
+  cudaStream_t cs = s;  // stream of the current (possibly conditional) body
+  if (g) {
+    gc->ok = gc->ok && cond_begin(s, h_sel, gc->s2);
+    cs = gc->s2;
+  }
   const u64 mcap = m_dev ? L.cap_gt : m_host;
   const int gs = grid_for((mcap + 2047) / 2048, nsm * 4);
   SelArgs sp{keys_for_emit, m_host, m_dev, ctrl, &ctrl->selP, selbuf, k, direct ? 0 : 1};
   if (direct) {
-    sel_pass1<MODE><<<gs, 256, 0, s>>>(sp);
+    sel_pass1<MODE><<<gs, 256, 0, cs>>>(sp);
     counted();
-    sel_pass2<MODE><<<gs, 256, 0, s>>>(sp);
+    sel_pass2<MODE><<<gs, 256, 0, cs>>>(sp);
     counted();
   } else {
-    sel_pass1<KM_KEY><<<gs, 256, 0, s>>>(sp);
+    sel_pass1<KM_KEY><<<gs, 256, 0, cs>>>(sp);
     counted();
-    sel_pass2<KM_KEY><<<gs, 256, 0, s>>>(sp);
+    sel_pass2<KM_KEY><<<gs, 256, 0, cs>>>(sp);
     counted();
   }
-  sel_pass3<<<gs, 256, 0, s>>>(sp);
+  sel_pass3<<<gs, 256, 0, cs>>>(sp);
   counted();
   ScanArgs em{};
   em.keys = keys_for_emit;
@@ -297,10 +356,14 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
   em.check_path = direct ? 0 : 1;
   em.direct = direct;
   if (direct)
-    scan_emit<MODE><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
+    scan_emit<MODE><<<grid_for(L.em_tiles, nsm * 4), 256, 0, cs>>>(em);
   else
-    scan_emit<KM_KEY><<<grid_for(L.em_tiles, nsm * 4), 256, 0, s>>>(em);
+    scan_emit<KM_KEY><<<grid_for(L.em_tiles, nsm * 4), 256, 0, cs>>>(em);
   counted();
+  if (g) {
+    gc->ok = gc->ok && cond_end(gc->s2);
+    cs = s;
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(sort_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SORT * 8);
@@ -309,33 +372,35 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
   sort_small<MODE><<<1, 1024, SMALL_SORT * 8, s>>>(ctrl, sb, reinterpret_cast<u32*>(out_values),
                                                    reinterpret_cast<long long*>(out_indices), (long long)offset);
   counted();
-  if (L.sort_cap > (u64)SMALL_SORT) {
+  if (bucket_stage) {
+    if (g) {
+      gc->ok = gc->ok && cond_begin(s, h_bucket, gc->s2) && cond_handle(gc->graph, &h_lsd);
+      cs = gc->s2;
+    }
     BucketBufs bb{reinterpret_cast<u32*>(ws + L.bk_total), reinterpret_cast<u32*>(ws + L.bk_count), reinterpret_cast<u32*>(ws + L.bk_start),
-                  reinterpret_cast<unsigned long long*>(ws + L.bk_comp), reinterpret_cast<u32*>(ws + L.bk_info)};
-    bucket_count<<<BK_CHUNKS, 512, 0, s>>>(ctrl, sb, bb);
+                  reinterpret_cast<unsigned long long*>(ws + L.bk_comp), reinterpret_cast<u32*>(ws + L.bk_info),
+                  h_lsd, g ? 1 : 0};
+    bucket_count<<<BK_CHUNKS, 512, 0, cs>>>(ctrl, sb, bb);
     counted();
-    bucket_scatter<<<BK_CHUNKS, 512, 0, s>>>(ctrl, sb, bb);
+    bucket_scatter<<<BK_CHUNKS, 512, 0, cs>>>(ctrl, sb, bb);
     counted();
-    bucket_sort<MODE><<<grid_for(BK_MAX, nsm * 6), 256, 0, s>>>(
+    bucket_sort<MODE><<<grid_for(BK_MAX, nsm * 6), 256, 0, cs>>>(
         ctrl, sb, bb, reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices),
         (long long)offset);
     counted();
-    run_sort(ctrl, sb, L, s, nsm);
-    writeout<MODE><<<grid_for((k + 255) / 256, nsm * 4), 256, 0, s>>>(
+    cudaStream_t ls = cs;
+    if (g) {
+      gc->ok = gc->ok && cond_begin(cs, h_lsd, gc->s3);
+      ls = gc->s3;
+    }
+    run_sort(ctrl, sb, L, ls, nsm);
+    writeout<MODE><<<grid_for((k + 255) / 256, nsm * 4), 256, 0, ls>>>(
         ctrl, sb, reinterpret_cast<u32*>(out_values), reinterpret_cast<long long*>(out_indices), (long long)offset);
     counted();
+    if (g) gc->ok = gc->ok && cond_end(gc->s3) && cond_end(gc->s2);
   }
 }
 
-// Graph capture context: when `graph` is set, run_finish ends the main
-// capture after finish_small, adds a conditional IF node set by finish_small
-// and captures the large-pool tail into its body.
-struct GraphCtx {
-  cudaGraph_t graph = nullptr;
-  cudaGraphConditionalHandle cond{};
-  unsigned long long main_kernels = 0, body_kernels = 0;
-  bool ok = true;
-};
 
 template <int MODE>
 void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, const int64_t* theta_override,
@@ -439,7 +504,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
            cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
                                          cudaStreamCaptureModeRelaxed) == cudaSuccess;
   big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices, offset,
-                 ws, L, s, nsm);
+                 ws, L, s, nsm, gc);
   cudaGraph_t body = nullptr;
   gc->ok = gc->ok && cudaStreamEndCapture(s, &body) == cudaSuccess;
   gc->body_kernels = dtopk_launch_count_internal() - gc->main_kernels;
@@ -518,6 +583,8 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
   dtopk_plan_s* p = new dtopk_plan_s();
   GraphCtx gc;
   bool ok = cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&gc.s2, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&gc.s3, cudaStreamNonBlocking) == cudaSuccess &&
             cudaGraphCreate(&p->graph, 0) == cudaSuccess &&
             cudaGraphConditionalHandleCreate(&gc.cond, p->graph, 0, cudaGraphCondAssignDefault) == cudaSuccess &&
             cudaStreamBeginCaptureToGraph(p->cap, p->graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
@@ -544,10 +611,12 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
       ok = cudaStreamEndCapture(s, &g) == cudaSuccess;
       gc.main_kernels = t_launches;
     }
-    ok = ok && gc.ok && cudaGraphInstantiate(&p->exec, p->graph, 0) == cudaSuccess;
+    ok = ok && gc.ok && cap_ok(cudaGraphInstantiate(&p->exec, p->graph, 0), "instantiate");
     p->main_kernels = gc.main_kernels;
     p->body_kernels = gc.body_kernels;
   }
+  if (gc.s2) cudaStreamDestroy(gc.s2);
+  if (gc.s3) cudaStreamDestroy(gc.s3);
   if (!ok) {
     cudaGetLastError();
     dtopk_plan_destroy(p);

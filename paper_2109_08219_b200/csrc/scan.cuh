@@ -209,10 +209,18 @@ __global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
   }
 }
 
+constexpr int SMALL_SORT = 8192;  // answers up to this size are sorted by one CTA
+
 // Decide how the pool beyond SMALL_POOL is finished (one thread).
-__global__ void tail_decide(Ctrl* ctrl, u64 k) {
+// In a CUDA-graph plan it also sets the conditionals that gate the select
+// kernels (BIG_SELECT only; use_cond bit 0) and the multi-CTA bucket sort
+// (answers beyond SMALL_SORT; bit 1), so skipped stages are not launched.
+__global__ void tail_decide(Ctrl* ctrl, u64 k, cudaGraphConditionalHandle c_sel, cudaGraphConditionalHandle c_bucket,
+                            int use_cond) {
   if (ctrl->small_done) {
     ctrl->big_mode = BIG_NONE;
+    if (use_cond & 1) cudaGraphSetConditional(c_sel, 0u);
+    if (use_cond & 2) cudaGraphSetConditional(c_bucket, 0u);
     return;
   }
   const u64 G = ctrl->res.pool_gt;
@@ -228,6 +236,9 @@ __global__ void tail_decide(Ctrl* ctrl, u64 k) {
   } else {
     ctrl->big_mode = BIG_SELECT;  // radix select + ordered emit, then sort k
   }
+  const bool sel = ctrl->big_mode == BIG_SELECT;
+  if (use_cond & 1) cudaGraphSetConditional(c_sel, sel ? 1u : 0u);
+  if (use_cond & 2) cudaGraphSetConditional(c_bucket, (sel ? k : (u64)ctrl->sort_m) > (u64)SMALL_SORT ? 1u : 0u);
 }
 
 // BIG_MERGE: append the ties (key theta) after P_gt.
@@ -250,7 +261,6 @@ __global__ void __launch_bounds__(256) merge_append(Ctrl* ctrl, u32* __restrict_
 // (ctrl->sort_src: 0 = A, 1 = B) are decided on the device.
 // ---------------------------------------------------------------------------
 constexpr int ST_TILE = 2048;
-constexpr int SMALL_SORT = 8192;  // answers up to this size are sorted by one CTA
 
 __device__ __forceinline__ int sort_bits(const Ctrl* c) {
   const u32 lo = c->sort_lo;
@@ -423,6 +433,8 @@ struct BucketBufs {
   u32* start;   // [BK_MAX + 1] bucket starts
   unsigned long long* comp;  // [sort cap] scattered composites
   u32* info;    // [0] shift, [1] buckets, [2] fallback flag
+  cudaGraphConditionalHandle c_lsd;  // graph plans: gates the LSD fallback sort
+  int use_cond;
 };
 
 __device__ __forceinline__ bool bucket_skip(const Ctrl* c) {
@@ -519,6 +531,7 @@ __device__ __forceinline__ bool bucket_starts(Ctrl* ctrl, const BucketBufs& bb, 
     bb.info[1] = nb;
     bb.info[2] = fb ? 1u : 0u;
     ctrl->lsd_fallback = fb ? 1u : 0u;
+    if (bb.use_cond) cudaGraphSetConditional(bb.c_lsd, fb ? 1u : 0u);
   }
   return fb;
 }
