@@ -40,7 +40,7 @@ int num_sms();
 
 struct Layout {
   size_t ctrl, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
-  size_t D, meta, partial, pmeta, selbuf, region_cnt, keepw, wsum, rec, e_sid, t_sid, t_cnt,
+  size_t D, meta, partial, pmeta, selbuf, region_cnt, sup_sid, sup_in, sup_cnt, sup_off, rec, e_sid, t_sid, t_cnt,
       stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, e_gpos, e_epos, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
       digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, total;
   u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
@@ -76,7 +76,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.g2 = (u32)g2;
   L.R2 = ((L.D_len + g2 - 1) / g2 + 511) / 512 * 512;
   L.k4_tiles = (L.cap_e * W + K4_TILE - 1) / K4_TILE;
-  L.k5_tiles = (L.words + K5_TILE - 1) / K5_TILE;
+  L.k5_tiles = std::max<u64>(1, (L.S + K5_TILE - 1) / K5_TILE);  // records <= S
   L.em_tiles = (L.m_emit + SC_TILE - 1) / SC_TILE;
   // largest sort: the answer (k), or a pool of up to 4k kept whole (BIG_SORT_POOL)
   L.sort_cap = direct ? k : std::max<u64>(k, std::min<u64>(4 * k, L.cap_gt));
@@ -95,9 +95,11 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.pmeta = take(parts ? 2 * L.nch * 4 : 0);
   L.selbuf = take(std::max<u64>((u64)L.g2 * L.R2, L.m_emit) * 4);
   L.region_cnt = take((u64)L.g2 * 4);
-  L.keepw = take(L.words * 4);
-  L.wsum = take(L.words * 8);
-  L.rec = take(L.words * 32 * 16);
+  L.sup_sid = take(L.S * 4);
+  L.sup_in = take((u64)L.g2 * 8 * 4);
+  L.sup_cnt = take((u64)L.g2 * 8 * 4);
+  L.sup_off = take(((u64)L.g2 * 8 + 1) * 4);
+  L.rec = take(L.S * 16);
   L.e_sid = take(L.cap_e * 4);
   L.t_sid = take(L.S * 4);
   L.t_cnt = take(L.S * 4);
@@ -218,11 +220,25 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   u32* D = reinterpret_cast<u32*>(ws + L.D);
   stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm);
   rec(ev, 1, s);
-  K2Args k2{D, L.D_len, k, ctrl, reinterpret_cast<u32*>(ws + L.selbuf), reinterpret_cast<u32*>(ws + L.region_cnt),
-            L.R2};
-  k2_scan_delegates<<<L.g2, 256, 0, s>>>(k2);
+  K2Args k2{D,
+            L.D_len,
+            k,
+            ctrl,
+            reinterpret_cast<u32*>(ws + L.selbuf),
+            reinterpret_cast<u32*>(ws + L.region_cnt),
+            L.R2,
+            beta,
+            reinterpret_cast<u32*>(ws + L.sup_sid),
+            reinterpret_cast<u32*>(ws + L.sup_in),
+            reinterpret_cast<u32*>(ws + L.sup_cnt),
+            reinterpret_cast<u32*>(ws + L.sup_off)};
+  if (beta == 2)
+    k2_scan_delegates<1><<<L.g2, 256, 0, s>>>(k2);
+  else
+    k2_scan_delegates<0><<<L.g2, 256, 0, s>>>(k2);
   counted();
-  k2_pass3<<<grid_for(L.g2, nsm * 2), 256, 0, s>>>(ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2);
+  k2_pass3<<<grid_for(L.g2, 32), 256, 0, s>>>(ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
+                                                    reinterpret_cast<u32*>(ws + L.sup_off));
   counted();
   rec(ev, 2, s);
 }
@@ -411,11 +427,25 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
   u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);
   u32* t_cnt = reinterpret_cast<u32*>(ws + L.t_cnt);
-  u32* keepw = reinterpret_cast<u32*>(ws + L.keepw);
-  uint2* wsum = reinterpret_cast<uint2*>(ws + L.wsum);
-  K3Args k3{reinterpret_cast<const u32*>(ws + L.D), reinterpret_cast<const u32*>(ws + L.meta),
-            L.S, n, alpha, beta, ctrl, theta_override, rc, keepw, wsum, e_sid, t_sid, t_cnt, L.cap_e};
-  k3_classify<<<grid_for((L.words + 31) / 32, nsm * 8), 256, 0, s>>>(k3);
+  const u64 nseg = (u64)L.g2 * 8;
+  K3Args k3{reinterpret_cast<const u32*>(ws + L.D),
+            reinterpret_cast<const u32*>(ws + L.meta),
+            L.S,
+            n,
+            alpha,
+            beta,
+            ctrl,
+            theta_override,
+            rc,
+            reinterpret_cast<const u32*>(ws + L.sup_sid),
+            reinterpret_cast<const u32*>(ws + L.sup_in),
+            reinterpret_cast<const u32*>(ws + L.sup_off),
+            nseg,
+            e_sid,
+            t_sid,
+            t_cnt,
+            L.cap_e};
+  k3_classify<<<grid_for((nseg + 7) / 8, nsm * 8), 256, 0, s>>>(k3);
   counted();
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
             reinterpret_cast<u64*>(ws + L.stg_idx), reinterpret_cast<u32*>(ws + L.seg_gt),
@@ -423,15 +453,12 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   k4_read<MODE><<<grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4), 256, 0, s>>>(k4);
   counted();
   const int exact = (flags & DTOPK_FLAG_EXACT_STATS) ? 1 : 0;
-  K4TArgs k4t{keys, n,  L.S,   alpha, k, ctrl, t_sid, t_cnt, keepw, wsum, rc.r, reinterpret_cast<const u32*>(ws + L.seg_eq),
+  K4TArgs k4t{keys, n,  L.S,   alpha, k, ctrl, t_sid, t_cnt, rc.r, reinterpret_cast<const u32*>(ws + L.seg_eq),
               exact};
   k4t_count<MODE><<<grid_for((L.S + 7) / 8, nsm * 4), 256, 0, s>>>(k4t);
   counted();
   K5Args k5{ctrl,
             rc,
-            keepw,
-            wsum,
-            L.S,
             n,
             alpha,
             k,

@@ -19,15 +19,15 @@
 // qualified subranges), so the concatenation re-reads only the fully qualified
 // ones; all-equal keys make every candidate C and nothing is re-read.
 //
-//   K3  classification, fully parallel: warp per 32 subranges; the records of
-//       the qualifying subranges of a 32-subrange word are stored compacted at
-//       the start of that word's 32 slots, plus the word's keep mask.
+//   K3  classification of K2's candidate superset (subranges whose max
+//       delegate reaches theta's top-11-bit bucket, already in subrange
+//       order): one 16-byte record per entry, entries below theta inert.
 //   K4  reads the E candidates; each candidate part (<= 8192 keys) writes its
 //       elements > theta and its ties, in index order, into a private staging
 //       slot -- no global ordering needed.
-//   K5  ordered scan over the words (decoupled look-back over tiles of 2048
-//       words) -> positions in the pool P_gt (index order) and in the tie
-//       list (first k, index order).
+//   K5  ordered scan over the records (thread per record, decoupled
+//       look-back over tiles of 256) -> positions in the pool P_gt (index
+//       order) and in the tie list (first k, index order).
 //   K6  locates the ties of class-D records that fall among the first k ties.
 #pragma once
 
@@ -37,11 +37,11 @@
 
 namespace dtopk {
 
-enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4 };
+enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4, CLS_NONE = 5 };
 
 constexpr int K4_TILE = 8192;   // keys per K4 tile
-constexpr int K5_WPT = 4;       // words (32 subranges each) per K5 thread
-constexpr int K5_TILE = 256 * K5_WPT;
+constexpr int K5_RPT = 4;      // consecutive records per K5 thread
+constexpr int K5_TILE = 256 * K5_RPT;  // records per K5 tile
 constexpr int SMALL_POOL = 8192;  // pools up to this size are finished by one CTA (8 keys per thread)
 
 // One 16-byte record per qualifying subrange: x = sid, y = d_1,
@@ -59,16 +59,16 @@ struct K3Args {
   int beta;
   Ctrl* ctrl;
   const int64_t* theta_override;
-  Records rec;
-  u32* keepw;  // [S/32] keep mask of every 32-subrange word
-  uint2* wsum; // [S/32] per word: x = keys > theta, y = ties | 1 << 31 if an E/T record needs K4/K4T counts
+  Records rec;          // [sup_total] one record per superset entry, subrange order
+  const u32* sup_sid;   // K2 superset: subrange ids, per segment
+  const u32* sup_in;    // [nseg] first superset slot of each segment
+  const u32* sup_off;   // [nseg + 1] first record of each segment (K2 pass 3)
+  u64 nseg;
   u32* e_sid;  // [nE] subrange of each E candidate
   u32* t_sid;  // [nT] subrange of each T candidate
   u32* t_cnt;  // [nT] ties of each T candidate (zeroed here, filled by K4T)
   u64 cap_e;
 };
-
-__device__ __forceinline__ u32 sat_add31(u32 a, u64 b) { return (u32)min((u64)a + b, (u64)0x7fffffffu); }
 
 __device__ __forceinline__ u64 sub_len(u64 sid, u64 n, int alpha) {
   const u64 W = 1ull << alpha;
@@ -87,8 +87,11 @@ __device__ __forceinline__ u32 classify(u32 d1, u32 d2, u32 m, u32 theta, int be
   return meta_const(m) ? CLS_C : CLS_T;
 }
 
-// K3: qualification and classification.  Warp per 32-subrange word; the
-// loads of several words are in flight per warp.
+// K3: qualification and classification of the K2 superset (subranges whose
+// max delegate reaches theta's digit-1 bucket), warp per superset segment,
+// lane per entry.  Entries below theta become inert CLS_NONE records, so the
+// record array keeps the superset's subrange order without a second
+// compaction; D and meta are gathered only for superset entries.
 __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
   __shared__ ull s_stat[4][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -101,93 +104,78 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
   }
   if (blockIdx.x == 0 && tid == 0) ctrl->res.theta = theta;
   const int beta = a.beta;
-  const u64 nwords = (a.S + 31) / 32;
   const u64 gw = ((u64)blockIdx.x * 256 + tid) >> 5;
   const u64 nw = ((u64)gridDim.x * 256) >> 5;
   const u32 lt = lanemask_lt();
   ull st_cand = 0, st_fq = 0, st_pq = 0, st_a = 0;
-  u32 dmax = 0, gt_word = 0;
-  constexpr int U = 8;
-  for (u64 w0 = gw * U; w0 < nwords; w0 += nw * U) {
-    u32 d1[U], d2[U], dl[U];
+  u32 dmax = 0;
+  u64 gt_rec = 0;
+  for (u64 seg = gw; seg < a.nseg; seg += nw) {
+    const u64 in0 = a.sup_in[seg];
+    const u64 o0 = a.sup_off[seg];
+    const u32 cnt = a.sup_off[seg + 1] - (u32)o0;
+    constexpr int U = 1;  // 32-entry groups per warp step (more in flight measured slower)
+    for (u32 j0 = 0; j0 < cnt; j0 += 32 * U) {
+      u32 sid[U], d1[U], d2[U], dl[U], m[U];
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const u64 sid = (w0 + u) * 32 + lane;
-      d1[u] = d2[u] = dl[u] = 0;
-      if (sid < a.S) {
-        if (beta == 2) {
-          const uint2 v = *reinterpret_cast<const uint2*>(a.D + sid * 2);
-          d1[u] = v.x;
-          d2[u] = dl[u] = v.y;
-        } else {
-          d1[u] = a.D[sid * beta];
-          d2[u] = beta >= 2 ? a.D[sid * beta + 1] : d1[u];
-          dl[u] = a.D[sid * beta + beta - 1];
-        }
+      for (int u = 0; u < U; u++) {
+        const u32 j = j0 + u * 32 + lane;
+        sid[u] = j < cnt ? a.sup_sid[in0 + j] : 0u;
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const u64 w = w0 + u;
-      if (w >= nwords) break;
-      const u64 sid = w * 32 + lane;
-      const bool keep = sid < a.S && d1[u] >= theta;
-      const u32 mask = __ballot_sync(FULL, keep);
-      if (lane == 0) a.keepw[w] = mask;
-      if (!mask) {
-        if (lane == 0) a.wsum[w] = make_uint2(0u, 0u);
-        continue;
-      }
-      // per-word known counts: A -> 1 key > theta, B -> 1 tie, C -> len ties;
-      // E / T set the "needs records" flag (counts come from K4 / K4T)
-      // per-word known counts: A -> 1 key > theta, B -> 1 tie, C -> len ties;
-      // E / T set the "needs records" flag (counts come from K4 / K4T).
-      // 32-bit sums: a word holds at most 32 * 2^alpha ties; above alpha 26
-      // the flag is set instead so K5 counts from the records in 64 bits.
-      const u32 m = keep ? a.meta[sid] : 0u;
-      const u32 cls = keep ? classify(d1[u], d2[u], m, theta, beta) : CLS_A;
-      u32 kg = keep && cls == CLS_A ? 1u : 0u;
-      u32 ke = 0, kf = keep && cls >= CLS_T ? 1u : 0u;
-      if (keep && cls == CLS_B) ke = 1;
-      if (keep && cls == CLS_C) {
-        if (a.alpha <= 26) ke = (u32)sub_len(sid, a.n, a.alpha);
-        else kf = 1;
-      }
-      kg = __reduce_add_sync(FULL, kg);
-      ke = __reduce_add_sync(FULL, ke);
-      const u32 flag = __ballot_sync(FULL, kf);
-      if (lane == 0) a.wsum[w] = make_uint2(kg, ke | (flag ? 0x80000000u : 0u));
-      // E / T list slots: one atomic per warp and list, only when present
-      u32 x = cls | (dl[u] >= theta ? 8u : 0u);
-      if (flag) {
-        const u32 be = __ballot_sync(FULL, keep && cls == CLS_E), bt = __ballot_sync(FULL, keep && cls == CLS_T);
-        u32 e0 = 0, t0 = 0;
-        if (lane == 0) {
-          if (be) e0 = atomicAdd(&ctrl->nE, (u32)__popc(be));
-          if (bt) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
-        }
-        e0 = __shfl_sync(FULL, e0, 0);
-        t0 = __shfl_sync(FULL, t0, 0);
-        if (keep && cls == CLS_E) {
-          const u32 e = e0 + __popc(be & lt);
-          if (e < a.cap_e) a.e_sid[e] = (u32)sid;
-          x |= e << 4;
-        } else if (keep && cls == CLS_T) {
-          const u32 t = t0 + __popc(bt & lt);
-          a.t_sid[t] = (u32)sid;
-          a.t_cnt[t] = 0;
-          x |= t << 4;
+      for (int u = 0; u < U; u++) {
+        const u32 j = j0 + u * 32 + lane;
+        d1[u] = d2[u] = dl[u] = m[u] = 0;
+        if (j < cnt) {
+          if (beta == 2) {
+            const uint2 v = *reinterpret_cast<const uint2*>(a.D + (u64)sid[u] * 2);
+            d1[u] = v.x;
+            d2[u] = dl[u] = v.y;
+          } else {
+            d1[u] = a.D[(u64)sid[u] * beta];
+            d2[u] = beta >= 2 ? a.D[(u64)sid[u] * beta + 1] : d1[u];
+            dl[u] = a.D[(u64)sid[u] * beta + beta - 1];
+          }
+          m[u] = a.meta[sid[u]];
         }
       }
-      if (!keep) continue;
-      const bool fq = dl[u] >= theta;
-      const u64 slot = w * 32 + __popc(mask & lt);
-      a.rec.r[slot] = make_uint4((u32)sid, d1[u], m, x);
-      st_cand++;
-      dmax = max(dmax, d1[u]);
-      if (fq) st_fq++; else st_pq++;
-      if (cls == CLS_A) st_a++;
-      if (cls == CLS_A || cls == CLS_E) gt_word = max(gt_word, (u32)w + 1);
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const u32 j = j0 + u * 32 + lane;
+        const bool valid = j < cnt;
+        const bool keep = valid && d1[u] >= theta;
+        const u32 cls = keep ? classify(d1[u], d2[u], m[u], theta, beta) : CLS_NONE;
+        const bool fq = keep && dl[u] >= theta;
+        u32 x = cls | (fq ? 8u : 0u);
+        // E / T list slots: one atomic per list and 32 entries, only when present
+        const u32 be = __ballot_sync(FULL, cls == CLS_E), bt = __ballot_sync(FULL, cls == CLS_T);
+        if (be | bt) {
+          u32 e0 = 0, t0 = 0;
+          if (lane == 0) {
+            if (be) e0 = atomicAdd(&ctrl->nE, (u32)__popc(be));
+            if (bt) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
+          }
+          e0 = __shfl_sync(FULL, e0, 0);
+          t0 = __shfl_sync(FULL, t0, 0);
+          if (cls == CLS_E) {
+            const u32 e = e0 + __popc(be & lt);
+            if (e < a.cap_e) a.e_sid[e] = sid[u];
+            x |= e << 4;
+          } else if (cls == CLS_T) {
+            const u32 t = t0 + __popc(bt & lt);
+            a.t_sid[t] = sid[u];
+            a.t_cnt[t] = 0;
+            x |= t << 4;
+          }
+        }
+        if (valid) a.rec.r[o0 + j] = make_uint4(sid[u], d1[u], m[u], x);
+        if (!keep) continue;
+        st_cand++;
+        dmax = max(dmax, d1[u]);
+        if (fq) st_fq++; else st_pq++;
+        if (cls == CLS_A) st_a++;
+        if (cls == CLS_A || cls == CLS_E) gt_rec = max(gt_rec, o0 + j + 1);
+      }
     }
   }
   ull v[4] = {st_cand, st_fq, st_pq, st_a};
@@ -198,10 +186,11 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
     if (lane == 0) s_stat[i][warp] = v[i];
   }
   dmax = __reduce_max_sync(FULL, dmax);
-  gt_word = __reduce_max_sync(FULL, gt_word);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) gt_rec = max(gt_rec, (u64)__shfl_xor_sync(FULL, (ull)gt_rec, o));
   if (lane == 0) {
     if (dmax) atomicMax(&ctrl->maxkey, dmax);
-    if (gt_word) atomicMax(&ctrl->gt_rec_end, (ull)gt_word);
+    if (gt_rec) atomicMax(&ctrl->gt_rec_end, (ull)gt_rec);
   }
   __syncthreads();
   if (tid == 0) {
@@ -448,8 +437,6 @@ struct K4TArgs {
   Ctrl* ctrl;
   const u32* t_sid;
   u32* t_cnt;
-  const u32* keepw;
-  const uint2* wsum;
   const uint4* rec;
   const u32* seg_eq;
   int exact;  // DTOPK_FLAG_EXACT_STATS: count every T candidate
@@ -473,7 +460,8 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
     }
     return;
   }
-  const u64 nwords = (a.S + 31) / 32;
+  const u64 total = ctrl->sup_total;
+  const u64 nchunks = (total + 31) / 32;  // 32-record chunks, subrange order
   const int lseg = a.alpha < 13 ? a.alpha : 13;
   const u64 ppc = (1ull << a.alpha) >> lseg;
   for (;;) {
@@ -486,28 +474,36 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
       if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, 1ull);
       break;
     }
-    if (chunk * K4T_WORDS_PER_TICKET >= nwords) break;
-    // one word per warp: ties of its B/C/E/T records
+    if (chunk * K4T_WORDS_PER_TICKET >= nchunks) break;
+    // one 32-record chunk per warp, lane per record: ties of its B/C/E/T records
     u32 eq = 0;
-    const u64 w = chunk * K4T_WORDS_PER_TICKET + warp;
-    if (w < nwords) {
-      const uint2 sm = a.wsum[w];
-      eq = sm.y & 0x7fffffffu;
-      if (sm.y >> 31) {
-        const u32 cnt = __popc(a.keepw[w]);
-        for (u32 q = 0; q < cnt; q++) {
-          const uint4 rc = a.rec[w * 32 + q];
-          const u32 cls = rc.w & 7u;
-          if (cls == CLS_T) {
-            const u32 c = count_ties_warp<MODE>(a.keys, a.n, a.alpha, rc.x, theta);
-            if (lane == 0) a.t_cnt[rc.w >> 4] = c;
-            eq = (u32)min((u64)eq + c, (u64)0x7fffffffu);
-          } else if (cls == CLS_E) {
-            const u64 e = rc.w >> 4;
-            for (u64 p = 0; p < ppc; p++) eq = (u32)min((u64)eq + a.seg_eq[e * ppc + p], (u64)0x7fffffffu);
-          }
-        }
+    const u64 c = chunk * K4T_WORDS_PER_TICKET + warp;
+    if (c < nchunks) {
+      const u64 i = c * 32 + lane;
+      const uint4 rc = i < total ? a.rec[i] : make_uint4(0u, 0u, 0u, CLS_NONE);
+      const u32 cls = rc.w & 7u;
+      u64 e = 0;
+      if (cls == CLS_B) {
+        e = 1;
+      } else if (cls == CLS_C) {
+        e = sub_len(rc.x, a.n, a.alpha);
+      } else if (cls == CLS_E) {
+        const u64 ei = rc.w >> 4;
+        for (u64 p = 0; p < ppc; p++) e += a.seg_eq[ei * ppc + p];
       }
+      u32 bt = __ballot_sync(FULL, cls == CLS_T);
+      while (bt) {
+        const int q = __ffs(bt) - 1;
+        bt &= bt - 1;
+        const u32 sid = __shfl_sync(FULL, rc.x, q);
+        const u32 tix = __shfl_sync(FULL, rc.w >> 4, q);
+        const u32 cn = count_ties_warp<MODE>(a.keys, a.n, a.alpha, sid, theta);
+        if (lane == 0) a.t_cnt[tix] = cn;
+        if (lane == q) e += cn;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(FULL, (ull)e, o);
+      eq = (u32)min(e, (u64)0x7fffffffu);
     }
     if (lane == 0) s_eq[warp] = eq;
     __syncthreads();
@@ -523,10 +519,7 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
 // ---------------------------------------------------------------------------
 struct K5Args {
   Ctrl* ctrl;
-  Records rec;     // word-local record slots
-  const u32* keepw;
-  const uint2* wsum;
-  u64 S;
+  Records rec;     // [sup_total] records, subrange order
   u64 n;
   int alpha;
   u64 k;
@@ -553,7 +546,9 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64&
   const u32 cls = x & 7u;
   g = 0;
   e = 0;
-  if (cls == CLS_A) {
+  if (cls == CLS_NONE) {
+    return;
+  } else if (cls == CLS_A) {
     g = 1;
   } else if (cls == CLS_B) {
     e = 1;
@@ -572,7 +567,9 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64&
   }
 }
 
-// K5: ordered assembly of P_gt and of the first k ties, over 32-subrange words.
+// K5: ordered assembly of P_gt and of the first k ties: K5_RPT consecutive
+// records per thread, tiles of K5_TILE records in subrange order, block scans of the (keys >
+// theta, ties) counts and a decoupled look-back across tiles.
 __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
   __shared__ u64 s_tile, s_gx, s_ex;
   __shared__ int s_skip;
@@ -581,12 +578,12 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
   const u32 theta = ctrl->res.theta;
-  const u64 nwords = (a.S + 31) / 32;
-  const u64 T = (nwords + K5_TILE - 1) / K5_TILE;
-  const u64 gt_end = ctrl->gt_rec_end;  // 1 + last word holding elements > theta
+  const u64 total = ctrl->sup_total;
+  const u64 T = max((u64)1, (total + K5_TILE - 1) / K5_TILE);
+  const u64 gt_end = ctrl->gt_rec_end;  // 1 + last record holding elements > theta
   const int lseg = a.alpha < 13 ? a.alpha : 13;
   const u64 ppc = (1ull << a.alpha) >> lseg;
-  ull st_concat = 0, st_skipw = 0;
+  ull st_concat = 0;
   for (;;) {
     if (tid == 0) {
       s_tile = atomicAdd(&ctrl->k5_ticket, 1u);
@@ -617,30 +614,17 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
       __syncthreads();
       continue;
     }
-    const u64 w0 = tile * K5_TILE + (u64)tid * K5_WPT;
-    u32 masks[K5_WPT];
-    u64 tg = 0, te = 0;
+    const u64 i0 = tile * K5_TILE + (u64)tid * K5_RPT;
+    uint4 rcs[K5_RPT];
 #pragma unroll
-    for (int r = 0; r < K5_WPT; r++) {
-      masks[r] = 0;
-      if (w0 + r < nwords) {
-        const uint2 sm = a.wsum[w0 + r];
-        if (sm.y >> 31) {  // E / T records: exact counts from K4 / K4T
-          masks[r] = a.keepw[w0 + r];
-          const u32 cnt = __popc(masks[r]);
-          const uint4* wr = a.rec.r + (w0 + r) * 32;
-          for (u32 q = 0; q < cnt; q++) {
-            u64 g, e;
-            rec_counts(a, wr[q], g, e);
-            tg += g;
-            te += e;
-          }
-        } else {
-          tg += sm.x;
-          te += sm.y;
-          if (sm.x | sm.y) masks[r] = 0xffffffffu;  // records fetched in phase 2 only if they emit
-        }
-      }
+    for (int r = 0; r < K5_RPT; r++)
+      rcs[r] = i0 + r < total ? a.rec.r[i0 + r] : make_uint4(0u, 0u, 0u, CLS_NONE);
+    u64 cg[K5_RPT], ce[K5_RPT], tg = 0, te = 0;
+#pragma unroll
+    for (int r = 0; r < K5_RPT; r++) {
+      rec_counts(a, rcs[r], cg[r], ce[r]);
+      tg += cg[r];
+      te += ce[r];
     }
     const u64 ig = block_incl_scan_256<u64>(tg, scratch_g);
     const u64 ie = block_incl_scan_256<u64>(te, scratch_e);
@@ -677,72 +661,49 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
     __syncthreads();
     u64 gpos = s_gx + ig - tg, epos = s_ex + ie - te;
 #pragma unroll
-    for (int r = 0; r < K5_WPT; r++) {
-      if (!masks[r]) continue;
-      const uint2 sm = a.wsum[w0 + r];
-      if (!a.exact && !(sm.y >> 31) && sm.x == 0 && epos >= a.k) {
-        epos += sm.y;  // ties only, all beyond position k: nothing to place
-        st_skipw++;
-        continue;
-      }
-      const u32 cnt = __popc(a.keepw[w0 + r]);
-      const uint4* wr = a.rec.r + (w0 + r) * 32;
-      for (u32 q = 0; q < cnt; q++) {
-        const uint4 rc = wr[q];
-        const u32 x = rc.w;
-        const u32 cls = x & 7u;
-        const bool fq = (x >> 3) & 1u;
-        const u64 sid = rc.x;
-        const u64 base = sid << a.alpha;
-        if (cls == CLS_A) {
-          a.gt_keys[gpos] = rc.y;
-          a.gt_idx[gpos] = base + meta_p1(rc.z);
-          gpos++;
-        } else if (cls == CLS_B) {
-          if (epos < a.k) a.ties[epos] = base + meta_p1(rc.z);
-          epos++;
-        } else if (cls == CLS_C) {
-          const u64 len = sub_len(sid, a.n, a.alpha);
-          if (epos < a.k) {  // a run of ties: K6 writes it (one warp per run)
-            const u32 wslot = atomicAdd(&ctrl->k6_count, 1u);
-            a.d_sid[wslot] = (u32)sid;
-            a.d_pos[wslot] = epos;
-            a.d_need[wslot] = (u32)min(len, a.k - epos) | 0x80000000u;
-          }
-          if (fq) st_concat += len;
-          epos += len;
-        } else if (cls == CLS_T) {
-          const u64 c1 = a.t_cnt[x >> 4];
-          if (epos < a.k && c1) {
-            const u32 wslot = atomicAdd(&ctrl->k6_count, 1u);
-            a.d_sid[wslot] = (u32)sid;
-            a.d_pos[wslot] = epos;
-            a.d_need[wslot] = (u32)min(c1, a.k - epos);
-          }
-          if (fq) st_concat += c1;
-          epos += c1;
-        } else {
-          // the staged keys of E candidates are copied in parallel by K5b
-          const u64 eidx = x >> 4;
-          u64 eg = 0, ee = 0;
-          for (u64 p = 0; p < ppc; p++) {
-            eg += a.seg_gt[eidx * ppc + p];
-            ee += a.seg_eq[eidx * ppc + p];
-          }
-          a.e_gpos[eidx] = gpos;
-          a.e_epos[eidx] = epos;
-          gpos += eg;
-          epos += ee;
-          if (fq) st_concat += eg + ee;
+    for (int r = 0; r < K5_RPT; r++) {
+      const uint4 rc = rcs[r];
+      const u32 x = rc.w;
+      const u32 cls = x & 7u;
+      const bool fq = (x >> 3) & 1u;
+      const u64 sid = rc.x;
+      const u64 base = sid << a.alpha;
+      if (cls == CLS_A) {
+        a.gt_keys[gpos] = rc.y;
+        a.gt_idx[gpos] = base + meta_p1(rc.z);
+      } else if (cls == CLS_B) {
+        if (epos < a.k) a.ties[epos] = base + meta_p1(rc.z);
+      } else if (cls == CLS_C) {
+        if (epos < a.k) {  // a run of ties: K6 writes it (one warp per run)
+          const u32 wslot = atomicAdd(&ctrl->k6_count, 1u);
+          a.d_sid[wslot] = (u32)sid;
+          a.d_pos[wslot] = epos;
+          a.d_need[wslot] = (u32)min(ce[r], a.k - epos) | 0x80000000u;
         }
+        if (fq) st_concat += ce[r];
+      } else if (cls == CLS_T) {
+        if (epos < a.k && ce[r]) {
+          const u32 wslot = atomicAdd(&ctrl->k6_count, 1u);
+          a.d_sid[wslot] = (u32)sid;
+          a.d_pos[wslot] = epos;
+          a.d_need[wslot] = (u32)min(ce[r], a.k - epos);
+        }
+        if (fq) st_concat += ce[r];
+      } else if (cls == CLS_E) {
+        // the staged keys of E candidates are copied in parallel by K5b
+        const u64 eidx = x >> 4;
+        a.e_gpos[eidx] = gpos;
+        a.e_epos[eidx] = epos;
+        if (fq) st_concat += cg[r] + ce[r];
       }
+      gpos += cg[r];
+      epos += ce[r];
     }
+    (void)ppc;
     __syncthreads();
   }
   for (int o = 16; o; o >>= 1) st_concat += __shfl_xor_sync(FULL, st_concat, o);
-  st_skipw = __reduce_add_sync(FULL, (u32)st_skipw);
   if (lane == 0) s_cc[warp] = st_concat;
-  if (lane == 0 && st_skipw) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, st_skipw);
   __syncthreads();
   if (tid == 0) {
     ull t = 0;

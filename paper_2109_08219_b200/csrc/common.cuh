@@ -55,6 +55,43 @@ __device__ __forceinline__ u32 dig1(u32 k) { return k >> 21; }
 __device__ __forceinline__ u32 dig2(u32 k) { return (k >> 10) & 0x7ffu; }
 __device__ __forceinline__ u32 dig3(u32 k) { return k & 0x3ffu; }
 
+// Digits of the delegate threshold theta = kth(D).  Delegates are maxima, so
+// they crowd the top of the key range: a linear top-11-bit bucket can hold
+// most of D (the max of 2048 uniform keys lands in the top 1/2048 of the
+// range with probability 0.63).  The first digit is therefore log-scale in
+// the distance from the top, d = ~key: (leading zeros of d, next 6 bits of
+// d), 33 x 64 buckets ordered like the keys.  A bucket is a key interval
+// [kmin, kmin + 2^r) with r <= 25; digit 2 = (key - kmin) >> 12 (13 bits),
+// digit 3 = (key - kmin) & 4095.
+constexpr int NBD1 = 2304;  // 2112 used, padded to a multiple of 256 (find_digit)
+constexpr int NBD2 = 8192, NBD3 = 4096;
+__device__ __forceinline__ u32 ddig1(u32 key) {
+  const u32 d = ~key;
+  if (d == 0) return (32u << 6) | 63u;
+  const u32 c = __clz(d);
+  const u32 m = c >= 31 ? 0u : (d << (c + 1)) >> 26;
+  return (c << 6) | (63u - m);
+}
+// key interval [kmin, kmax] of log bucket b
+__device__ __forceinline__ void dbucket_range(u32 b, u32& kmin, u32& kmax) {
+  const u32 c = b >> 6, m = 63u - (b & 63u);
+  if (c >= 32) {
+    kmin = kmax = 0xffffffffu;
+    return;
+  }
+  const u32 lead = 1u << (31 - c);
+  u32 dlo, dhi;
+  if (c <= 25) {
+    const u32 r = 25 - c;
+    dlo = lead | (m << r);
+    dhi = dlo | ((1u << r) - 1u);
+  } else {
+    dlo = dhi = lead | (m >> (c - 25));
+  }
+  kmin = ~dhi;
+  kmax = ~dlo;
+}
+
 // ---------------------------------------------------------------------------
 // Control block (device memory, zeroed once per call).
 // ---------------------------------------------------------------------------
@@ -67,9 +104,9 @@ struct DigitResult {
 };
 
 struct SelectState {
-  ull hist1[NB1];
-  ull hist2[NB2];
-  ull hist3[NB3];
+  ull hist1[NBD1];  // sized for the delegate digits; the pool select uses NB1/NB2/NB3 of them
+  ull hist2[NBD2];
+  ull hist3[NBD3];
   ull buf_count;  // pass-2 compaction counter
   DigitResult r1, r2, r3;
   u32 kth;
@@ -88,6 +125,7 @@ struct Ctrl {
   ull cand_count;  // records
   ull nA;          // class-A records (one element > theta each)
   ull gt_rec_end;  // 1 + last record index that holds elements > theta
+  u32 sup_total;   // records = candidate-superset entries (K2, resolved with theta)
   ull sumEgt;      // elements > theta found by K4
   // assembly (K5) and tie location (K6)
   u32 k5_ticket;

@@ -42,7 +42,7 @@ constexpr int K1_CPS = DTOPK_K1_CPS;        // resident CTAs per SM
 constexpr int K1_STAGES = DTOPK_K1_STAGES;  // stages in flight (a multiple of the consumer warps)
 constexpr int K1_PREFETCH = DTOPK_K1_PREFETCH;  // chunks prefetched into L2 ahead of the TMA ring
 constexpr int K1_THREADS = (K1_CWARPS + 1) * 32;
-constexpr size_t K1_SMEM = (size_t)K1_STAGES * K1_CHUNK * 4 + 2 * K1_STAGES * 8 + NB1 * 4;
+constexpr size_t K1_SMEM = (size_t)K1_STAGES * K1_CHUNK * 4 + 2 * K1_STAGES * 8 + NBD1 * 4;
 
 struct K1Args {
   const u32* keys;
@@ -177,11 +177,11 @@ __device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 s
     if (one_writer) {  // a single emitting lane: no aggregation needed
       if (w) {
 #pragma unroll
-        for (int i = 0; i < B; i++) atomicAdd(&shist[L[i] >> 21], 1u);
+        for (int i = 0; i < B; i++) atomicAdd(&shist[ddig1(L[i])], 1u);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, w);
+      for (int i = 0; i < B; i++) hist_add_agg(shist, ddig1(L[i]), w);
     }
   }
 }
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
 
   const u64 nch = (a.n + K1_CHUNK - 1) >> K1_LOG_CHUNK;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < NB1; i += K1_THREADS) shist[i] = 0;
+  for (int i = tid; i < NBD1; i += K1_THREADS) shist[i] = 0;
   if (tid == 0) {
     for (int s = 0; s < K1_STAGES; s++) {
       mbar_init(&full[s], 1);
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   }
   __syncthreads();
   if (a.do_hist) {
-    for (int i = tid; i < NB1; i += K1_THREADS) {
+    for (int i = tid; i < NBD1; i += K1_THREADS) {
       const u32 v = shist[i];
       if (v) atomicAdd(&a.hist1[i], (ull)v);
     }
@@ -438,8 +438,8 @@ template <int B>
 __global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial, const u32* __restrict__ pmeta,
                                                 u64 nch, int alpha, u64 S, u32* __restrict__ D,
                                                 u32* __restrict__ meta, ull* __restrict__ hist1) {
-  __shared__ u32 shist[NB1];
-  for (int i = threadIdx.x; i < NB1; i += 256) shist[i] = 0;
+  __shared__ u32 shist[NBD1];
+  for (int i = threadIdx.x; i < NBD1; i += 256) shist[i] = 0;
   __syncthreads();
   const u64 cps = 1ull << (alpha - K1_LOG_CHUNK);
   const u64 stride = (u64)gridDim.x * 256;
@@ -462,10 +462,10 @@ __global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial,
 #pragma unroll
     for (int i = 0; i < B; i++) L[i] = A.L[i];
 #pragma unroll
-    for (int i = 0; i < B; i++) hist_add_agg(shist, L[i] >> 21, s < S);
+    for (int i = 0; i < B; i++) hist_add_agg(shist, ddig1(L[i]), s < S);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < NB1; i += 256) {
+  for (int i = threadIdx.x; i < NBD1; i += 256) {
     const u32 v = shist[i];
     if (v) atomicAdd(&hist1[i], (ull)v);
   }
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(256) k1_generic(const u32* __restrict__ keys, 
       if (r == 0) d1 = m;
       if (lane == 0) {
         D[s * beta + r] = m;
-        atomicAdd(&hist1[m >> 21], 1ull);
+        atomicAdd(&hist1[ddig1(m)], 1ull);
       }
     }
     // position of the first max and constant-subrange flag: second pass (cold path)

@@ -24,6 +24,13 @@ struct K2Args {
   u32* selbuf;  // region of CTA c: [c * R, c * R + region_cnt[c])
   u32* region_cnt;
   u64 R;        // delegates per CTA region (multiple of 512)
+  // candidate superset (delegate path): subranges whose max delegate lies in
+  // theta's top-11-bit bucket or above, in subrange order per warp segment
+  int beta;
+  u32* sup_sid;  // [S]: segment (cta, warp) writes from sup_in[seg]
+  u32* sup_in;   // [g2 * 8] first slot of each segment
+  u32* sup_cnt;  // [g2 * 8] entries of each segment
+  u32* sup_off;  // [g2 * 8 + 1] exclusive prefix of sup_cnt (theta resolver)
 };
 
 // Warp-aggregated append of `x` (where pred) to buf[*counter++].
@@ -38,84 +45,187 @@ __device__ __forceinline__ void warp_append(u32* buf, ull* counter, u32 x, bool 
   if (pred) buf[base + __popc(b & lanemask_lt())] = x;
 }
 
+// Resolve theta from the digit-3 histogram (ctrl->selD.hist3) and publish the
+// exclusive prefix of the superset segment counts.  One CTA (256 threads).
+__device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, const DigitResult& r2, u32 nregions,
+                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off, DigitResult* r3,
+                                 ull* scratch) {
+  const int tid = threadIdx.x;
+  find_digit<NBD3>(ctrl->selD.hist3, r2.rem, r3, scratch);
+  if (tid == 0) {
+    const u32 kth = kmin + (r2.digit << 12) + r3->digit;
+    ctrl->selD.r3 = *r3;
+    ctrl->selD.kth = kth;
+    ctrl->res.theta_local = kth;
+    ctrl->res.theta_slot = (int64_t)kth;
+    ctrl->res.delegate_bucket = r1.cnt;
+  }
+  if (sup_cnt == nullptr) return;
+  const u32 nseg = nregions * 8;
+  const u32 per = (nseg + 255) / 256;
+  u32 sum = 0;
+  for (u32 q = 0; q < per; q++) {
+    const u32 i = tid * per + q;
+    if (i < nseg) sum += __ldcg(&sup_cnt[i]);
+  }
+  u32* sc = reinterpret_cast<u32*>(scratch);
+  const u32 incl = block_incl_scan_256<u32>(sum, sc);
+  u32 run = incl - sum;
+  for (u32 q = 0; q < per; q++) {
+    const u32 i = tid * per + q;
+    if (i < nseg) {
+      sup_off[i] = run;
+      run += __ldcg(&sup_cnt[i]);
+    }
+  }
+  if (tid == 255) {
+    sup_off[nseg] = incl;
+    ctrl->sup_total = incl;
+  }
+}
+
 // K2: pass 2 of kth(D) -- one read of D.  CTA c owns the contiguous range
-// [c*R, (c+1)*R) of D; its warps histogram digit 2 of the delegates in
-// theta's digit-1 bucket and compact them into the CTA's own region of selbuf
-// through a shared-memory counter (no global atomics, no barriers in the loop).
+// [c*R, (c+1)*R) of D and each of its warps one eighth of it.  A warp step is
+// 512 delegates, 16 consecutive ones per lane (four uint4).  theta's digit-1
+// bucket is the key interval [kmin, kmax] (log-scale digit, ddig1):
+//   * delegates inside it: digit-2 histogram (shared memory) and compaction
+//     into the CTA's region of selbuf (order irrelevant);
+//   * max delegates d_1 >= kmin (every subrange that can qualify, whatever
+//     theta turns out to be inside the bucket): ordered compaction of their
+//     subrange ids into the warp's segment of the superset, the only input
+//     K3 reads -- D is not scanned again.
+// A lane first tests its 16 keys against kmin through their maximum (for
+// beta = 2 the max delegates alone), so most steps cost ~1 op per key.
+template <int BETA2>
 __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
-  __shared__ u32 shist[NB2];
+  __shared__ u32 shist[NBD2];
   __shared__ DigitResult r1;
   __shared__ ull scratch[8];
   __shared__ u32 s_cnt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < NB2; i += 256) shist[i] = 0;
+  for (int i = tid; i < NBD2; i += 256) shist[i] = 0;
   if (tid == 0) s_cnt = 0;
-  find_digit<NB1>(a.ctrl->selD.hist1, a.k, &r1, scratch);
+  find_digit<NBD1>(a.ctrl->selD.hist1, a.k, &r1, scratch);
   if (blockIdx.x == 0 && tid == 0) a.ctrl->selD.r1 = r1;
-  const u32 b1 = r1.digit;
+  u32 kmin, kmax;
+  dbucket_range(r1.digit, kmin, kmax);
+  const u32 span = kmax - kmin;
   const u64 lo = (u64)blockIdx.x * a.R;
   const u64 hi = min(a.nD, lo + a.R);
+  const u64 wlen = a.R / 8;
+  const u64 wlo = min(hi, lo + (u64)warp * wlen), whi = min(hi, wlo + wlen);
+  const u64 beta = BETA2 ? 2u : (u64)a.beta;
+  const u64 out0 = (wlo + beta - 1) / beta;  // first subrange whose d_1 lies in [wlo, whi)
   u32* region = a.selbuf + lo;
-  const u32 lt = lanemask_lt();
-  for (u64 base = lo + (u64)warp * 512; base < hi; base += 8 * 512) {
+  const bool sup = a.sup_sid != nullptr;
+  u32 run = 0;
+  for (u64 base = wlo; base < whi; base += 512) {
+    const u64 i0 = base + (u64)lane * 16;
     u32 v[16];
-    u32 bl[16];
-    u32 cnt = 0;
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-      const u64 i = base + (u64)j * 32 + lane;
-      v[j] = i < hi ? a.D[i] : 0u;
-    }
+    for (int j = 0; j < 4; j++) {
+      const u64 i = i0 + 4 * j;
+      if (i + 4 <= whi) {
+        const uint4 q = *reinterpret_cast<const uint4*>(a.D + i);
+        v[4 * j] = q.x;
+        v[4 * j + 1] = q.y;
+        v[4 * j + 2] = q.z;
+        v[4 * j + 3] = q.w;
+      } else {
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-      const u64 i = base + (u64)j * 32 + lane;
-      const bool p = i < hi && dig1(v[j]) == b1;
-      bl[j] = __ballot_sync(FULL, p);
-      cnt += __popc(bl[j]);
-      if (p) atomicAdd(&shist[dig2(v[j])], 1u);
+        for (int c = 0; c < 4; c++) v[4 * j + c] = i + c < whi ? a.D[i + c] : 0u;
+      }
     }
-    if (cnt) {
-      u32 o = 0;
-      if (lane == 0) o = atomicAdd(&s_cnt, cnt);
-      o = __shfl_sync(FULL, o, 0);
+    u32 mx = 0;
+    if (BETA2) {  // (d1, d2) pairs, d1 >= d2: the max of the lane is a max delegate
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) mx = max(mx, v[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j++) mx = max(mx, v[j]);
+    }
+    const bool any = mx >= kmin;
+    if (!__any_sync(FULL, any)) continue;
+    u32 nb = 0, nc = 0;
+    if (any) {
+      u32 r = BETA2 ? 0u : (u32)(i0 % beta);  // ladder slot of element i0 (i0 is even for beta 2)
 #pragma unroll
       for (int j = 0; j < 16; j++) {
-        if ((bl[j] >> lane) & 1u) region[o + __popc(bl[j] & lt)] = v[j];
-        o += __popc(bl[j]);
+        const bool in = i0 + j < whi;
+        nb += (in && v[j] - kmin <= span) ? 1u : 0u;
+        nc += (sup && in && r == 0 && v[j] >= kmin) ? 1u : 0u;
+        r = BETA2 ? (r ^ 1u) : ((r + 1 == (u32)beta) ? 0u : r + 1);
+      }
+    }
+    if (sup && __any_sync(FULL, nc)) {
+      const u32 incl = warp_incl_scan<u32>(nc);
+      u64 o = out0 + run + incl - nc;
+      run += __shfl_sync(FULL, incl, 31);
+      if (nc) {
+        u32 rr = BETA2 ? 0u : (u32)(i0 % beta);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          if (i0 + j < whi && rr == 0 && v[j] >= kmin) a.sup_sid[o++] = (u32)((i0 + j) / beta);
+          rr = BETA2 ? (rr ^ 1u) : ((rr + 1 == (u32)beta) ? 0u : rr + 1);
+        }
+      }
+    }
+    if (!__any_sync(FULL, nb)) continue;
+    const u32 incl = warp_incl_scan<u32>(nb);
+    u32 o = 0;
+    if (lane == 31) o = atomicAdd(&s_cnt, incl);
+    o = __shfl_sync(FULL, o, 31) + incl - nb;
+    if (nb) {
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        if (i0 + j < whi && v[j] - kmin <= span) {
+          atomicAdd(&shist[(v[j] - kmin) >> 12], 1u);
+          region[o++] = v[j];
+        }
       }
     }
   }
+  if (sup && lane == 0) {
+    a.sup_in[blockIdx.x * 8 + warp] = (u32)out0;
+    a.sup_cnt[blockIdx.x * 8 + warp] = run;
+  }
   __syncthreads();
+  Ctrl* ctrl = a.ctrl;
   if (tid == 0) a.region_cnt[blockIdx.x] = s_cnt;
-  for (int i = tid; i < NB2; i += 256) {
+  for (int i = tid; i < NBD2; i += 256) {
     const u32 c = shist[i];
-    if (c) atomicAdd(&a.ctrl->selD.hist2[i], (ull)c);
+    if (c) atomicAdd(&ctrl->selD.hist2[i], (ull)c);
   }
 }
 
-// Pass 3 of kth(D) over the compacted bucket regions; the last CTA resolves theta.
+// Pass 3 of kth(D) over the compacted bucket regions;
+// the last CTA resolves theta and the superset record offsets.
 __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
-                                                const u32* __restrict__ region_cnt, u32 nregions, u64 R) {
-  __shared__ u32 shist[NB3];
-  __shared__ DigitResult r2, r3;
+                                                const u32* __restrict__ region_cnt, u32 nregions, u64 R,
+                                                const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off) {
+  __shared__ u32 shist[NBD3];
+  __shared__ DigitResult r3;
   __shared__ ull scratch[8];
   __shared__ int am_last;
   const int tid = threadIdx.x;
-  for (int i = tid; i < NB3; i += 256) shist[i] = 0;
+  for (int i = tid; i < NBD3; i += 256) shist[i] = 0;
+  __shared__ DigitResult r2;
   const DigitResult r1 = ctrl->selD.r1;
-  find_digit<NB2>(ctrl->selD.hist2, r1.rem, &r2, scratch);
+  u32 kmin, kmax;
+  dbucket_range(r1.digit, kmin, kmax);
+  find_digit<NBD2>(ctrl->selD.hist2, r1.rem, &r2, scratch);
   if (blockIdx.x == 0 && tid == 0) ctrl->selD.r2 = r2;
   const u32 b2 = r2.digit;
   for (u32 g = blockIdx.x; g < nregions; g += gridDim.x) {
     const u32 cnt = region_cnt[g];
     const u32* reg = selbuf + (u64)g * R;
     for (u32 i = tid; i < cnt; i += 256) {
-      const u32 x = reg[i];
-      if (dig2(x) == b2) atomicAdd(&shist[dig3(x)], 1u);
+      const u32 x = reg[i] - kmin;
+      if ((x >> 12) == b2) atomicAdd(&shist[x & 4095u], 1u);
     }
   }
   __syncthreads();
-  for (int i = tid; i < NB3; i += 256) {
+  for (int i = tid; i < NBD3; i += 256) {
     const u32 v = shist[i];
     if (v) atomicAdd(&ctrl->selD.hist3[i], (ull)v);
   }
@@ -125,15 +235,7 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   __syncthreads();
   if (am_last) {
     __threadfence();
-    find_digit<NB3>(ctrl->selD.hist3, r2.rem, &r3, scratch);
-    if (tid == 0) {
-      const u32 kth = (r1.digit << 21) | (b2 << 10) | r3.digit;
-      ctrl->selD.r3 = r3;
-      ctrl->selD.kth = kth;
-      ctrl->res.theta_local = kth;
-      ctrl->res.theta_slot = (int64_t)kth;
-      ctrl->res.delegate_bucket = r1.cnt;
-    }
+    k2_resolve_theta(ctrl, kmin, r1, r2, nregions, sup_cnt, sup_off, &r3, scratch);
   }
 }
 
