@@ -196,12 +196,15 @@ def run_ours(args):
     from paper_2109_08219_b200.pipeline import DrTopK
 
     world, rank, local = _dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # DTOPK_DIST_BACKEND=gloo lets several ranks share one GPU (functional runs on a 1-GPU box;
+    # NCCL refuses duplicate devices).  The product path is NCCL, one rank per GPU.
+    backend = os.environ.get("DTOPK_DIST_BACKEND", "nccl")
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     lib = _native.load()
     n = 1 << args.log2n
     k = args.k
@@ -227,8 +230,12 @@ def run_ours(args):
     if world == 1:
         step = lambda ev=None: plan.launch(v, stream, events=ev)  # noqa: E731
     else:
+        # weak scaling: rank r owns keys [r*n, (r+1)*n) of one n*world vector; K1-K2 locally,
+        # theta all-reduce(MAX), K3.. with theta*, all-gather of <= k pairs per rank, device merge
+        sharded = dtopk.ShardedTopK(v, n * world, k, cfg, index_offset=rank * n)
+
         def step(ev=None):
-            dtopk.sharded_topk(v, n * world, k, cfg)
+            sharded.step()
 
     # per-step stage events on the launch stream: the K1 (Delegate) duration
     # of every timed step is measured live inside the timed region
@@ -254,7 +261,7 @@ def run_ours(args):
     ms = t_start.elapsed_time(t_end) / args.steps
     ms = max_over_ranks(ms)
     value = n * world / (ms * 1e-3)
-    hdr = plan.header()
+    hdr = plan.header() if world == 1 else sharded.local.header()
     graph_info = None
     if world == 1 and plan.use_graph:
         main_k, tail_k = plan.plan_kernels(v)
@@ -364,16 +371,19 @@ def run_ours(args):
             if world == 1:
                 r = dtopk.dr_topk(host, cfg)
             else:
-                dv = host.to(dev, non_blocking=True)
-                r = dtopk.sharded_topk(dv, n * world, k, cfg)
-                r.values.cpu()
-                r.indices.cpu()
+                v.copy_(host, non_blocking=True)
+                sharded.step()
+                sharded.values.cpu()
+                sharded.indices.cpu()
         torch.cuda.synchronize()
         e2e_s = max_over_ranks((time.perf_counter() - t0) / reps)
         if rank == 0:
             out["e2e"] = {"value": n * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 4,
-                          "d2h_bytes_per_step": k * (4 + 8) + 104, "ms_per_step": e2e_s * 1e3,
-                          "path": "paper_2109_08219_b200.dr_topk(pinned host tensor) -> numpy-style host results"}
+                          "d2h_bytes_per_step": k * (4 + 8) + (104 if world == 1 else 0), "ms_per_step": e2e_s * 1e3,
+                          "path": ("paper_2109_08219_b200.dr_topk(pinned host tensor) -> numpy-style host results"
+                                   if world == 1 else
+                                   "pinned host shard -> HBM, ShardedTopK.step (NCCL theta all-reduce + pair "
+                                   "all-gather + device merge), answer -> host")}
         del host
 
     for e in stage_ev:

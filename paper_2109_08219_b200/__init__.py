@@ -27,7 +27,7 @@ from .core import (
     validate_config,
 )
 from .delegate import DelegateVector, extract_delegates, extract_delegates_blocked
-from .distributed import PartitionPlan, WorkerFailed, plan, shard_bounds, sharded_topk
+from .distributed import PartitionPlan, ShardedTopK, WorkerFailed, plan, shard_bounds, sharded_topk
 from .kernels import KeyedEntry, kth_largest, radix_topk
 from .pipeline import DrTopK, QualificationReport, concatenate_filtered, dr_topk, first_topk
 from .tuning import auto_alpha
@@ -46,6 +46,7 @@ __all__ = [
     "InvalidK",
     "KeyedEntry",
     "PartitionPlan",
+    "ShardedTopK",
     "PipelineConfig",
     "QualificationReport",
     "TopKResult",

@@ -196,6 +196,128 @@ def sharded_topk(shard, n_total: int, k: int, cfg: PipelineConfig | None = None,
     return TopKResult(values=values, threshold=thr, stats=stats, indices=indices)
 
 
+class ShardedTopK:
+    """Planned ``sharded_topk`` for one rank (fixed shard size, k, config, dtype).
+
+    The benchmark and serving path: workspaces and buffers are allocated once,
+    and a step never synchronises the host.  Per step, on the current stream:
+    K1-K2 (``dtopk_select_begin``) -> all_reduce(MAX) of the int64 theta slot,
+    in place in the workspace -> K3.. (``dtopk_select_finish`` with theta*) ->
+    all_gather of the device-side pair count and of the fixed-size (value,
+    global index) buffers -> device compaction that moves every rank's valid
+    pairs to the front in rank order (padding after them, worst key) -> exact
+    device top-k of the concatenation (direct radix path of the same library),
+    whose positions map back to global indices.  Rank order is global index
+    order, so the tie rule (lowest index first) holds across ranks.
+    """
+
+    def __init__(self, shard: torch.Tensor, n_total: int, k: int, cfg: PipelineConfig | None = None, *,
+                 group=None, index_offset: int | None = None, exchange_theta: bool = True):
+        from . import _device, _native
+        from .pipeline import DrTopK
+
+        cfg = cfg or PipelineConfig(k=k)
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        dv = _device.to_device(shard)
+        if dv.kind != "torch_cuda":
+            raise ValueError("ShardedTopK needs the shard resident on this rank's GPU")
+        self.dv = dv
+        self.n_local = dv.n
+        if not 1 <= k <= n_total:
+            raise InvalidK(f"k={k} outside [1, {n_total}]")
+        if index_offset is None:
+            index_offset, _ = shard_bounds(n_total, self.world, self.rank)
+        self.index_offset = int(index_offset)
+        self.k = int(k)
+        self.k_local = min(self.k, self.n_local)
+        self.lcfg = validate_config(replace(cfg, k=self.k_local), self.n_local)
+        self.exchange_theta = exchange_theta
+        dev = dv.device
+        self.local = DrTopK(self.n_local, self.lcfg, dv.code, dv.out_dtype, dev, timed=False)
+        self.lib = self.local.lib
+        ws = self.local.ws
+        off = _native.DtopkResult.theta_slot.offset
+        self.theta = ws[off:off + 8].view(torch.int64)
+        koff = _native.DtopkResult.k_out.offset
+        self.kout = ws[koff:koff + 8].view(torch.int64)
+        w, kl = self.world, self.k_local
+        self.cat_n = w * kl
+        # worst key of the merge order, as the raw bits of the output dtype
+        worst = {(_native.DTYPE_U32, True): 0, (_native.DTYPE_U32, False): -1,
+                 (_native.DTYPE_F32, True): -1, (_native.DTYPE_F32, False): 0x7FFFFFFF}[(dv.code, self.lcfg.largest)]
+        self.pad_bits = torch.tensor(worst, dtype=torch.int32, device=dev)
+        self.g_cnt = torch.empty(w, dtype=torch.int64, device=dev)
+        self.g_val = torch.empty(self.cat_n, dtype=torch.int32, device=dev)
+        self.g_idx = torch.empty(self.cat_n, dtype=torch.int64, device=dev)
+        self.cat_val = torch.empty(self.cat_n, dtype=torch.int32, device=dev)
+        self.cat_idx = torch.empty(self.cat_n, dtype=torch.int64, device=dev)
+        self.j = torch.arange(kl, dtype=torch.int64, device=dev).view(1, kl)
+        self.merge = DrTopK(self.cat_n, PipelineConfig(k=self.k, alpha=0, auto_alpha=False, largest=self.lcfg.largest),
+                            dv.code, dv.out_dtype, dev, timed=False)
+        self.values = self.merge.values
+        self.indices = torch.empty(self.k, dtype=torch.int64, device=dev)
+
+    def step(self, keys: torch.Tensor | None = None) -> None:
+        """One sharded top-k; results in ``self.values`` / ``self.indices`` (stream-ordered)."""
+        from . import _native
+
+        keys = self.dv.keys if keys is None else keys
+        p, c = self.local, self.lcfg
+        s = torch.cuda.current_stream(self.dv.device)
+        if c.direct_fallback:
+            p.launch(keys, s, index_offset=self.index_offset)
+        else:
+            _native.check(p.lib.dtopk_select_begin(keys.data_ptr(), self.n_local, self.dv.code, c.k, int(c.largest),
+                                                   c.alpha, c.beta, p.flags, p.ws.data_ptr(), p.ws_bytes,
+                                                   s.cuda_stream, None), "dtopk_select_begin")
+            if self.exchange_theta:
+                dist.all_reduce(self.theta, op=dist.ReduceOp.MAX, group=self.group)
+            _native.check(p.lib.dtopk_select_finish(
+                keys.data_ptr(), self.n_local, self.dv.code, c.k, int(c.largest), c.alpha, c.beta, p.flags,
+                self.theta.data_ptr() if self.exchange_theta else None, p.values.data_ptr(), p.indices.data_ptr(),
+                self.index_offset, p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None), "dtopk_select_finish")
+        kl = self.k_local
+        cnt = self.kout.clamp(max=kl) if not c.direct_fallback else torch.full_like(self.kout, kl)
+        _all_gather_flat(self.g_cnt, cnt, self.group)
+        _all_gather_flat(self.g_val, p.values.view(torch.int32)[:kl], self.group)
+        _all_gather_flat(self.g_idx, p.indices[:kl], self.group)
+        # compaction: rank r's first cnt_r pairs to [pre_r, pre_r + cnt_r), padding to the tail
+        cnt_r = self.g_cnt.view(-1, 1)
+        valid = self.j < cnt_r
+        pre = torch.cumsum(self.g_cnt, 0) - self.g_cnt
+        total = self.g_cnt.sum()
+        inval = kl - self.g_cnt
+        pre_inv = torch.cumsum(inval, 0) - inval
+        dest = torch.where(valid, pre.view(-1, 1) + self.j, total + pre_inv.view(-1, 1) + (self.j - cnt_r))
+        vals = torch.where(valid.view(-1), self.g_val, self.pad_bits)
+        self.cat_val.scatter_(0, dest.view(-1), vals)
+        self.cat_idx.scatter_(0, dest.view(-1), self.g_idx)
+        self.merge.launch(self.cat_val.view(self.values.dtype), s)
+        torch.index_select(self.cat_idx, 0, self.merge.indices, out=self.indices)
+
+    def result(self) -> TopKResult:
+        """Synchronise and wrap the last step's answer (reads the merge header)."""
+        from .core import WorkloadStats as _WS
+
+        hdr = self.merge.header()
+        stats = _WS()
+        stats.device = {"gathered_pairs": int(self.g_cnt.sum().item()), "theta_global": int(self.theta.item())}
+        from . import _device
+
+        thr = _device.key_to_value(int(hdr.kth_key), self.dv.code, self.lcfg.largest)
+        return TopKResult(values=self.values, threshold=thr, stats=stats, indices=self.indices)
+
+
+def _all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    """all_gather of equal-size contributions into one flat tensor (rank order)."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+    else:  # gloo (CPU tests, or several ranks sharing one GPU): list form
+        dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp, group=group)
+
+
 def _dev_of(x):
     return x.device if isinstance(x, torch.Tensor) else torch.device("cpu")
 

@@ -310,3 +310,22 @@ def test_graph_plan_replay_matches_eager(k, oracle_mod, cuda):
         np.testing.assert_array_equal(p.indices.cpu().numpy(), ei)
         np.testing.assert_array_equal(p.values.cpu().numpy(), ek)
         v.view(torch.int32)[::97] += 1  # new data, same buffer: the plan re-reads it
+
+
+def test_sharded_two_ranks_on_one_gpu(cuda):
+    """The multi-rank product path (ShardedTopK and sharded_topk) against the
+    oracle with 2 ranks; gloo lets both ranks share this box's single GPU."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, DTOPK_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "tools/dist_check.py"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
