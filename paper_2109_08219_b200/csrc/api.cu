@@ -39,7 +39,7 @@ inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 int num_sms();
 
 struct Layout {
-  size_t ctrl, lb_k5g, lb_k5e, lb_emg, lb_eme, zero_bytes;
+  size_t ctrl, lb_emg, lb_eme, zero_bytes, k5_tg, k5_te;
   size_t D, meta, partial, pmeta, selbuf, region_cnt, sup_sid, sup_in, sup_cnt, sup_off, rec, e_sid, t_sid, t_cnt,
       stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, e_gpos, e_epos, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
       digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, total;
@@ -83,8 +83,6 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.sort_tiles = (L.sort_cap + ST_TILE - 1) / ST_TILE;
   L.ctrl = take(sizeof(Ctrl));
   L.bk_total = take(L.sort_cap > (u64)SMALL_SORT ? BK_MAX * 4 : 0);
-  L.lb_k5g = take(L.k5_tiles * 8);
-  L.lb_k5e = take(L.k5_tiles * 8);
   L.lb_emg = take(L.em_tiles * 8);
   L.lb_eme = take(L.em_tiles * 8);
   L.zero_bytes = off;
@@ -95,11 +93,13 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.pmeta = take(parts ? 2 * L.nch * 4 : 0);
   L.selbuf = take(std::max<u64>((u64)L.g2 * L.R2, L.m_emit) * 4);
   L.region_cnt = take((u64)L.g2 * 4);
-  L.sup_sid = take(L.S * 4);
+  L.sup_sid = take(L.S * 16);
   L.sup_in = take((u64)L.g2 * 8 * 4);
   L.sup_cnt = take((u64)L.g2 * 8 * 4);
   L.sup_off = take(((u64)L.g2 * 8 + 1) * 4);
   L.rec = take(L.S * 16);
+  L.k5_tg = take(L.k5_tiles * 8);
+  L.k5_te = take(L.k5_tiles * 8);
   L.e_sid = take(L.cap_e * 4);
   L.t_sid = take(L.S * 4);
   L.t_cnt = take(L.S * 4);
@@ -228,7 +228,7 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
             reinterpret_cast<u32*>(ws + L.region_cnt),
             L.R2,
             beta,
-            reinterpret_cast<u32*>(ws + L.sup_sid),
+            reinterpret_cast<uint4*>(ws + L.sup_sid),
             reinterpret_cast<u32*>(ws + L.sup_in),
             reinterpret_cast<u32*>(ws + L.sup_cnt),
             reinterpret_cast<u32*>(ws + L.sup_off)};
@@ -237,7 +237,7 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   else
     k2_scan_delegates<0><<<L.g2, 256, 0, s>>>(k2);
   counted();
-  k2_pass3<<<grid_for(L.g2, 32), 256, 0, s>>>(ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
+  k2_pass3<<<grid_for(L.g2, nsm), 256, 0, s>>>(ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
                                                     reinterpret_cast<u32*>(ws + L.sup_off));
   counted();
   rec(ev, 2, s);
@@ -437,14 +437,15 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
             ctrl,
             theta_override,
             rc,
-            reinterpret_cast<const u32*>(ws + L.sup_sid),
+            reinterpret_cast<const uint4*>(ws + L.sup_sid),
             reinterpret_cast<const u32*>(ws + L.sup_in),
             reinterpret_cast<const u32*>(ws + L.sup_off),
             nseg,
             e_sid,
             t_sid,
             t_cnt,
-            L.cap_e};
+            L.cap_e,
+            reinterpret_cast<u64*>(ws + L.e_epos)};
   k3_classify<<<grid_for((nseg + 7) / 8, nsm * 8), 256, 0, s>>>(k3);
   counted();
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
@@ -475,10 +476,12 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
             reinterpret_cast<u32*>(ws + L.d_need),
             reinterpret_cast<u64*>(ws + L.e_gpos),
             reinterpret_cast<u64*>(ws + L.e_epos),
-            reinterpret_cast<u64*>(ws + L.lb_k5g),
-            reinterpret_cast<u64*>(ws + L.lb_k5e),
+            reinterpret_cast<u64*>(ws + L.k5_tg),
+            reinterpret_cast<u64*>(ws + L.k5_te),
             exact};
-  k5_assemble<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
+  k5_count<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
+  counted();
+  k5_emit<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
   counted();
   k5b_copy<<<grid_for((L.nseg + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, alpha, k, k5.stg_key, k5.stg_idx, k5.seg_gt,
                                                                k5.seg_eq, k5.e_gpos, k5.e_epos, L.cap_e,

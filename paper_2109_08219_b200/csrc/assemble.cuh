@@ -60,7 +60,7 @@ struct K3Args {
   Ctrl* ctrl;
   const int64_t* theta_override;
   Records rec;          // [sup_total] one record per superset entry, subrange order
-  const u32* sup_sid;   // K2 superset: subrange ids, per segment
+  const uint4* sup_sid;  // K2 superset: {sid, d_1, d_2, d_beta} (beta 2) or {sid, d_1, -, -}, per segment
   const u32* sup_in;    // [nseg] first superset slot of each segment
   const u32* sup_off;   // [nseg + 1] first record of each segment (K2 pass 3)
   u64 nseg;
@@ -68,6 +68,7 @@ struct K3Args {
   u32* t_sid;  // [nT] subrange of each T candidate
   u32* t_cnt;  // [nT] ties of each T candidate (zeroed here, filled by K4T)
   u64 cap_e;
+  u64* e_epos;  // [nE] tie-list position of each E candidate: set to "beyond k" here, by k5_emit if it places ties
 };
 
 __device__ __forceinline__ u64 sub_len(u64 sid, u64 n, int alpha) {
@@ -120,19 +121,18 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const u32 j = j0 + u * 32 + lane;
-        sid[u] = j < cnt ? a.sup_sid[in0 + j] : 0u;
+        const uint4 e = j < cnt ? a.sup_sid[in0 + j] : make_uint4(0u, 0u, 0u, 0u);
+        sid[u] = e.x;
+        d1[u] = e.y;
+        d2[u] = e.z;
+        dl[u] = e.w;
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const u32 j = j0 + u * 32 + lane;
-        d1[u] = d2[u] = dl[u] = m[u] = 0;
-        if (j < cnt) {
-          if (beta == 2) {
-            const uint2 v = *reinterpret_cast<const uint2*>(a.D + (u64)sid[u] * 2);
-            d1[u] = v.x;
-            d2[u] = dl[u] = v.y;
-          } else {
-            d1[u] = a.D[(u64)sid[u] * beta];
+        m[u] = 0;
+        if (j < cnt && d1[u] >= theta) {  // D and meta gathered for qualifying entries only
+          if (beta != 2) {
             d2[u] = beta >= 2 ? a.D[(u64)sid[u] * beta + 1] : d1[u];
             dl[u] = a.D[(u64)sid[u] * beta + beta - 1];
           }
@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
           t0 = __shfl_sync(FULL, t0, 0);
           if (cls == CLS_E) {
             const u32 e = e0 + __popc(be & lt);
-            if (e < a.cap_e) a.e_sid[e] = sid[u];
+            if (e < a.cap_e) {
+              a.e_sid[e] = sid[u];
+              a.e_epos[e] = ~0ull;  // k5_emit may skip this record's tile: then K5b must place nothing
+            }
             x |= e << 4;
           } else if (cls == CLS_T) {
             const u32 t = t0 + __popc(bt & lt);
@@ -536,8 +539,8 @@ struct K5Args {
   u32* d_need;
   u64* e_gpos;       // per E candidate: first slot in P_gt / in the tie list (K5b copies)
   u64* e_epos;
-  u64* lb_gt;
-  u64* lb_eq;
+  u64* tile_g;   // [tiles] keys > theta per record tile (K5a), then its exclusive prefix
+  u64* tile_e;   // [tiles] ties per record tile (K5a), then its exclusive prefix
   int exact;         // DTOPK_FLAG_EXACT_STATS: never skip (exact concatenated_len)
 };
 
@@ -567,105 +570,127 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64&
   }
 }
 
-// K5: ordered assembly of P_gt and of the first k ties: K5_RPT consecutive
-// records per thread, tiles of K5_TILE records in subrange order, block scans of the (keys >
-// theta, ties) counts and a decoupled look-back across tiles.
-__global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
-  __shared__ u64 s_tile, s_gx, s_ex;
-  __shared__ int s_skip;
+// K5 runs as two kernels over record tiles (K5_RPT consecutive records per
+// thread, K5_TILE per tile) -- no serial look-back chain:
+//   k5_count  per-tile (keys > theta, ties) counts; the last CTA turns them
+//             into exclusive prefixes and publishes |P_gt|, the path, k_out
+//   k5_emit   per tile, block scans on top of the tile prefix -> positions in
+//             P_gt (index order) and in the first-k tie list
+template <bool EMIT>
+__device__ __forceinline__ void k5_tile_counts(const K5Args& a, u64 i0, u64 total, uint4 (&rcs)[K5_RPT],
+                                               u64 (&cg)[K5_RPT], u64 (&ce)[K5_RPT], u64& tg, u64& te) {
+  tg = te = 0;
+#pragma unroll
+  for (int r = 0; r < K5_RPT; r++)
+    rcs[r] = i0 + r < total ? a.rec.r[i0 + r] : make_uint4(0u, 0u, 0u, CLS_NONE);
+#pragma unroll
+  for (int r = 0; r < K5_RPT; r++) {
+    rec_counts(a, rcs[r], cg[r], ce[r]);
+    tg += cg[r];
+    te += ce[r];
+  }
+}
+
+__global__ void __launch_bounds__(256) k5_count(K5Args a) {
   __shared__ u64 scratch_g[8], scratch_e[8];
   __shared__ ull s_cc[8];
+  __shared__ int am_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
-  const u32 theta = ctrl->res.theta;
   const u64 total = ctrl->sup_total;
   const u64 T = max((u64)1, (total + K5_TILE - 1) / K5_TILE);
-  const u64 gt_end = ctrl->gt_rec_end;  // 1 + last record holding elements > theta
-  const int lseg = a.alpha < 13 ? a.alpha : 13;
-  const u64 ppc = (1ull << a.alpha) >> lseg;
   ull st_concat = 0;
-  for (;;) {
-    if (tid == 0) {
-      s_tile = atomicAdd(&ctrl->k5_ticket, 1u);
-      s_skip = !a.exact && ld_volatile_u32(&ctrl->ties_full) && s_tile * K5_TILE >= gt_end;
-    }
-    __syncthreads();
-    const u64 tile = s_tile;
-    if (tile >= T) break;
-    if (s_skip) {
-      // nothing > theta from here on and the first k ties are placed: publish
-      // the final prefix without reading anything
-      if (tid == 0) {
-        const u64 G = ctrl->nA + ctrl->sumEgt;
-        atomicAdd((ull*)&ctrl->res.concat_skipped_fq, 1ull);  // concatenated_len becomes a lower bound
-        st_release(&a.lb_gt[tile], LB_PRE | G);
-        st_release(&a.lb_eq[tile], LB_PRE | a.k);
-        if (tile == T - 1) {
-          ctrl->res.pool_gt = G;
-          ctrl->res.pool_eq = a.k;
-          ctrl->res.path = G >= a.k ? PATH_SELECT : PATH_MERGE;
-          ctrl->res.k_out = a.k;
-          if (G < a.k) {
-            ctrl->sort_lo = theta;
-            atomicMax(&ctrl->maxkey, theta);
-          }
-        }
-      }
-      __syncthreads();
-      continue;
-    }
-    const u64 i0 = tile * K5_TILE + (u64)tid * K5_RPT;
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
     uint4 rcs[K5_RPT];
-#pragma unroll
-    for (int r = 0; r < K5_RPT; r++)
-      rcs[r] = i0 + r < total ? a.rec.r[i0 + r] : make_uint4(0u, 0u, 0u, CLS_NONE);
-    u64 cg[K5_RPT], ce[K5_RPT], tg = 0, te = 0;
+    u64 cg[K5_RPT], ce[K5_RPT], tg, te;
+    k5_tile_counts<false>(a, tile * K5_TILE + (u64)tid * K5_RPT, total, rcs, cg, ce, tg, te);
 #pragma unroll
     for (int r = 0; r < K5_RPT; r++) {
-      rec_counts(a, rcs[r], cg[r], ce[r]);
-      tg += cg[r];
-      te += ce[r];
+      const u32 x = rcs[r].w, cls = x & 7u;
+      if (((x >> 3) & 1u) && (cls == CLS_C || cls == CLS_T || cls == CLS_E)) st_concat += cg[r] + ce[r];
     }
     const u64 ig = block_incl_scan_256<u64>(tg, scratch_g);
     const u64 ie = block_incl_scan_256<u64>(te, scratch_e);
-    if (warp == 7) {
-      const u64 ag = __shfl_sync(FULL, ig, 31), ae = __shfl_sync(FULL, ie, 31);
-      if (lane == 0) {
-        lb_publish_agg(a.lb_gt, tile, ag);
-        lb_publish_agg(a.lb_eq, tile, ae);
-      }
-      const u64 xg = lb_warp_prefix(a.lb_gt, tile);
-      const u64 xe = lb_warp_prefix(a.lb_eq, tile);
-      if (lane == 0) {
-        lb_publish_prefix(a.lb_gt, tile, xg + ag);
-        lb_publish_prefix(a.lb_eq, tile, xe + ae);
-        s_gx = xg;
-        s_ex = xe;
-        if (xe + ae >= a.k) atomicExch(&ctrl->ties_full, 1u);
-        if (tile == T - 1) {
-          const u64 G = xg + ag, E = xe + ae;
-          ctrl->res.pool_gt = G;
-          ctrl->res.pool_eq = min(E, a.k);
-          if (G >= a.k) {
-            ctrl->res.path = PATH_SELECT;
-            ctrl->res.k_out = a.k;
-          } else {
-            ctrl->res.path = PATH_MERGE;
-            ctrl->res.k_out = min(a.k, G + E);
-            ctrl->sort_lo = theta;
-            atomicMax(&ctrl->maxkey, theta);
-          }
-        }
-      }
+    if (tid == 255) {
+      a.tile_g[tile] = ig;
+      a.tile_e[tile] = ie;
     }
-    __syncthreads();
-    u64 gpos = s_gx + ig - tg, epos = s_ex + ie - te;
+  }
+  for (int o = 16; o; o >>= 1) st_concat += __shfl_xor_sync(FULL, st_concat, o);
+  if (lane == 0) s_cc[warp] = st_concat;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    ull t = 0;
+    for (int w = 0; w < 8; w++) t += s_cc[w];
+    if (t) atomicAdd((ull*)&ctrl->res.concatenated_len, t);
+    am_last = atomicAdd(&ctrl->k5_ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // exclusive prefixes of the tile counts (T <= S / K5_TILE), in place
+  const u64 per = (T + 255) / 256;
+  u64 sg = 0, se = 0;
+  for (u64 q = 0; q < per; q++) {
+    const u64 t = (u64)tid * per + q;
+    if (t < T) {
+      sg += __ldcg(&a.tile_g[t]);
+      se += __ldcg(&a.tile_e[t]);
+    }
+  }
+  const u64 xg = block_incl_scan_256<u64>(sg, scratch_g);
+  const u64 xe = block_incl_scan_256<u64>(se, scratch_e);
+  u64 rg = xg - sg, re = xe - se;
+  for (u64 q = 0; q < per; q++) {
+    const u64 t = (u64)tid * per + q;
+    if (t < T) {
+      const u64 g = __ldcg(&a.tile_g[t]), e = __ldcg(&a.tile_e[t]);
+      a.tile_g[t] = rg;
+      a.tile_e[t] = re;
+      rg += g;
+      re += e;
+    }
+  }
+  if (tid == 255) {
+    const u64 G = xg, E = xe;
+    const u32 theta = ctrl->res.theta;
+    ctrl->res.pool_gt = G;
+    ctrl->res.pool_eq = min(E, a.k);
+    if (G >= a.k) {
+      ctrl->res.path = PATH_SELECT;
+      ctrl->res.k_out = a.k;
+    } else {
+      ctrl->res.path = PATH_MERGE;
+      ctrl->res.k_out = min(a.k, G + E);
+      ctrl->sort_lo = theta;
+      atomicMax(&ctrl->maxkey, theta);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k5_emit(K5Args a) {
+  __shared__ u64 scratch_g[8], scratch_e[8];
+  const int tid = threadIdx.x;
+  Ctrl* ctrl = a.ctrl;
+  const u64 total = ctrl->sup_total;
+  const u64 T = max((u64)1, (total + K5_TILE - 1) / K5_TILE);
+  const u64 G = ctrl->res.pool_gt;
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    const u64 gx = a.tile_g[tile], ex = a.tile_e[tile];
+    const u64 gnext = tile + 1 < T ? a.tile_g[tile + 1] : G;
+    if (gnext == gx && ex >= a.k) continue;  // no key > theta and every tie beyond position k
+    uint4 rcs[K5_RPT];
+    u64 cg[K5_RPT], ce[K5_RPT], tg, te;
+    k5_tile_counts<true>(a, tile * K5_TILE + (u64)tid * K5_RPT, total, rcs, cg, ce, tg, te);
+    const u64 ig = block_incl_scan_256<u64>(tg, scratch_g);
+    const u64 ie = block_incl_scan_256<u64>(te, scratch_e);
+    u64 gpos = gx + ig - tg, epos = ex + ie - te;
 #pragma unroll
     for (int r = 0; r < K5_RPT; r++) {
       const uint4 rc = rcs[r];
       const u32 x = rc.w;
       const u32 cls = x & 7u;
-      const bool fq = (x >> 3) & 1u;
       const u64 sid = rc.x;
       const u64 base = sid << a.alpha;
       if (cls == CLS_A) {
@@ -680,7 +705,6 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
           a.d_pos[wslot] = epos;
           a.d_need[wslot] = (u32)min(ce[r], a.k - epos) | 0x80000000u;
         }
-        if (fq) st_concat += ce[r];
       } else if (cls == CLS_T) {
         if (epos < a.k && ce[r]) {
           const u32 wslot = atomicAdd(&ctrl->k6_count, 1u);
@@ -688,27 +712,15 @@ __global__ void __launch_bounds__(256) k5_assemble(K5Args a) {
           a.d_pos[wslot] = epos;
           a.d_need[wslot] = (u32)min(ce[r], a.k - epos);
         }
-        if (fq) st_concat += ce[r];
       } else if (cls == CLS_E) {
         // the staged keys of E candidates are copied in parallel by K5b
         const u64 eidx = x >> 4;
         a.e_gpos[eidx] = gpos;
         a.e_epos[eidx] = epos;
-        if (fq) st_concat += cg[r] + ce[r];
       }
       gpos += cg[r];
       epos += ce[r];
     }
-    (void)ppc;
-    __syncthreads();
-  }
-  for (int o = 16; o; o >>= 1) st_concat += __shfl_xor_sync(FULL, st_concat, o);
-  if (lane == 0) s_cc[warp] = st_concat;
-  __syncthreads();
-  if (tid == 0) {
-    ull t = 0;
-    for (int w = 0; w < 8; w++) t += s_cc[w];
-    if (t) atomicAdd((ull*)&ctrl->res.concatenated_len, t);
   }
 }
 
@@ -728,7 +740,10 @@ __global__ void __launch_bounds__(256) k5b_copy(Ctrl* ctrl, int alpha, u64 k, co
   const u64 nw = ((u64)gridDim.x * 256) >> 5;
   for (u64 sg = gw; sg < nE * ppc; sg += nw) {
     const u64 e = sg / ppc, part = sg - e * ppc;
-    u64 go = e_gpos[e], eo = e_epos[e];
+    // e_epos == ~0: k5_emit skipped this record's tile (no key > theta in it, every tie beyond k)
+    const u64 eo0 = e_epos[e];
+    if (eo0 == ~0ull) continue;
+    u64 go = e_gpos[e], eo = eo0;
     for (u64 p = 0; p < part; p++) {
       go += seg_gt[e * ppc + p];
       eo += seg_eq[e * ppc + p];

@@ -225,6 +225,27 @@ __device__ __forceinline__ u32 lanemask_lt() {
   return m;
 }
 
+// Warp-aggregated shared-memory histogram increment; all 32 lanes must call.
+__device__ __forceinline__ void hist_add_agg(u32* shist, u32 bin, bool pred) {
+  const u32 key = pred ? bin : 0xffffffffu;
+  const u32 peers = __match_any_sync(FULL, key);
+  if (pred && (u32)(__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&shist[bin], (u32)__popc(peers));
+}
+
+// Shared-memory histogram increment for mostly-uniform or mostly-identical
+// bins: one atomic when the whole warp hits one bin (tie-heavy inputs), plain
+// per-lane atomics otherwise.  All 32 lanes must call.
+__device__ __forceinline__ void hist_add_warp(u32* shist, u32 bin, bool pred) {
+  const u32 key = pred ? bin : 0xffffffffu;
+  int same = 0;
+  __match_all_sync(FULL, key, &same);
+  if (same) {
+    if (pred && (threadIdx.x & 31) == 0) atomicAdd(&shist[bin], 32u);
+  } else if (pred) {
+    atomicAdd(&shist[bin], 1u);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // top-beta ladders (registers, non-increasing, zero initialised: the
 // reference's _rows_ladder semantics, delegate.py:93-107)

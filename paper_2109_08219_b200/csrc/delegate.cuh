@@ -144,12 +144,6 @@ __device__ __forceinline__ void acc_shfl(Acc<B>& A, int off) {
 // unique whenever d_2 < d_1).
 __device__ __forceinline__ u32 pack_meta(bool constant, u32 p1) { return (constant ? 0x80000000u : 0u) | (p1 & 0x7fffffffu); }
 
-// Warp-aggregated shared-memory histogram increment; all 32 lanes must call.
-__device__ __forceinline__ void hist_add_agg(u32* shist, u32 bin, bool pred) {
-  const u32 key = pred ? bin : 0xffffffffu;
-  const u32 peers = __match_any_sync(FULL, key);
-  if (pred && (u32)(__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&shist[bin], (u32)__popc(peers));
-}
 
 template <int B>
 __device__ __forceinline__ void store_delegates(u32* D, u64 sid, const u32 (&L)[B]) {

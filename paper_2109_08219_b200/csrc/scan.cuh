@@ -420,11 +420,20 @@ __global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, SortBufs b, int 
 //                  and write the answer slice directly.
 // A bucket above BK_CAP (skewed keys) sends the sort to the LSD radix sort.
 // ---------------------------------------------------------------------------
+#ifndef DTOPK_BK_CHUNKS
+#define DTOPK_BK_CHUNKS 64
+#endif
+#ifndef DTOPK_BK_TARGET
+#define DTOPK_BK_TARGET 1024
+#endif
+#ifndef DTOPK_BK_SUB_BITS
+#define DTOPK_BK_SUB_BITS 11
+#endif
 constexpr int BK_MAX = 4096;      // buckets
-constexpr int BK_CHUNKS = 64;     // count / scatter CTAs
-constexpr int BK_TARGET = 1024;   // elements per bucket aimed for
+constexpr int BK_CHUNKS = DTOPK_BK_CHUNKS;    // count / scatter CTAs
+constexpr int BK_TARGET = DTOPK_BK_TARGET;    // elements per bucket aimed for
 constexpr int BK_CAP = 4096;      // largest bucket bucket_sort takes (16 per thread)
-constexpr int BK_SUB_BITS = 11;   // sub-bins of the in-bucket counting sort
+constexpr int BK_SUB_BITS = DTOPK_BK_SUB_BITS;  // sub-bins of the in-bucket counting sort
 constexpr int BK_SUB = 1 << BK_SUB_BITS;
 
 struct BucketBufs {

@@ -27,7 +27,7 @@ struct K2Args {
   // candidate superset (delegate path): subranges whose max delegate lies in
   // theta's top-11-bit bucket or above, in subrange order per warp segment
   int beta;
-  u32* sup_sid;  // [S]: segment (cta, warp) writes from sup_in[seg]
+  uint4* sup_sid;  // [S] {sid, d_1, d_2, d_beta} (beta 2; else {sid, d_1, 0, 0}): segment (cta, warp) from sup_in[seg]
   u32* sup_in;   // [g2 * 8] first slot of each segment
   u32* sup_cnt;  // [g2 * 8] entries of each segment
   u32* sup_off;  // [g2 * 8 + 1] exclusive prefix of sup_cnt (theta resolver)
@@ -165,7 +165,12 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
         u32 rr = BETA2 ? 0u : (u32)(i0 % beta);
 #pragma unroll
         for (int j = 0; j < 16; j++) {
-          if (i0 + j < whi && rr == 0 && v[j] >= kmin) a.sup_sid[o++] = (u32)((i0 + j) / beta);
+          if (i0 + j < whi && rr == 0 && v[j] >= kmin) {
+            const u32 sid = (u32)((i0 + j) / beta);
+            // beta 2: (d1, d2) sit in this lane's registers (pairs start at even j)
+            const u32 d2 = BETA2 ? v[j | 1] : 0u;
+            a.sup_sid[o++] = make_uint4(sid, v[j], d2, d2);
+          }
           rr = BETA2 ? (rr ^ 1u) : ((rr + 1 == (u32)beta) ? 0u : rr + 1);
         }
       }
@@ -175,14 +180,12 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
     u32 o = 0;
     if (lane == 31) o = atomicAdd(&s_cnt, incl);
     o = __shfl_sync(FULL, o, 31) + incl - nb;
-    if (nb) {
 #pragma unroll
-      for (int j = 0; j < 16; j++) {
-        if (i0 + j < whi && v[j] - kmin <= span) {
-          atomicAdd(&shist[(v[j] - kmin) >> 12], 1u);
-          region[o++] = v[j];
-        }
-      }
+    for (int j = 0; j < 16; j++) {
+      const bool mem = i0 + j < whi && v[j] - kmin <= span;
+      // warp-aggregated: tie-heavy inputs put whole warps on one bin
+      hist_add_warp(shist, (v[j] - kmin) >> 12, mem);
+      if (mem) region[o++] = v[j];
     }
   }
   if (sup && lane == 0) {
@@ -219,9 +222,15 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   for (u32 g = blockIdx.x; g < nregions; g += gridDim.x) {
     const u32 cnt = region_cnt[g];
     const u32* reg = selbuf + (u64)g * R;
-    for (u32 i = tid; i < cnt; i += 256) {
-      const u32 x = reg[i] - kmin;
-      if ((x >> 12) == b2) atomicAdd(&shist[x & 4095u], 1u);
+    for (u32 i0 = 0; i0 < cnt; i0 += 256 * 8) {  // 8 loads in flight per thread
+      u32 x[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const u32 i = i0 + u * 256 + tid;
+        x[u] = i < cnt ? reg[i] - kmin : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) hist_add_warp(shist, x[u] & 4095u, x[u] != 0xffffffffu && (x[u] >> 12) == b2);
     }
   }
   __syncthreads();
