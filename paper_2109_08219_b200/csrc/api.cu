@@ -72,7 +72,8 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.m_emit = direct ? n : L.cap_gt;
   L.words = (L.S + 31) / 32;
   // K2 regions: one contiguous range of D per CTA
-  const u64 g2 = std::max<u64>(1, std::min<u64>((u64)num_sms() * 4, (L.D_len + 4095) / 4096));
+  // <= 768 CTAs: the superset prefix holds K2_SEG_PER (24) segments per thread
+  const u64 g2 = std::max<u64>(1, std::min<u64>(std::min<u64>((u64)num_sms() * 4, 768), (L.D_len + 4095) / 4096));
   L.g2 = (u32)g2;
   L.R2 = ((L.D_len + g2 - 1) / g2 + 511) / 512 * 512;
   L.k4_tiles = (L.cap_e * W + K4_TILE - 1) / K4_TILE;

@@ -629,27 +629,41 @@ __global__ void __launch_bounds__(256) k5_count(K5Args a) {
   __syncthreads();
   if (!am_last) return;
   __threadfence();
-  // exclusive prefixes of the tile counts (T <= S / K5_TILE), in place
+  // exclusive prefixes of the tile counts (T <= S / K5_TILE), in place; blocks of
+  // 8 tiles per thread and step so the loads of a step are in flight together
   const u64 per = (T + 255) / 256;
   u64 sg = 0, se = 0;
-  for (u64 q = 0; q < per; q++) {
-    const u64 t = (u64)tid * per + q;
-    if (t < T) {
-      sg += __ldcg(&a.tile_g[t]);
-      se += __ldcg(&a.tile_e[t]);
+  for (u64 q0 = 0; q0 < per; q0 += 8) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const u64 t = (u64)tid * per + q0 + q;
+      if (q0 + q < per && t < T) {
+        sg += __ldcg(&a.tile_g[t]);
+        se += __ldcg(&a.tile_e[t]);
+      }
     }
   }
   const u64 xg = block_incl_scan_256<u64>(sg, scratch_g);
   const u64 xe = block_incl_scan_256<u64>(se, scratch_e);
   u64 rg = xg - sg, re = xe - se;
-  for (u64 q = 0; q < per; q++) {
-    const u64 t = (u64)tid * per + q;
-    if (t < T) {
-      const u64 g = __ldcg(&a.tile_g[t]), e = __ldcg(&a.tile_e[t]);
-      a.tile_g[t] = rg;
-      a.tile_e[t] = re;
-      rg += g;
-      re += e;
+  for (u64 q0 = 0; q0 < per; q0 += 8) {
+    u64 g[8], e[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const u64 t = (u64)tid * per + q0 + q;
+      const bool in = q0 + q < per && t < T;
+      g[q] = in ? __ldcg(&a.tile_g[t]) : 0;
+      e[q] = in ? __ldcg(&a.tile_e[t]) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const u64 t = (u64)tid * per + q0 + q;
+      if (q0 + q < per && t < T) {
+        a.tile_g[t] = rg;
+        a.tile_e[t] = re;
+      }
+      rg += g[q];
+      re += e[q];
     }
   }
   if (tid == 255) {

@@ -61,10 +61,11 @@ __device__ __forceinline__ u32 dig3(u32 k) { return k & 0x3ffu; }
 // range with probability 0.63).  The first digit is therefore log-scale in
 // the distance from the top, d = ~key: (leading zeros of d, next 6 bits of
 // d), 33 x 64 buckets ordered like the keys.  A bucket is a key interval
-// [kmin, kmin + 2^r) with r <= 25; digit 2 = (key - kmin) >> 12 (13 bits),
-// digit 3 = (key - kmin) & 4095.
+// [kmin, kmin + 2^r) with r <= 25; digit 2 = (key - kmin) >> 13 (12 bits),
+// digit 3 = (key - kmin) & 8191.
 constexpr int NBD1 = 2304;  // 2112 used, padded to a multiple of 256 (find_digit)
-constexpr int NBD2 = 8192, NBD3 = 4096;
+constexpr int NBD2 = 4096, NBD3 = 8192;
+constexpr int DSH3 = 13;  // digit 2 = (key - kmin) >> 13 (12 bits), digit 3 = low 13 bits
 __device__ __forceinline__ u32 ddig1(u32 key) {
   const u32 d = ~key;
   if (d == 0) return (32u << 6) | 63u;

@@ -45,6 +45,8 @@ __device__ __forceinline__ void warp_append(u32* buf, ull* counter, u32 x, bool 
   if (pred) buf[base + __popc(b & lanemask_lt())] = x;
 }
 
+constexpr int K2_SEG_PER = 24;  // superset segments per thread in the prefix (8 warps x <= 768 K2 CTAs)
+
 // Resolve theta from the digit-3 histogram (ctrl->selD.hist3) and publish the
 // exclusive prefix of the superset segment counts.  One CTA (256 threads).
 __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, const DigitResult& r2, u32 nregions,
@@ -53,7 +55,7 @@ __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, co
   const int tid = threadIdx.x;
   find_digit<NBD3>(ctrl->selD.hist3, r2.rem, r3, scratch);
   if (tid == 0) {
-    const u32 kth = kmin + (r2.digit << 12) + r3->digit;
+    const u32 kth = kmin + (r2.digit << DSH3) + r3->digit;
     ctrl->selD.r3 = *r3;
     ctrl->selD.kth = kth;
     ctrl->res.theta_local = kth;
@@ -61,22 +63,25 @@ __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, co
     ctrl->res.delegate_bucket = r1.cnt;
   }
   if (sup_cnt == nullptr) return;
+  // nseg = 8 * nregions <= 8 * 4 * SMs (api.cu): at most K2_SEG_PER per thread, all loads in flight
   const u32 nseg = nregions * 8;
   const u32 per = (nseg + 255) / 256;
+  u32 c[K2_SEG_PER];
   u32 sum = 0;
-  for (u32 q = 0; q < per; q++) {
+#pragma unroll
+  for (int q = 0; q < K2_SEG_PER; q++) {
     const u32 i = tid * per + q;
-    if (i < nseg) sum += __ldcg(&sup_cnt[i]);
+    c[q] = (q < (int)per && i < nseg) ? __ldcg(&sup_cnt[i]) : 0u;
+    sum += c[q];
   }
   u32* sc = reinterpret_cast<u32*>(scratch);
   const u32 incl = block_incl_scan_256<u32>(sum, sc);
   u32 run = incl - sum;
-  for (u32 q = 0; q < per; q++) {
+#pragma unroll
+  for (int q = 0; q < K2_SEG_PER; q++) {
     const u32 i = tid * per + q;
-    if (i < nseg) {
-      sup_off[i] = run;
-      run += __ldcg(&sup_cnt[i]);
-    }
+    if (q < (int)per && i < nseg) sup_off[i] = run;
+    run += c[q];
   }
   if (tid == 255) {
     sup_off[nseg] = incl;
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
     for (int j = 0; j < 16; j++) {
       const bool mem = i0 + j < whi && v[j] - kmin <= span;
       // warp-aggregated: tie-heavy inputs put whole warps on one bin
-      hist_add_warp(shist, (v[j] - kmin) >> 12, mem);
+      hist_add_warp(shist, (v[j] - kmin) >> DSH3, mem);
       if (mem) region[o++] = v[j];
     }
   }
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
         x[u] = i < cnt ? reg[i] - kmin : 0xffffffffu;
       }
 #pragma unroll
-      for (int u = 0; u < 8; u++) hist_add_warp(shist, x[u] & 4095u, x[u] != 0xffffffffu && (x[u] >> 12) == b2);
+      for (int u = 0; u < 8; u++) hist_add_warp(shist, x[u] & ((1u << DSH3) - 1u), x[u] != 0xffffffffu && (x[u] >> DSH3) == b2);
     }
   }
   __syncthreads();
