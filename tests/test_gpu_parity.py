@@ -329,3 +329,24 @@ def test_sharded_two_ranks_on_one_gpu(cuda):
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "tools/dist_check.py"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("dist,largest", [("uniform", True), ("normal_f32", False)])
+def test_tuning_sweep_gpu(dist, largest, cuda):
+    """Row f3: the sweep harness over an alpha grid and a beta grid, values
+    verified against a device sort at every point, reference CSV schema."""
+    import io
+
+    from paper_2109_08219_b200 import tuning
+
+    v = data.generate(dist, 1 << 20, seed=11, device=cuda)
+    base = dtopk.PipelineConfig(k=128, largest=largest)
+    rows = tuning.sweep(v, 128, alphas=[6, 8, 10], base=base, repeats=2)
+    assert [r.alpha for r in rows] == [6, 8, 10]
+    assert all(r.delegate_len == 2 * ((1 << 20) >> r.alpha) for r in rows)
+    assert all(r.total_ns > 0 for r in rows)
+    rows_b = tuning.sweep(v, 128, betas=[1, 2, 3], base=base)
+    assert [r.beta for r in rows_b] == [1, 2, 3]
+    buf = io.StringIO()
+    tuning.write_csv(rows + rows_b, buf)
+    assert len(buf.getvalue().splitlines()) == 7

@@ -183,3 +183,33 @@ def test_plan_arithmetic():
         dtopk.plan(2**20, 2**19, workers=8, max_resident=2**26)
     assert dtopk.shard_bounds(10, 3, 2) == (8, 2)
     assert sum(dtopk.shard_bounds(1_000_003, 7, r)[1] for r in range(7)) == 1_000_003
+
+
+def test_tuning_cost_model_and_csv_schema():
+    """Row f3 mirror: the reference cost model (tuning.py:61-71), its convex
+    argmin near Eq. 11, and the sweep CSV schema (tuning.py:33-36, 189-201)."""
+    import io
+    import math
+
+    from paper_2109_08219_b200 import tuning
+
+    n, k = 1 << 20, 128
+    c = tuning.model_cost(8, k, n)
+    inv, size = 2.0 ** -8, 2.0 ** 8
+    assert c.t_delegate == (1 + inv) * n + 31 * n * inv
+    assert c.t_firstk == 5 * n * inv + 2 * k
+    assert c.t_concat == k + 2 * k * size
+    assert c.t_secondk == 4 * k * size
+    assert c.total == c.t_delegate + c.t_firstk + c.t_concat + c.t_secondk
+    totals = {a: tuning.model_cost(a, k, n).total for a in range(1, 20)}
+    best = min(totals, key=totals.get)
+    assert abs(best - 0.5 * (math.log2(n) - math.log2(k) + 2.62)) <= 1.0
+    with pytest.raises(ValueError):
+        tuning.CostModelParams(c_global=0)
+    row = tuning.SweepRow(8, 2, 128, n, 1, 2, 3, 4, 10, 8192, 2)
+    buf = io.StringIO()
+    tuning.write_csv([row], buf)
+    assert buf.getvalue() == tuning.CSV_HEADER + "\n8,2,128,1048576,1,2,3,4,10,8192,2\n"
+    assert tuning.CSV_HEADER.split(",")[0] == "alpha" and len(tuning.CSV_HEADER.split(",")) == 11
+    # b200_const inverts Eq. 11 for exact optima
+    assert abs(tuning.b200_const({(1 << 30, 1024): 11}) - (2 * 11.5 - 30 + 10)) < 1e-9
