@@ -213,3 +213,36 @@ def test_tuning_cost_model_and_csv_schema():
     assert tuning.CSV_HEADER.split(",")[0] == "alpha" and len(tuning.CSV_HEADER.split(",")) == 11
     # b200_const inverts Eq. 11 for exact optima
     assert abs(tuning.b200_const({(1 << 30, 1024): 11}) - (2 * 11.5 - 30 + 10)) < 1e-9
+
+
+def test_reference_generators_and_vector_file(tmp_path):
+    """Rows a11 / f1: the reference's ud / nd / cd generators and the DTKV file
+    format, against vectors and file bytes the unmodified reference produced
+    (tests/golden/make_gen_golden.py)."""
+    import os
+
+    from paper_2109_08219_b200 import data
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "gen_golden.npz"))
+    np.testing.assert_array_equal(data.generate("ud", 4096, 7), g["ud_4096_7"])
+    np.testing.assert_array_equal(data.generate("nd", 4096, 7), g["nd_4096_7"])
+    np.testing.assert_array_equal(data.generate("cd", 16384, 3, k=100), g["cd_16384_3"])
+    p = tmp_path / "v.dtkv"
+    data.write_vector(p, g["ud_4096_7"][:333])
+    assert p.read_bytes() == g["dtkv_bytes"].tobytes()
+    assert data.read_header(p) == 333
+    np.testing.assert_array_equal(data.read_vector(p, offset=5, count=100), g["ud_4096_7"][5:105])
+    buf = np.empty(50, dtype=np.uint32)
+    data.read_vector(p, offset=300, count=33, out=buf)
+    np.testing.assert_array_equal(buf[:33], g["ud_4096_7"][300:333])
+    bad = tmp_path / "bad.dtkv"
+    bad.write_bytes(b"XXXX" + p.read_bytes()[4:])
+    with pytest.raises(data.BadMagic):
+        data.read_header(bad)
+    bad.write_bytes(p.read_bytes()[:-4])
+    with pytest.raises(data.TruncatedFile):
+        data.read_header(bad)
+    with pytest.raises(data.InfeasibleN):
+        data.gen_customized(100, 1, 0)
+    with pytest.raises(ValueError):
+        data.read_vector(p, offset=300, count=100)
