@@ -27,7 +27,17 @@ from .core import (
     validate_config,
 )
 from .delegate import DelegateVector, extract_delegates, extract_delegates_blocked
-from .distributed import PartitionPlan, ShardedTopK, WorkerFailed, plan, shard_bounds, sharded_topk
+from .distributed import (
+    DistributedReport,
+    GatherMessage,
+    PartitionPlan,
+    ShardedTopK,
+    WorkerFailed,
+    plan,
+    run_distributed,
+    shard_bounds,
+    sharded_topk,
+)
 from .kernels import KeyedEntry, kth_largest, radix_topk
 from .pipeline import DrTopK, QualificationReport, concatenate_filtered, dr_topk, first_topk
 from .tuning import auto_alpha
@@ -45,7 +55,10 @@ __all__ = [
     "InvalidBeta",
     "InvalidK",
     "KeyedEntry",
+    "DistributedReport",
+    "GatherMessage",
     "PartitionPlan",
+    "run_distributed",
     "ShardedTopK",
     "PipelineConfig",
     "QualificationReport",

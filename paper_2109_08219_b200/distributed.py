@@ -26,8 +26,12 @@ is exercised by world-size-2 ``gloo`` tests on CPU; the product uses
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, replace
+import queue
+import threading
+import time
+from dataclasses import dataclass, field, replace
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -325,3 +329,170 @@ def _dev_of(x):
 def _as_gatherable(ts):
     # NCCL/gloo lack uint32 all_gather: move the bits as int32
     return [t.view(torch.int32) if t.dtype == torch.uint32 else t for t in ts]
+
+
+# ---------------------------------------------------------------------------
+# Partitioned run on one GPU with streamed partitions (reference:
+# distributed.run_distributed, distributed.py:140-251)
+# ---------------------------------------------------------------------------
+@dataclass
+class GatherMessage:
+    """One worker's contribution (distributed.py:63-75): its local top-k
+    (device tensors, values best first plus global indices) and lane timings."""
+
+    worker_id: int
+    local_topk: torch.Tensor
+    local_indices: torch.Tensor
+    compute_nanos: int
+    reload_nanos: int
+    sent_at_nanos: int = 0
+
+    def payload_bytes(self) -> int:
+        return (self.local_topk.element_size() + 8) * int(self.local_topk.numel())
+
+
+@dataclass
+class DistributedReport:
+    result: TopKResult
+    messages: list
+    received_at_nanos: list
+    gathered_bytes: int
+    total_nanos: int
+    reloaded_partitions: int = 0
+    extra: dict = field(default_factory=dict)
+
+    def communication_nanos(self, worker_id: int) -> int:
+        msg = self.messages[worker_id]
+        return max(0, self.received_at_nanos[worker_id] - msg.sent_at_nanos)
+
+
+def _merge_by_index(values: torch.Tensor, indices: torch.Tensor, k: int, largest: bool):
+    """Exact top-k of (value, global index) pairs under (value best first,
+    index ascending): order the pairs by index, then the device top-k's
+    position tie-break is the index tie-break."""
+    from .pipeline import dr_topk
+
+    order = torch.argsort(indices)
+    # torch has no uint32 gather on CUDA: move the bits as int32
+    bits = values.view(torch.int32) if values.dtype == torch.uint32 else values
+    v, i = bits[order], indices[order]
+    if values.dtype == torch.uint32:
+        v = v.view(torch.uint32)
+    r = dr_topk(v, PipelineConfig(k=min(k, v.numel()), alpha=0, auto_alpha=False, largest=largest))
+    return r.values, i[r.indices]
+
+
+def _worker_lane(worker_id, source, parts, plan_, k, cfg, device, outbox):
+    from ._device import to_device
+    from .data import read_vector
+    from .pipeline import dr_topk
+
+    try:
+        torch.cuda.set_device(device)
+        stream = torch.cuda.Stream(device)
+        with torch.cuda.stream(stream):
+            is_file = not isinstance(source, (np.ndarray, torch.Tensor))
+            stage = None
+            if is_file:
+                cap = max(plan_.partitions[i].length for i in parts) if parts else 1
+                stage = torch.empty(cap, dtype=torch.uint32, pin_memory=True)
+
+            def load(part):
+                if not is_file:
+                    chunk = source[part.offset:part.offset + part.length]
+                    return to_device(chunk, device).keys if not isinstance(chunk, torch.Tensor) or not chunk.is_cuda \
+                        else chunk
+                host = read_vector(source, offset=part.offset, count=part.length,
+                                   out=stage.numpy()[: part.length])
+                del host
+                dev = torch.empty(part.length, dtype=torch.uint32, device=device)
+                dev.copy_(stage[: part.length], non_blocking=True)
+                stream.synchronize()
+                return dev
+
+            resident = {i: load(plan_.partitions[i]) for i in parts if plan_.partitions[i].resident}
+            reload_nanos, vals, idxs = 0, [], []
+            t_compute = time.perf_counter_ns()
+            for i in parts:
+                part = plan_.partitions[i]
+                if i in resident:
+                    chunk = resident.pop(i)
+                else:  # a partition beyond the residency cap: streamed from the file (reload overhead)
+                    t0 = time.perf_counter_ns()
+                    chunk = load(part)
+                    reload_nanos += time.perf_counter_ns() - t0
+                r = dr_topk(chunk, replace(cfg, k=min(k, part.length)))
+                vals.append(r.values)
+                idxs.append(r.indices + part.offset)
+                del chunk
+            if vals:
+                v, ix = torch.cat(vals), torch.cat(idxs)
+                if len(vals) > 1:
+                    v, ix = _merge_by_index(v, ix, k, cfg.largest)
+            else:  # more workers than partitions: this lane owns nothing
+                v = torch.empty(0, dtype=torch.uint32, device=device)
+                ix = torch.empty(0, dtype=torch.int64, device=device)
+            stream.synchronize()
+            compute_nanos = time.perf_counter_ns() - t_compute - reload_nanos
+        msg = GatherMessage(worker_id, v, ix, compute_nanos, reload_nanos)
+        msg.sent_at_nanos = time.perf_counter_ns()
+        outbox.put((worker_id, msg, None))
+    except BaseException as exc:  # surfaced as WorkerFailed by the coordinator
+        outbox.put((worker_id, None, exc))
+
+
+def run_distributed(source, k: int, cfg: PipelineConfig | None = None, workers: int = 1, *,
+                    max_resident: int = DEFAULT_MAX_RESIDENT, device=None) -> DistributedReport:
+    """Partitioned top-k with gather-to-primary aggregation on the GPU.
+
+    ``source``: a numpy / torch vector or a DTKV file path.  The partition
+    plan is the reference's (``plan``); worker lanes are threads with their
+    own CUDA streams.  Partitions beyond a worker's first are streamed from
+    the file (pinned staging, H2D) when the residency cap forces it -- the
+    out-of-HBM path -- and their read time is reported as reload overhead.
+    Every lane sends its local top-k with global indices; the coordinator
+    merges them exactly (value best first, lowest index on ties).
+    """
+    from ._device import to_caller
+    from .data import read_header
+
+    start = time.perf_counter_ns()
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if isinstance(source, (str, bytes)) or hasattr(source, "__fspath__"):
+        n, kind = read_header(source), "numpy"
+    elif isinstance(source, torch.Tensor):
+        n, kind = int(source.numel()), ("torch_cuda" if source.is_cuda else "torch_cpu")
+    else:
+        source = np.ascontiguousarray(np.asarray(source)).ravel()
+        if source.dtype != np.float32:
+            source = source.astype(np.uint32)
+        n, kind = source.size, "numpy"
+    cfg = cfg if cfg is not None else PipelineConfig(k=k)
+    plan_ = plan(n, k, workers, max_resident)
+    outbox: queue.Queue = queue.Queue()
+    lanes = [threading.Thread(target=_worker_lane, args=(w, source, plan_.assignments[w], plan_, k, cfg, device,
+                                                         outbox), name=f"dtopk-worker-{w}", daemon=True)
+             for w in range(workers)]
+    for t in lanes:
+        t.start()
+    messages, received, failure = [None] * workers, [0] * workers, None
+    for _ in range(workers):
+        wid, msg, exc = outbox.get()
+        received[wid] = time.perf_counter_ns()
+        if exc is not None and failure is None:
+            failure = (wid, exc)
+        messages[wid] = msg
+    for t in lanes:
+        t.join()
+    if failure is not None:
+        raise WorkerFailed(f"worker {failure[0]} failed: {failure[1]!r}") from failure[1]
+    v = torch.cat([m.local_topk.to(device) for m in messages])
+    ix = torch.cat([m.local_indices.to(device) for m in messages])
+    fv, fi = _merge_by_index(v, ix, k, cfg.largest)
+    torch.cuda.synchronize(device)
+    stats = WorkloadStats()
+    res = TopKResult(values=to_caller(fv, kind), threshold=to_caller(fv[-1:], "numpy")[0].item(), stats=stats, indices=to_caller(fi, kind))
+    reloaded = sum(1 for w, ps in plan_.assignments.items() for i in ps if not plan_.partitions[i].resident)
+    return DistributedReport(result=res, messages=messages, received_at_nanos=received,
+                             gathered_bytes=sum(m.payload_bytes() for m in messages),
+                             total_nanos=time.perf_counter_ns() - start, reloaded_partitions=reloaded)

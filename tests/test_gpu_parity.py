@@ -350,3 +350,50 @@ def test_tuning_sweep_gpu(dist, largest, cuda):
     buf = io.StringIO()
     tuning.write_csv(rows + rows_b, buf)
     assert len(buf.getvalue().splitlines()) == 7
+
+
+@pytest.mark.parametrize("workers,max_resident", [(1, 1 << 26), (3, 1 << 26), (2, 100_000), (4, 65_536)])
+def test_run_distributed_streams_partitions(workers, max_resident, oracle_mod, cuda, tmp_path):
+    """Rows f1/f2: the partitioned run (reference plan, worker lanes, gather to
+    primary); a residency cap below the share streams partitions from the
+    DTKV file.  Values and indices against the oracle."""
+    n, k = 600_007, 3000
+    v = data.gen_uniform(n, 9)
+    path = tmp_path / "v.dtkv"
+    data.write_vector(path, v)
+    rep = dtopk.run_distributed(path, k, workers=workers, max_resident=max_resident)
+    ek, ei = oracle_mod.topk_with_indices(v, k)
+    np.testing.assert_array_equal(rep.result.values, ek)
+    np.testing.assert_array_equal(rep.result.indices, ei)
+    plan = dtopk.plan(n, k, workers, max_resident)
+    assert rep.reloaded_partitions == sum(1 for p in plan.partitions if not p.resident)
+    assert len(rep.messages) == workers and rep.gathered_bytes > 0
+    if rep.reloaded_partitions:
+        assert sum(m.reload_nanos for m in rep.messages) > 0
+    # in-memory source, ties (nd): same answer
+    nd = data.gen_normal(200_000, 2)
+    rep2 = dtopk.run_distributed(nd, 5000, workers=3, max_resident=30_000)
+    ek2, ei2 = oracle_mod.topk_with_indices(nd, 5000)
+    np.testing.assert_array_equal(rep2.result.values, ek2)
+    np.testing.assert_array_equal(rep2.result.indices, ei2)
+
+
+def test_cli_gen_run_sweep_dist(cuda, tmp_path, capsys):
+    """Row f2: the reference CLI's subcommands and CSV schemas on the GPU path."""
+    from paper_2109_08219_b200 import cli, tuning
+
+    f = str(tmp_path / "v.dtkv")
+    assert cli.main(["gen", "--dist", "cd", "--n", "2^16", "--k", "100", "--out", f]) == 0
+    assert cli.main(["run", f, "--k", "100", "--verify", "--csv", str(tmp_path / "r.csv")]) == 0
+    out = capsys.readouterr().out
+    assert "verified=true" in out and "ratio_sum=" in out
+    assert (tmp_path / "r.csv").read_text().splitlines()[0] == tuning.CSV_HEADER
+    assert cli.main(["run", "--dist", "nd", "--n", "2^18", "--k", "2^10", "--verify"]) == 0
+    assert cli.main(["sweep", f, "--k", "100", "--param", "alpha", "--grid", "4,6,8",
+                     "--csv", str(tmp_path / "s.csv")]) == 0
+    assert len((tmp_path / "s.csv").read_text().splitlines()) == 4
+    assert cli.main(["dist", f, "--k", "100", "--workers", "3", "--max-resident", "2^13", "--verify",
+                     "--csv", str(tmp_path / "d.csv")]) == 0
+    lines = (tmp_path / "d.csv").read_text().splitlines()
+    assert lines[0] == cli.DIST_CSV_HEADER and len(lines) == 4
+    assert cli.main(["run", f, "--k", "0"]) == 2  # InvalidK -> exit 2 (cli.py:270-275)

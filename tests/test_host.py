@@ -246,3 +246,18 @@ def test_reference_generators_and_vector_file(tmp_path):
         data.gen_customized(100, 1, 0)
     with pytest.raises(ValueError):
         data.read_vector(p, offset=300, count=100)
+
+
+def test_cli_parser_and_counts():
+    """Row f2 host side: count notation and the reference's subcommand set."""
+    from paper_2109_08219_b200 import cli
+
+    assert cli.parse_count("2^24") == 1 << 24 and cli.parse_count(" 77 ") == 77
+    assert cli.parse_grid("2^4,5, 6") == [16, 5, 6]
+    p = cli.build_parser()
+    a = p.parse_args(["sweep", "--dist", "ud", "--n", "2^20", "--k", "128", "--param", "beta", "--grid", "1,2,3"])
+    assert a.command == "sweep" and a.param == "beta" and a.const == 3.0 and a.backend == "radix"
+    a = p.parse_args(["dist", "x.dtkv", "--k", "10", "--workers", "4"])
+    assert a.max_resident == str(1 << 26)
+    with pytest.raises(SystemExit):
+        p.parse_args(["run", "--k", "1", "--backend", "heap"])
