@@ -239,7 +239,7 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
     k2_scan_delegates<0><<<L.g2, 256, 0, s>>>(k2);
   counted();
   k2_pass3<<<grid_for(L.g2, nsm), 256, 0, s>>>(ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
-                                                    reinterpret_cast<u32*>(ws + L.sup_off));
+                                                    reinterpret_cast<u32*>(ws + L.sup_off), D, L.D_len);
   counted();
   rec(ev, 2, s);
 }

@@ -896,28 +896,28 @@ __device__ __forceinline__ void finish_small_r(Ctrl* ctrl, u64 m, u64 ko, u64 G,
 // only the bits d can occupy, with the pool position as the value.  The input
 // is in position order, so stability yields (key desc, position asc).
 // Padding slots (>= m) carry the largest d and come last by stability.
-template <int MODE>
+template <int MODE, int ITEMS>
 __device__ __forceinline__ void finish_small_radix(Ctrl* ctrl, u64 m, u64 ko, u64 G, u32 theta, u32 hi,
                                                    const u32* __restrict__ gt_keys, const u64* __restrict__ gt_idx,
                                                    const u64* __restrict__ ties, u32* __restrict__ ov,
                                                    long long* __restrict__ oi, long long offset, void* smem) {
-  typedef cub::BlockRadixSort<u32, 1024, 8, u32> Sorter;
+  typedef cub::BlockRadixSort<u32, 1024, ITEMS, u32> Sorter;
   static_assert(sizeof(typename Sorter::TempStorage) <= SMALL_POOL * 8, "finish_small shared memory");
   const u32 range = hi - theta;
   const int nbits = range ? 32 - __clz(range) : 0;
   const u32 pad = nbits >= 32 ? 0xffffffffu : ((1u << nbits) - 1u);
-  u32 d[8], pos[8];
+  u32 d[ITEMS], pos[ITEMS];
 #pragma unroll
-  for (int j = 0; j < 8; j++) {
-    const u32 i = threadIdx.x * 8u + (u32)j;
+  for (int j = 0; j < ITEMS; j++) {
+    const u32 i = threadIdx.x * (u32)ITEMS + (u32)j;
     pos[j] = i;
     d[j] = pad;
     if (i < m) d[j] = hi - (i < G ? gt_keys[i] : theta);
   }
   if (nbits) Sorter(*reinterpret_cast<typename Sorter::TempStorage*>(smem)).Sort(d, pos, 0, nbits);
 #pragma unroll
-  for (int j = 0; j < 8; j++) {
-    const u32 r = threadIdx.x * 8u + (u32)j;
+  for (int j = 0; j < ITEMS; j++) {
+    const u32 r = threadIdx.x * (u32)ITEMS + (u32)j;
     if (r < ko) {
       const u32 key = hi - d[j];
       ov[r] = from_key<MODE>(key);
@@ -948,12 +948,14 @@ __global__ void __launch_bounds__(1024) finish_small(Ctrl* ctrl, const u32* __re
   const u64 ko = ctrl->res.k_out;
   const u32 theta = ctrl->res.theta;
   const u32 hi = max(ctrl->maxkey, theta);
-  if (m <= 1024)
+  // tiny pools: register/shuffle bitonic; larger: CUB block radix sort over the occupied bits only
+  // (the pool of a large-n top-k spans few bits, e.g. ~12 for n = 2^30, k = 1024)
+  if (m <= 64)
     finish_small_r<MODE, 1>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   else if (m <= 2048)
-    finish_small_r<MODE, 2>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+    finish_small_radix<MODE, 2>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   else
-    finish_small_radix<MODE>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+    finish_small_radix<MODE, 8>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   if (threadIdx.x == 0) ctrl->small_done = 1;
 }
 

@@ -123,6 +123,9 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
   const u64 out0 = (wlo + beta - 1) / beta;  // first subrange whose d_1 lies in [wlo, whi)
   u32* region = a.selbuf + lo;
   const bool sup = a.sup_sid != nullptr;
+  // a bucket holding a large share of D (tie-heavy or narrow-range inputs): do
+  // not copy it into the regions; pass 3 scans D itself (same bytes, no writes)
+  const bool compact = r1.cnt * 4 <= a.nD;
   u32 run = 0;
   for (u64 base = wlo; base < whi; base += 512) {
     const u64 i0 = base + (u64)lane * 16;
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
       const bool mem = i0 + j < whi && v[j] - kmin <= span;
       // warp-aggregated: tie-heavy inputs put whole warps on one bin
       hist_add_warp(shist, (v[j] - kmin) >> DSH3, mem);
-      if (mem) region[o++] = v[j];
+      if (mem && compact) region[o++] = v[j];
     }
   }
   if (sup && lane == 0) {
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
   }
   __syncthreads();
   Ctrl* ctrl = a.ctrl;
-  if (tid == 0) a.region_cnt[blockIdx.x] = s_cnt;
+  if (tid == 0) a.region_cnt[blockIdx.x] = compact ? s_cnt : 0u;
   for (int i = tid; i < NBD2; i += 256) {
     const u32 c = shist[i];
     if (c) atomicAdd(&ctrl->selD.hist2[i], (ull)c);
@@ -210,7 +213,8 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
 // the last CTA resolves theta and the superset record offsets.
 __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
                                                 const u32* __restrict__ region_cnt, u32 nregions, u64 R,
-                                                const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off) {
+                                                const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off,
+                                                const u32* __restrict__ D, u64 nD) {
   __shared__ u32 shist[NBD3];
   __shared__ DigitResult r3;
   __shared__ ull scratch[8];
@@ -224,6 +228,31 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   find_digit<NBD2>(ctrl->selD.hist2, r1.rem, &r2, scratch);
   if (blockIdx.x == 0 && tid == 0) ctrl->selD.r2 = r2;
   const u32 b2 = r2.digit;
+  if (r1.cnt * 4 > nD) {
+    // K2 did not compact this (large) bucket: scan D, four uint4 per thread and step
+    const u32 span = kmax - kmin;
+    const u64 nq = nD / 4;
+    for (u64 q0 = (u64)blockIdx.x * 1024; q0 < nq; q0 += (u64)gridDim.x * 1024) {
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const u64 q = q0 + u * 256 + tid;
+        x[u] = q < nq ? ld_nc_v4(D + 4 * q) : make_uint4(kmin - 1, kmin - 1, kmin - 1, kmin - 1);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const u32 e[4] = {x[u].x - kmin, x[u].y - kmin, x[u].z - kmin, x[u].w - kmin};
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+          hist_add_warp(shist, e[c] & ((1u << DSH3) - 1u), e[c] <= span && (e[c] >> DSH3) == b2);
+      }
+    }
+    if (blockIdx.x == 0) {  // tail of nD % 4 delegates
+      const u64 i = nq * 4 + tid;
+      const u32 e = i < nD ? D[i] - kmin : 0xffffffffu;
+      if (tid < 32) hist_add_warp(shist, e & ((1u << DSH3) - 1u), e <= span && (e >> DSH3) == b2);
+    }
+  }
   for (u32 g = blockIdx.x; g < nregions; g += gridDim.x) {
     const u32 cnt = region_cnt[g];
     const u32* reg = selbuf + (u64)g * R;
