@@ -145,6 +145,24 @@ int num_sms() {
   return cache[dev];
 }
 
+// Launch with programmatic stream serialization (PDL, see common.cuh): the
+// kernel's CTAs may be scheduled while its predecessor in the stream runs;
+// the kernel itself waits (griddepcontrol.wait) before touching its inputs.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline int grid_for(u64 work_items, int cap) {
   if (work_items == 0) return 1;
   return (int)std::max<u64>(1, std::min<u64>(work_items, (u64)cap));
@@ -234,11 +252,11 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
             reinterpret_cast<u32*>(ws + L.sup_cnt),
             reinterpret_cast<u32*>(ws + L.sup_off)};
   if (beta == 2)
-    k2_scan_delegates<1><<<L.g2, 256, 0, s>>>(k2);
+    launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
   else
-    k2_scan_delegates<0><<<L.g2, 256, 0, s>>>(k2);
+    launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, s, k2);
   counted();
-  k2_pass3<<<grid_for(L.g2, nsm), 256, 0, s>>>(ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
+  launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
                                                     reinterpret_cast<u32*>(ws + L.sup_off), D, L.D_len);
   counted();
   rec(ev, 2, s);
@@ -447,17 +465,17 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
             t_cnt,
             L.cap_e,
             reinterpret_cast<u64*>(ws + L.e_epos)};
-  k3_classify<<<grid_for((nseg + 7) / 8, nsm * 8), 256, 0, s>>>(k3);
+  launch_pdl(k3_classify, dim3(grid_for((nseg + 7) / 8, nsm * 8)), dim3(256), 0, s, k3);
   counted();
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
             reinterpret_cast<u64*>(ws + L.stg_idx), reinterpret_cast<u32*>(ws + L.seg_gt),
             reinterpret_cast<u32*>(ws + L.seg_eq), L.cap_e};
-  k4_read<MODE><<<grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4), 256, 0, s>>>(k4);
+  launch_pdl(k4_read<MODE>, dim3(grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4)), dim3(256), 0, s, k4);
   counted();
   const int exact = (flags & DTOPK_FLAG_EXACT_STATS) ? 1 : 0;
   K4TArgs k4t{keys, n,  L.S,   alpha, k, ctrl, t_sid, t_cnt, rc.r, reinterpret_cast<const u32*>(ws + L.seg_eq),
               exact};
-  k4t_count<MODE><<<grid_for((L.S + 7) / 8, nsm * 4), 256, 0, s>>>(k4t);
+  launch_pdl(k4t_count<MODE>, dim3(grid_for((L.S + 7) / 8, nsm * 4)), dim3(256), 0, s, k4t);
   counted();
   K5Args k5{ctrl,
             rc,
@@ -480,15 +498,15 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
             reinterpret_cast<u64*>(ws + L.k5_tg),
             reinterpret_cast<u64*>(ws + L.k5_te),
             exact};
-  k5_count<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
+  launch_pdl(k5_count, dim3(grid_for(L.k5_tiles, nsm * 4)), dim3(256), 0, s, k5);
   counted();
-  k5_emit<<<grid_for(L.k5_tiles, nsm * 4), 256, 0, s>>>(k5);
+  launch_pdl(k5_emit, dim3(grid_for(L.k5_tiles, nsm * 4)), dim3(256), 0, s, k5);
   counted();
-  k5b_copy<<<grid_for((L.nseg + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, alpha, k, k5.stg_key, k5.stg_idx, k5.seg_gt,
+  launch_pdl(k5b_copy, dim3(grid_for((L.nseg + 7) / 8, nsm * 4)), dim3(256), 0, s, ctrl, alpha, k, k5.stg_key, k5.stg_idx, k5.seg_gt,
                                                                k5.seg_eq, k5.e_gpos, k5.e_epos, L.cap_e,
                                                                k5.gt_keys, k5.gt_idx, k5.ties);
   counted();
-  k6_ties<MODE><<<grid_for((L.cap_d + 7) / 8, nsm * 4), 256, 0, s>>>(ctrl, keys, n, alpha, k5.d_sid, k5.d_pos,
+  launch_pdl(k6_ties<MODE>, dim3(grid_for((L.cap_d + 7) / 8, nsm * 4)), dim3(256), 0, s, ctrl, keys, n, alpha, k5.d_sid, k5.d_pos,
                                                                       k5.d_need, k5.ties);
   counted();
   rec(ev, 3, s);
@@ -499,7 +517,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   }
   const bool need_tail = std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL;  // pools beyond SMALL_POOL possible
   const bool cond = gc && need_tail;
-  finish_small<MODE><<<1, 1024, SMALL_POOL * 8, s>>>(ctrl, k5.gt_keys, k5.gt_idx, k5.ties,
+  launch_pdl(finish_small<MODE>, dim3(1), dim3(1024), SMALL_POOL * 8, s, ctrl, k5.gt_keys, k5.gt_idx, k5.ties,
                                                      reinterpret_cast<u32*>(out_values),
                                                      reinterpret_cast<long long*>(out_indices), (long long)offset,
                                                      cond ? gc->cond : cudaGraphConditionalHandle{}, cond ? 1 : 0);

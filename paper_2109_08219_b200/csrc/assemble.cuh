@@ -94,6 +94,8 @@ __device__ __forceinline__ u32 classify(u32 d1, u32 d2, u32 m, u32 theta, int be
 // record array keeps the superset's subrange order without a second
 // compaction; D and meta are gathered only for superset entries.
 __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ ull s_stat[4][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
@@ -226,6 +228,8 @@ struct K4Args {
 // from a tile-wide exclusive scan minus the scan value at the segment start.
 template <int MODE>
 __global__ void __launch_bounds__(256) k4_read(K4Args a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ u32 s_wg[8], s_we[8];
   __shared__ u32 s_seg_g[K4_TILE / 4], s_seg_e[K4_TILE / 4];
   __shared__ u32 s_max[8];
@@ -447,6 +451,8 @@ struct K4TArgs {
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ u64 s_chunk;
   __shared__ u32 s_eq[8];
   Ctrl* ctrl = a.ctrl;
@@ -592,6 +598,8 @@ __device__ __forceinline__ void k5_tile_counts(const K5Args& a, u64 i0, u64 tota
 }
 
 __global__ void __launch_bounds__(256) k5_count(K5Args a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ u64 scratch_g[8], scratch_e[8];
   __shared__ ull s_cc[8];
   __shared__ int am_last;
@@ -684,6 +692,8 @@ __global__ void __launch_bounds__(256) k5_count(K5Args a) {
 }
 
 __global__ void __launch_bounds__(256) k5_emit(K5Args a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ u64 scratch_g[8], scratch_e[8];
   const int tid = threadIdx.x;
   Ctrl* ctrl = a.ctrl;
@@ -745,6 +755,8 @@ __global__ void __launch_bounds__(256) k5b_copy(Ctrl* ctrl, int alpha, u64 k, co
                                                 const u32* __restrict__ seg_eq, const u64* __restrict__ e_gpos,
                                                 const u64* __restrict__ e_epos, u64 cap_e, u32* __restrict__ gt_keys,
                                                 u64* __restrict__ gt_idx, u64* __restrict__ ties) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const u64 nE = min((u64)ctrl->nE, cap_e);
   const int lseg = alpha < 13 ? alpha : 13;
@@ -778,6 +790,8 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k6_ties(Ctrl* ctrl, const u32* __restrict__ keys, u64 n, int alpha,
                                                const u32* __restrict__ d_sid, const u64* __restrict__ d_pos,
                                                const u32* __restrict__ d_need, u64* __restrict__ ties) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const u32 theta = ctrl->res.theta;
   const u32 cnt = ctrl->k6_count;
@@ -939,6 +953,8 @@ __global__ void __launch_bounds__(1024) finish_small(Ctrl* ctrl, const u32* __re
                                                      u32* __restrict__ ov, long long* __restrict__ oi,
                                                      long long offset, cudaGraphConditionalHandle cond,
                                                      int use_cond) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ unsigned long long sk[];
   const u32 path = ctrl->res.path;
   const u64 G = ctrl->res.pool_gt;

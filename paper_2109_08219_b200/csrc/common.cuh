@@ -220,6 +220,14 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
+// Programmatic dependent launch (PDL): the post-K1 chain is launched with
+// programmatic stream serialization, so each kernel's CTAs are scheduled while
+// its predecessor still runs and block here until the predecessor's grid has
+// completed and its writes are visible.  pdl_trigger lets the next kernel in
+// the chain be scheduled as soon as every CTA of this one has started.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ u32 lanemask_lt() {
   u32 m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -353,6 +353,7 @@ __device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stag
 
 template <int MODE, int B>
 __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
+  pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   u32* stages = reinterpret_cast<u32*>(smem_raw);
   u64* full = reinterpret_cast<u64*>(smem_raw + (size_t)K1_STAGES * K1_CHUNK * 4);
@@ -432,6 +433,7 @@ template <int B>
 __global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial, const u32* __restrict__ pmeta,
                                                 u64 nch, int alpha, u64 S, u32* __restrict__ D,
                                                 u32* __restrict__ meta, ull* __restrict__ hist1) {
+  pdl_trigger();
   __shared__ u32 shist[NBD1];
   for (int i = threadIdx.x; i < NBD1; i += 256) shist[i] = 0;
   __syncthreads();
@@ -472,6 +474,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k1_generic(const u32* __restrict__ keys, u64 n, int alpha, int beta,
                                                   u64 S, u32* __restrict__ D, u32* __restrict__ meta,
                                                   ull* __restrict__ hist1) {
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;

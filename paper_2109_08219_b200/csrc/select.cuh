@@ -103,6 +103,8 @@ __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, co
 // beta = 2 the max delegates alone), so most steps cost ~1 op per key.
 template <int BETA2>
 __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ u32 shist[NBD2];
   __shared__ DigitResult r1;
   __shared__ ull scratch[8];
@@ -215,6 +217,8 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
                                                 const u32* __restrict__ region_cnt, u32 nregions, u64 R,
                                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off,
                                                 const u32* __restrict__ D, u64 nD) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ u32 shist[NBD3];
   __shared__ DigitResult r3;
   __shared__ ull scratch[8];
