@@ -339,14 +339,18 @@ def run_ours(args):
             for _ in range(3):
                 p.launch(v, stream)
             torch.cuda.synchronize()
+            # median of 5 batches of back-to-back replays (robust to clock / HBM drift over the sweep)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = max(5, args.steps // 4)
-            a.record(stream)
-            for _ in range(reps):
-                p.launch(v, stream)
-            b.record(stream)
-            torch.cuda.synchronize()
-            t = a.elapsed_time(b) / reps
+            reps = max(5, args.steps // 10)
+            batch = []
+            for _ in range(5):
+                a.record(stream)
+                for _ in range(reps):
+                    p.launch(v, stream)
+                b.record(stream)
+                torch.cuda.synchronize()
+                batch.append(a.elapsed_time(b) / reps)
+            t = statistics.median(batch)
             p.launch(v, stream, events=ev_arrays[0])
             h = p.header()
             st_ms = {name: round(lib.dtopk_event_elapsed_ms(ev_arrays[0][i], ev_arrays[0][i + 1]), 4)

@@ -163,6 +163,10 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+#ifndef DTOPK_K5B_GRID
+#define DTOPK_K5B_GRID 8  // K5b: latency-bound, one warp per part; 8 CTAs per SM keep more parts in flight
+#endif
+
 inline int grid_for(u64 work_items, int cap) {
   if (work_items == 0) return 1;
   return (int)std::max<u64>(1, std::min<u64>(work_items, (u64)cap));
@@ -502,7 +506,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   counted();
   launch_pdl(k5_emit, dim3(grid_for(L.k5_tiles, nsm * 4)), dim3(256), 0, s, k5);
   counted();
-  launch_pdl(k5b_copy, dim3(grid_for((L.nseg + 7) / 8, nsm * 4)), dim3(256), 0, s, ctrl, alpha, k, k5.stg_key, k5.stg_idx, k5.seg_gt,
+  launch_pdl(k5b_copy, dim3(grid_for((L.nseg + 7) / 8, nsm * DTOPK_K5B_GRID)), dim3(256), 0, s, ctrl, alpha, k, k5.stg_key, k5.stg_idx, k5.seg_gt,
                                                                k5.seg_eq, k5.e_gpos, k5.e_epos, L.cap_e,
                                                                k5.gt_keys, k5.gt_idx, k5.ties);
   counted();
