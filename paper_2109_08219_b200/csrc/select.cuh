@@ -156,46 +156,53 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
     }
     const bool any = mx >= kmin;
     if (!__any_sync(FULL, any)) continue;
-    u32 nb = 0, nc = 0;
+    // per-lane bit masks over the 16 keys: bucket members and candidate max delegates
+    const u32 rem = i0 < whi ? (u32)min((u64)16, whi - i0) : 0u;  // keys of this lane inside the warp range
+    u32 mb = 0, mc = 0;
     if (any) {
       u32 r = BETA2 ? 0u : (u32)(i0 % beta);  // ladder slot of element i0 (i0 is even for beta 2)
 #pragma unroll
       for (int j = 0; j < 16; j++) {
-        const bool in = i0 + j < whi;
-        nb += (in && v[j] - kmin <= span) ? 1u : 0u;
-        nc += (sup && in && r == 0 && v[j] >= kmin) ? 1u : 0u;
+        const bool in = (u32)j < rem;
+        mb |= (in && v[j] - kmin <= span) ? (1u << j) : 0u;
+        if (sup) mc |= (in && r == 0 && v[j] >= kmin) ? (1u << j) : 0u;
         r = BETA2 ? (r ^ 1u) : ((r + 1 == (u32)beta) ? 0u : r + 1);
       }
     }
+    const u32 nc = __popc(mc), nb = __popc(mb);
     if (sup && __any_sync(FULL, nc)) {
       const u32 incl = warp_incl_scan<u32>(nc);
       u64 o = out0 + run + incl - nc;
       run += __shfl_sync(FULL, incl, 31);
-      if (nc) {
-        u32 rr = BETA2 ? 0u : (u32)(i0 % beta);
+      if (mc) {
 #pragma unroll
         for (int j = 0; j < 16; j++) {
-          if (i0 + j < whi && rr == 0 && v[j] >= kmin) {
-            const u32 sid = (u32)((i0 + j) / beta);
+          if ((mc >> j) & 1u) {
             // beta 2: (d1, d2) sit in this lane's registers (pairs start at even j)
             const u32 d2 = BETA2 ? v[j | 1] : 0u;
-            a.sup_sid[o++] = make_uint4(sid, v[j], d2, d2);
+            a.sup_sid[o++] = make_uint4((u32)((i0 + j) / beta), v[j], d2, d2);
           }
-          rr = BETA2 ? (rr ^ 1u) : ((rr + 1 == (u32)beta) ? 0u : rr + 1);
         }
       }
     }
-    if (!__any_sync(FULL, nb)) continue;
+    const u32 wnb = __reduce_add_sync(FULL, nb);
+    if (wnb == 0) continue;
     const u32 incl = warp_incl_scan<u32>(nb);
     u32 o = 0;
     if (lane == 31) o = atomicAdd(&s_cnt, incl);
     o = __shfl_sync(FULL, o, 31) + incl - nb;
+    if (wnb > 64) {  // many members (tie-heavy / narrow range): warp-aggregated bins
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-      const bool mem = i0 + j < whi && v[j] - kmin <= span;
-      // warp-aggregated: tie-heavy inputs put whole warps on one bin
-      hist_add_warp(shist, (v[j] - kmin) >> DSH3, mem);
-      if (mem && compact) region[o++] = v[j];
+      for (int j = 0; j < 16; j++) hist_add_warp(shist, (v[j] - kmin) >> DSH3, (mb >> j) & 1u);
+    } else if (mb) {
+#pragma unroll
+      for (int j = 0; j < 16; j++)
+        if ((mb >> j) & 1u) atomicAdd(&shist[(v[j] - kmin) >> DSH3], 1u);
+    }
+    if (compact && mb) {
+#pragma unroll
+      for (int j = 0; j < 16; j++)
+        if ((mb >> j) & 1u) region[o++] = v[j];
     }
   }
   if (sup && lane == 0) {
