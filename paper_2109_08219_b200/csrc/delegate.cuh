@@ -139,6 +139,25 @@ __device__ __forceinline__ void acc_shfl(Acc<B>& A, int off) {
   acc_merge<B>(A, R, rp, rmn);
 }
 
+// beta = 2 merge of a whole warp's accumulators with warp reductions instead
+// of five shuffle butterfly levels: d_1 = max, the first lane holding it
+// supplies p, d_2 = max over the other lanes' L[0] and that lane's L[1],
+// min = min.  (Partial-mask reductions for smaller groups measured slower than
+// the butterflies.)  All 32 lanes must call.
+template <int B>
+__device__ __forceinline__ void acc_warp_b2(Acc<B>& A) {
+  if constexpr (B == 2) {
+    const int lane = threadIdx.x & 31;
+    const u32 m = __reduce_max_sync(FULL, A.L[0]);
+    const int first = __ffs(__ballot_sync(FULL, A.L[0] == m)) - 1;
+    const u32 m2 = __reduce_max_sync(FULL, lane == first ? A.L[1] : A.L[0]);
+    A.p = __shfl_sync(FULL, A.p, first);
+    A.mn = __reduce_min_sync(FULL, A.mn);
+    A.L[0] = m;
+    A.L[1] = m2;
+  }
+}
+
 // meta word of a subrange: bit 31 = constant subrange (every key equals d_1),
 // bits 0..30 = offset of an occurrence of d_1 inside the subrange (exact and
 // unique whenever d_2 < d_1).
@@ -326,7 +345,11 @@ __device__ __forceinline__ bool k1_warp_chunk(const K1Args& a, const u32* stage,
     released = true;
   }
   const int G = alpha >= K1_LOG_CHUNK ? 32 : 1 << (alpha - 6);  // lanes per subrange (alpha == 6: 1)
-  for (int off = 1; off < G; off <<= 1) acc_shfl<B>(A0, off);
+  if (B == 2 && G == 32) {
+    acc_warp_b2(A0);  // whole-warp subrange (alpha >= 11): warp reductions
+  } else {
+    for (int off = 1; off < G; off <<= 1) acc_shfl<B>(A0, off);
+  }
   const u64 wmask = (1ull << alpha) - 1;
   if (alpha <= K1_LOG_CHUNK) {
     const u32 meta = pack_meta(A0.mn == A0.L[0], (u32)((start + A0.p) & wmask));
