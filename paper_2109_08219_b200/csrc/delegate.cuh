@@ -194,7 +194,10 @@ __device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 s
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < B; i++) hist_add_agg(shist, ddig1(L[i]), w);
+      for (int i = 0; i < B; i++) {
+        // plain shared atomics: measured faster than match_any aggregation, also on all-equal input
+        if (w) atomicAdd(&shist[ddig1(L[i])], 1u);
+      }
     }
   }
 }

@@ -1,6 +1,9 @@
 // k1_exp.cu -- times k1_delegates alone on 2^30 random u32 keys (tooling).
 //   nvcc ... -DDTOPK_K1_EXP=<0|1|2> tools/k1_exp.cu
 #include <cstdio>
+#ifndef DTOPK_GEN_DIST
+#define DTOPK_GEN_DIST 0
+#endif
 #include "../paper_2109_08219_b200/csrc/delegate.cuh"
 #include "../paper_2109_08219_b200/csrc/generate.cuh"
 using namespace dtopk;
@@ -16,7 +19,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&D, (n / 32) * 4);
   cudaMalloc(&meta, (n / 64) * 4);
   cudaMalloc(&hist, NB1 * 8);
-  gen_kernel<<<nsm * 8, 256>>>(x, n, 0, 1234, 0);
+  gen_kernel<<<nsm * 8, 256>>>(x, n, DTOPK_GEN_DIST, 1234, 0x5A5A5A5A);
   for (int alpha : {6, 8, 11, 16}) {
     if (alpha > K1_LOG_CHUNK && alpha != 16) continue;
     const u64 S = n >> alpha;
