@@ -397,3 +397,33 @@ def test_cli_gen_run_sweep_dist(cuda, tmp_path, capsys):
     lines = (tmp_path / "d.csv").read_text().splitlines()
     assert lines[0] == cli.DIST_CSV_HEADER and len(lines) == 4
     assert cli.main(["run", f, "--k", "0"]) == 2  # InvalidK -> exit 2 (cli.py:270-275)
+
+
+@pytest.mark.parametrize("seed", range(96))
+def test_randomized_configs(seed, oracle_mod, cuda):
+    """Property sweep: random n, k, distribution, alpha / beta, largest /
+    smallest, u32 / f32 -- values, indices and the reference counters must all
+    match the oracle (catches interactions the targeted tests miss)."""
+    rng = np.random.default_rng(1000 + seed)
+    dist = ["uniform", "few_distinct", "nd_u32", "ascending", "descending", "all_equal", "normal_f32",
+            "pareto_f32"][seed % 8]
+    n = int(rng.integers(1, 1 << 21)) if seed % 3 else int(rng.integers(1 << 16, 1 << 22))
+    k = int(min(n, max(1, rng.choice([1, 7, 100, 1000, 5000, 40000, n // 2]))))
+    v = data.generate(dist, n, seed=seed, device=cuda)
+    kw = {"largest": bool(seed % 2)}
+    if seed % 4 == 1:
+        alpha = int(rng.integers(1, max(2, min(18, n.bit_length()))))
+        beta = int(rng.integers(1, 6))
+        if beta >= (1 << alpha) or beta * -(-n // (1 << alpha)) < k:
+            beta = 1
+        if beta * -(-n // (1 << alpha)) < k:
+            alpha = 1
+        if (1 << alpha) > n:
+            return
+        kw.update(alpha=alpha, beta=beta, auto_alpha=False)
+    elif seed % 4 == 2:
+        kw.update(beta=int(rng.integers(1, 9)))
+    try:
+        check_topk(v, k, oracle_mod, **kw)
+    except dtopk.InvalidBeta:
+        pass
