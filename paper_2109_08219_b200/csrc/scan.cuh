@@ -595,11 +595,17 @@ __global__ void __launch_bounds__(256, 4) bucket_sort(Ctrl* ctrl, SortBufs b, Bu
     for (int i = threadIdx.x; i < BK_SUB; i += 256) hs[i] = 0;
     __syncthreads();
     u32 ss[PER];  // sub << 16 | slot in the sub-bin, then sub << 16 | place in tmp
+    unsigned long long ce[PER];  // the bucket's composites, loaded once (all in flight together)
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+      const u32 i = r * 256 + threadIdx.x;
+      ce[r] = i < cnt ? bb.comp[lo + i] : 0ull;
+    }
 #pragma unroll
     for (int r = 0; r < PER; r++) {
       const u32 i = r * 256 + threadIdx.x;
       if (i < cnt) {
-        const u32 sub = (dhi[2 * (u64)(lo + i)] >> s2) & (BK_SUB - 1);
+        const u32 sub = ((u32)(ce[r] >> 32) >> s2) & (BK_SUB - 1);
         ss[r] = sub << 16 | atomicAdd(&hs[sub], 1u);
       }
     }
@@ -624,7 +630,7 @@ __global__ void __launch_bounds__(256, 4) bucket_sort(Ctrl* ctrl, SortBufs b, Bu
       if (i < cnt) {
         const u32 sub = ss[r] >> 16;
         const u32 place = hs[sub] + (ss[r] & 0xffffu);
-        tmp[place] = bb.comp[lo + i];
+        tmp[place] = ce[r];
         ss[r] = sub << 16 | place;
       }
     }
