@@ -263,6 +263,11 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
                                                     reinterpret_cast<u32*>(ws + L.sup_off), D, L.D_len);
   counted();
+  if (beta == 2)
+    launch_pdl(k2b_superset<1>, dim3(L.g2), dim3(256), 0, s, k2);
+  else
+    launch_pdl(k2b_superset<0>, dim3(L.g2), dim3(256), 0, s, k2);
+  counted();
   rec(ev, 2, s);
 }
 

@@ -127,6 +127,7 @@ struct Ctrl {
   ull nA;          // class-A records (one element > theta each)
   ull gt_rec_end;  // 1 + last record index that holds elements > theta
   u32 sup_total;   // records = candidate-superset entries (K2, resolved with theta)
+  u32 k2b_done;    // K2b CTAs finished (exact superset of a deferred, large-bucket call)
   ull sumEgt;      // elements > theta found by K4
   // assembly (K5) and tie location (K6)
   u32 k5_ticket;

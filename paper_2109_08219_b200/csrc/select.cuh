@@ -47,22 +47,10 @@ __device__ __forceinline__ void warp_append(u32* buf, ull* counter, u32 x, bool 
 
 constexpr int K2_SEG_PER = 24;  // superset segments per thread in the prefix (8 warps x <= 768 K2 CTAs)
 
-// Resolve theta from the digit-3 histogram (ctrl->selD.hist3) and publish the
-// exclusive prefix of the superset segment counts.  One CTA (256 threads).
-__device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, const DigitResult& r2, u32 nregions,
-                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off, DigitResult* r3,
-                                 ull* scratch) {
+// Exclusive prefix of the superset segment counts -> sup_off, sup_total (one CTA).
+__device__ void k2_superset_prefix(Ctrl* ctrl, u32 nregions, const u32* __restrict__ sup_cnt,
+                                   u32* __restrict__ sup_off, ull* scratch) {
   const int tid = threadIdx.x;
-  find_digit<NBD3>(ctrl->selD.hist3, r2.rem, r3, scratch);
-  if (tid == 0) {
-    const u32 kth = kmin + (r2.digit << DSH3) + r3->digit;
-    ctrl->selD.r3 = *r3;
-    ctrl->selD.kth = kth;
-    ctrl->res.theta_local = kth;
-    ctrl->res.theta_slot = (int64_t)kth;
-    ctrl->res.delegate_bucket = r1.cnt;
-  }
-  if (sup_cnt == nullptr) return;
   // nseg = 8 * nregions <= 8 * 4 * SMs (api.cu): at most K2_SEG_PER per thread, all loads in flight
   const u32 nseg = nregions * 8;
   const u32 per = (nseg + 255) / 256;
@@ -87,6 +75,25 @@ __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, co
     sup_off[nseg] = incl;
     ctrl->sup_total = incl;
   }
+}
+
+// Resolve theta from the digit-3 histogram (ctrl->selD.hist3) and publish the
+// exclusive prefix of the superset segment counts.  One CTA (256 threads).
+__device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, const DigitResult& r2, u32 nregions,
+                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off, DigitResult* r3,
+                                 ull* scratch, u64 nD) {
+  const int tid = threadIdx.x;
+  find_digit<NBD3>(ctrl->selD.hist3, r2.rem, r3, scratch);
+  if (tid == 0) {
+    const u32 kth = kmin + (r2.digit << DSH3) + r3->digit;
+    ctrl->selD.r3 = *r3;
+    ctrl->selD.kth = kth;
+    ctrl->res.theta_local = kth;
+    ctrl->res.theta_slot = (int64_t)kth;
+    ctrl->res.delegate_bucket = r1.cnt;
+  }
+  if (sup_cnt == nullptr || r1.cnt * 4 > nD) return;  // deferred: K2b builds and offsets the superset
+  k2_superset_prefix(ctrl, nregions, sup_cnt, sup_off, scratch);
 }
 
 // K2: pass 2 of kth(D) -- one read of D.  CTA c owns the contiguous range
@@ -124,7 +131,10 @@ __global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
   const u64 beta = BETA2 ? 2u : (u64)a.beta;
   const u64 out0 = (wlo + beta - 1) / beta;  // first subrange whose d_1 lies in [wlo, whi)
   u32* region = a.selbuf + lo;
-  const bool sup = a.sup_sid != nullptr;
+  // a bucket holding a large share of D (tie-heavy / narrow range): the bucket
+  // floor says little, so the superset is left to K2b, which filters D with
+  // the exact theta after pass 3
+  const bool sup = a.sup_sid != nullptr && r1.cnt * 4 <= a.nD;
   // a bucket holding a large share of D (tie-heavy or narrow-range inputs): do
   // not copy it into the regions; pass 3 scans D itself (same bytes, no writes)
   const bool compact = r1.cnt * 4 <= a.nD;
@@ -289,8 +299,91 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   __syncthreads();
   if (am_last) {
     __threadfence();
-    k2_resolve_theta(ctrl, kmin, r1, r2, nregions, sup_cnt, sup_off, &r3, scratch);
+    k2_resolve_theta(ctrl, kmin, r1, r2, nregions, sup_cnt, sup_off, &r3, scratch, nD);
   }
+}
+
+// K2b: exact candidate superset for calls whose theta bucket held a large share
+// of D (K2 deferred it): one more read of D with the exact theta, ordered
+// compaction per (CTA, warp) segment as in K2, then the last CTA offsets the
+// segments.  Other calls exit at once.
+template <int BETA2>
+__global__ void __launch_bounds__(256) k2b_superset(K2Args a) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ ull scratch[8];
+  __shared__ int am_last;
+  __shared__ uint4 stage[8][BETA2 ? 256 : 1];
+  Ctrl* ctrl = a.ctrl;
+  const DigitResult r1 = ctrl->selD.r1;
+  if (a.sup_sid == nullptr || r1.cnt * 4 <= a.nD) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u32 theta = ctrl->selD.kth;  // <= any external theta applied in K3: still a superset
+  const u64 lo = (u64)blockIdx.x * a.R;
+  const u64 hi = min(a.nD, lo + a.R);
+  const u64 wlen = a.R / 8;
+  const u64 wlo = min(hi, lo + (u64)warp * wlen), whi = min(hi, wlo + wlen);
+  const u64 beta = BETA2 ? 2u : (u64)a.beta;
+  const u64 out0 = (wlo + beta - 1) / beta;
+  u32 run = 0;
+  for (u64 base = wlo; base < whi; base += 512) {
+    const u64 i0 = base + (u64)lane * 16;
+    u32 v[16];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const u64 i = i0 + 4 * j;
+      if (i + 4 <= whi) {
+        const uint4 q = ld_nc_v4(a.D + i);
+        v[4 * j] = q.x;
+        v[4 * j + 1] = q.y;
+        v[4 * j + 2] = q.z;
+        v[4 * j + 3] = q.w;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++) v[4 * j + c] = i + c < whi ? a.D[i + c] : 0u;
+      }
+    }
+    const u32 rem = i0 < whi ? (u32)min((u64)16, whi - i0) : 0u;
+    u32 mc = 0, r = BETA2 ? 0u : (u32)(i0 % beta);
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      mc |= ((u32)j < rem && r == 0 && v[j] >= theta) ? (1u << j) : 0u;
+      r = BETA2 ? (r ^ 1u) : ((r + 1 == (u32)beta) ? 0u : r + 1);
+    }
+    const u32 nc = __popc(mc);
+    if (!__any_sync(FULL, nc)) continue;
+    const u32 incl = warp_incl_scan<u32>(nc);
+    const u32 tot = __shfl_sync(FULL, incl, 31);
+    if (BETA2) {
+      // stage the warp's (<= 256) entries in shared memory, then store them
+      // contiguously: all-candidate inputs (ties) would otherwise store one
+      // 16-byte entry per 128-byte line per instruction
+      u32 t = incl - nc;
+#pragma unroll
+      for (int j = 0; j < 16; j += 2)
+        if ((mc >> j) & 1u) stage[warp][t++] = make_uint4((u32)((i0 + j) >> 1), v[j], v[j + 1], v[j + 1]);
+      __syncwarp();
+      for (u32 q = lane; q < tot; q += 32) a.sup_sid[out0 + run + q] = stage[warp][q];
+      __syncwarp();
+    } else {
+      u64 o = out0 + run + incl - nc;
+#pragma unroll
+      for (int j = 0; j < 16; j++)
+        if ((mc >> j) & 1u) a.sup_sid[o++] = make_uint4((u32)((i0 + j) / beta), v[j], 0u, 0u);
+    }
+    run += tot;
+  }
+  if (lane == 0) {
+    a.sup_in[blockIdx.x * 8 + warp] = (u32)out0;
+    a.sup_cnt[blockIdx.x * 8 + warp] = run;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = atomicAdd(&ctrl->k2b_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  k2_superset_prefix(ctrl, gridDim.x, a.sup_cnt, a.sup_off, scratch);
 }
 
 // ---------------------------------------------------------------------------
