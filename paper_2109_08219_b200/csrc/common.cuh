@@ -63,7 +63,7 @@ __device__ __forceinline__ u32 dig3(u32 k) { return k & 0x3ffu; }
 // d), 33 x 64 buckets ordered like the keys.  A bucket is a key interval
 // [kmin, kmin + 2^r) with r <= 25; digit 2 = (key - kmin) >> 13 (12 bits),
 // digit 3 = (key - kmin) & 8191.
-constexpr int NBD1 = 2304;  // 2112 used, padded to a multiple of 256 (find_digit)
+constexpr int NBD1 = 2560;  // 2112 used, padded to 256 x an even count (find_digit reads bin pairs)
 constexpr int NBD2 = 4096, NBD3 = 8192;
 constexpr int DSH3 = 13;  // digit 2 = (key - kmin) >> 13 (12 bits), digit 3 = low 13 bits
 __device__ __forceinline__ u32 ddig1(u32 key) {
@@ -104,7 +104,7 @@ struct DigitResult {
   ull above;  // population of all higher buckets
 };
 
-struct SelectState {
+struct alignas(16) SelectState {  // 16-byte aligned: find_digit reads the histograms as ulonglong2
   ull hist1[NBD1];  // sized for the delegate digits; the pool select uses NB1/NB2/NB3 of them
   ull hist2[NBD2];
   ull hist3[NBD3];
@@ -328,15 +328,20 @@ __device__ __forceinline__ T block_incl_scan_256(T v, T* scratch) {
 template <int NB>
 __device__ void find_digit(const ull* hist, ull k_rem, DigitResult* out, ull* scratch) {
   constexpr int PER = NB / 256;
+  static_assert(PER % 2 == 0, "find_digit reads bin pairs");
   const int t = threadIdx.x;
   ull loc[PER];
   ull sum = 0;
+  // thread t owns bins NB-1-t*PER .. NB-PER-t*PER (descending); 16-byte loads of bin pairs
+  const ulonglong2* h2 = reinterpret_cast<const ulonglong2*>(hist + NB - PER - t * PER);
 #pragma unroll
-  for (int i = 0; i < PER; i++) {
-    const int b = NB - 1 - (t * PER + i);
-    loc[i] = __ldcg(&hist[b]);
-    sum += loc[i];
+  for (int i = 0; i < PER / 2; i++) {
+    const ulonglong2 q = __ldcg(&h2[i]);  // bins NB-PER-t*PER + 2i, +2i+1
+    loc[PER - 1 - 2 * i] = q.x;
+    loc[PER - 2 - 2 * i] = q.y;
   }
+#pragma unroll
+  for (int i = 0; i < PER; i++) sum += loc[i];
   if (t == 0) out->valid = 0;
   const ull incl = block_incl_scan_256<ull>(sum, scratch);
   ull run = incl - sum;

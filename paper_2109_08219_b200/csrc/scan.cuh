@@ -588,7 +588,6 @@ __global__ void __launch_bounds__(256, 4) bucket_sort(Ctrl* ctrl, SortBufs b, Bu
   const u64 ko = ctrl->res.k_out;
   const u32 hi = max(ctrl->maxkey, ctrl->sort_lo);
   const u64* idx = ctrl->sort_src ? b.ib : b.ia;
-  const u32* dhi = reinterpret_cast<const u32*>(bb.comp) + 1;  // d of composite j at dhi[2 j]
   for (u32 bk = blockIdx.x; bk < nb; bk += gridDim.x) {
     const u32 lo = bb.start[bk], cnt = bb.start[bk + 1] - lo;
     if ((u64)lo >= ko || cnt == 0) continue;  // uniform across the CTA
