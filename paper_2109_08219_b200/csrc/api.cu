@@ -96,7 +96,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.region_cnt = take((u64)L.g2 * 4);
   L.sup_sid = take(L.S * 16);
   L.sup_in = take((u64)L.g2 * 8 * 4);
-  L.sup_cnt = take((u64)L.g2 * 8 * 4);
+  L.sup_cnt = take(std::max<u64>((u64)L.g2 * 8, 256 * K2_SEG_PER) * 4);  // padded: read as uint4 by thread
   L.sup_off = take(((u64)L.g2 * 8 + 1) * 4);
   L.rec = take(L.S * 16);
   L.k5_tg = take(L.k5_tiles * 8);

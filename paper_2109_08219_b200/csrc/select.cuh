@@ -51,15 +51,23 @@ constexpr int K2_SEG_PER = 24;  // superset segments per thread in the prefix (8
 __device__ void k2_superset_prefix(Ctrl* ctrl, u32 nregions, const u32* __restrict__ sup_cnt,
                                    u32* __restrict__ sup_off, ull* scratch) {
   const int tid = threadIdx.x;
-  // nseg = 8 * nregions <= 8 * 4 * SMs (api.cu): at most K2_SEG_PER per thread, all loads in flight
+  // nseg = 8 * nregions <= 8 * 768 = 256 * K2_SEG_PER: thread t owns segments
+  // [t * K2_SEG_PER, +K2_SEG_PER), read as uint4 (sup_cnt is padded to 256 * K2_SEG_PER)
   const u32 nseg = nregions * 8;
-  const u32 per = (nseg + 255) / 256;
   u32 c[K2_SEG_PER];
   u32 sum = 0;
+  const uint4* c4 = reinterpret_cast<const uint4*>(sup_cnt) + tid * (K2_SEG_PER / 4);
+#pragma unroll
+  for (int q = 0; q < K2_SEG_PER / 4; q++) {
+    const uint4 x = __ldcg(&c4[q]);
+    c[4 * q] = x.x;
+    c[4 * q + 1] = x.y;
+    c[4 * q + 2] = x.z;
+    c[4 * q + 3] = x.w;
+  }
 #pragma unroll
   for (int q = 0; q < K2_SEG_PER; q++) {
-    const u32 i = tid * per + q;
-    c[q] = (q < (int)per && i < nseg) ? __ldcg(&sup_cnt[i]) : 0u;
+    if ((u32)(tid * K2_SEG_PER + q) >= nseg) c[q] = 0u;
     sum += c[q];
   }
   u32* sc = reinterpret_cast<u32*>(scratch);
@@ -67,8 +75,8 @@ __device__ void k2_superset_prefix(Ctrl* ctrl, u32 nregions, const u32* __restri
   u32 run = incl - sum;
 #pragma unroll
   for (int q = 0; q < K2_SEG_PER; q++) {
-    const u32 i = tid * per + q;
-    if (q < (int)per && i < nseg) sup_off[i] = run;
+    const u32 i = tid * K2_SEG_PER + q;
+    if (i < nseg) sup_off[i] = run;
     run += c[q];
   }
   if (tid == 255) {
