@@ -20,15 +20,18 @@
 // ones; all-equal keys make every candidate C and nothing is re-read.
 //
 //   K3  classification of K2's candidate superset (subranges whose max
-//       delegate reaches theta's top-11-bit bucket, already in subrange
-//       order): one 16-byte record per entry, entries below theta inert.
+//       delegate reaches theta's first-digit bucket, or >= theta exactly when
+//       K2b built it; already in subrange order): one 16-byte record per
+//       entry, entries below theta inert.
 //   K4  reads the E candidates; each candidate part (<= 8192 keys) writes its
 //       elements > theta and its ties, in index order, into a private staging
 //       slot -- no global ordering needed.
-//   K5  ordered scan over the records (thread per record, decoupled
-//       look-back over tiles of 256) -> positions in the pool P_gt (index
-//       order) and in the tie list (first k, index order).
-//   K6  locates the ties of class-D records that fall among the first k ties.
+//   K4T counts the ties of T candidates (ordered early stop on tie-heavy input).
+//   K5  ordered scan over the records (k5_count: tile sums, last CTA turns
+//       them into prefixes; k5_emit: block scans on top) -> positions in the
+//       pool P_gt (index order) and in the tie list (first k, index order).
+//   K5b copies the staged keys / ties of E candidates to their places.
+//   K6  locates the ties of C / T records that fall among the first k ties.
 #pragma once
 
 #include <cub/block/block_radix_sort.cuh>
@@ -417,13 +420,13 @@ __global__ void __launch_bounds__(256) k4_read(K4Args a) {
 
 // K4T: count the ties of T candidates (d_1 == theta, max not unique,
 // subrange not constant).  Few T candidates: count them all in parallel (one
-// warp each).  Many (tie-heavy inputs): walk the 32-subrange words in index
-// order in chunks taken by ticket, and stop taking chunks once the completed
+// warp each).  Many (tie-heavy inputs): walk the records in index order, 32
+// per warp and 8 warps per ticket, and stop taking tickets once the completed
 // chunks already hold k ties -- every later tie lands beyond position k, so
 // its count is never needed (it stays 0; concatenated_len is then a lower
 // bound, flagged through concat_skipped_fq).
 constexpr u32 K4T_PARALLEL_MAX = 4096;
-constexpr u32 K4T_WORDS_PER_TICKET = 8;
+constexpr u32 K4T_CHUNKS_PER_TICKET = 8;  // 32-record chunks (one per warp) per ticket
 
 template <int MODE>
 __device__ __forceinline__ u32 count_ties_warp(const u32* __restrict__ keys, u64 n, int alpha, u64 sid, u32 theta) {
@@ -483,10 +486,10 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
       if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, 1ull);
       break;
     }
-    if (chunk * K4T_WORDS_PER_TICKET >= nchunks) break;
+    if (chunk * K4T_CHUNKS_PER_TICKET >= nchunks) break;
     // one 32-record chunk per warp, lane per record: ties of its B/C/E/T records
     u32 eq = 0;
-    const u64 c = chunk * K4T_WORDS_PER_TICKET + warp;
+    const u64 c = chunk * K4T_CHUNKS_PER_TICKET + warp;
     if (c < nchunks) {
       const u64 i = c * 32 + lane;
       const uint4 rc = i < total ? a.rec[i] : make_uint4(0u, 0u, 0u, CLS_NONE);
