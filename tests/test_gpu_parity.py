@@ -427,3 +427,45 @@ def test_randomized_configs(seed, oracle_mod, cuda):
         check_topk(v, k, oracle_mod, **kw)
     except dtopk.InvalidBeta:
         pass
+
+
+def _key_tensor(v: torch.Tensor, largest: bool) -> torch.Tensor:
+    """Device int64 keys of the library's order (larger key = selected first)."""
+    b = v.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    if v.dtype == torch.float32:
+        b = torch.where(b >> 31 == 1, b ^ 0xFFFFFFFF, b | 0x80000000)
+    return b if largest else 0xFFFFFFFF - b
+
+
+@pytest.mark.parametrize("dist,k,largest", [
+    ("uniform", 1, True), ("uniform", 1024, True), ("uniform", 1 << 20, True), ("uniform", 1 << 16, False),
+    ("normal_f32", 1024, True), ("ascending", 1 << 16, True), ("nd_u32", 1 << 16, True),
+])
+def test_full_size_properties(dist, k, largest, cuda):
+    """BASELINE sizes (N = 2^30) where the CPU oracle is too slow: size-independent
+    properties that pin the answer -- values[i] == v[indices[i]], indices unique,
+    (key desc, index asc) order, exactly the keys above the k-th plus the lowest-
+    index ties, and the k-th key's rank: #(key > kth) < k <= #(key >= kth)."""
+    n = 1 << 30
+    v = data.generate(dist, n, seed=5, device=cuda)
+    r = dtopk.dr_topk(v, dtopk.PipelineConfig(k=k, largest=largest))
+    idx, vals = r.indices, r.values
+    assert idx.numel() == k and vals.numel() == k
+    assert torch.equal(v.view(torch.int32)[idx], vals.view(torch.int32))
+    assert torch.unique(idx).numel() == k
+    key = _key_tensor(v, largest)
+    kk = key[idx]
+    assert bool((kk[:-1] >= kk[1:]).all())
+    same = kk[:-1] == kk[1:]
+    assert bool((idx[:-1][same] < idx[1:][same]).all())
+    kth = int(kk[-1])
+    gt = int((key > kth).sum())
+    ge = int((key >= kth).sum())
+    assert gt < k <= ge
+    assert int((kk > kth).sum()) == gt  # every key above the k-th is in the answer
+    ties_taken = idx[kk == kth]
+    if ties_taken.numel() < ge - gt:  # lowest-index ties first
+        all_ties = torch.nonzero(key == kth).flatten()
+        assert torch.equal(torch.sort(ties_taken).values, all_ties[: ties_taken.numel()])
+    del key, v
+    torch.cuda.empty_cache()
