@@ -469,3 +469,27 @@ def test_full_size_properties(dist, k, largest, cuda):
         assert torch.equal(torch.sort(ties_taken).values, all_ties[: ties_taken.numel()])
     del key, v
     torch.cuda.empty_cache()
+
+
+def test_config5_single_gpu_2pow33_properties(cuda):
+    """BASELINE config 5 size on one GPU (N = 2^33, 32 GiB): answer properties,
+    with the rank counts of the k-th key taken chunk by chunk."""
+    n, k = 1 << 33, 1024
+    v = data.generate("uniform", n, seed=9, device=cuda)
+    r = dtopk.dr_topk(v, dtopk.PipelineConfig(k=k))
+    idx = r.indices
+    vi = v.view(torch.int32)
+    assert torch.equal(vi[idx], r.values.view(torch.int32))
+    assert torch.unique(idx).numel() == k
+    kk = vi[idx].to(torch.int64) & 0xFFFFFFFF
+    assert bool((kk[:-1] >= kk[1:]).all())
+    kth = int(kk[-1])
+    gt = ge = 0
+    for c in range(0, n, 1 << 30):
+        ch = vi[c:c + (1 << 30)].to(torch.int64) & 0xFFFFFFFF
+        gt += int((ch > kth).sum())
+        ge += int((ch >= kth).sum())
+        del ch
+    assert gt < k <= ge
+    del v, vi
+    torch.cuda.empty_cache()
