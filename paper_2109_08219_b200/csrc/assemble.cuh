@@ -42,6 +42,9 @@ namespace dtopk {
 
 enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4, CLS_NONE = 5 };
 
+#ifndef DTOPK_K3_U
+#define DTOPK_K3_U 1
+#endif
 constexpr int K4_TILE = 8192;   // keys per K4 tile
 constexpr int K5_RPT = 4;      // consecutive records per K5 thread
 constexpr int K5_TILE = 256 * K5_RPT;  // records per K5 tile
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
     const u64 in0 = a.sup_in[seg];
     const u64 o0 = a.sup_off[seg];
     const u32 cnt = a.sup_off[seg + 1] - (u32)o0;
-    constexpr int U = 1;  // 32-entry groups per warp step (more in flight measured slower)
+    constexpr int U = DTOPK_K3_U;  // 32-entry groups per warp step (1 measured fastest; 2, 4 slower)
     for (u32 j0 = 0; j0 < cnt; j0 += 32 * U) {
       u32 sid[U], d1[U], d2[U], dl[U], m[U];
 #pragma unroll
