@@ -123,6 +123,23 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
     const u64 in0 = a.sup_in[seg];
     const u64 o0 = a.sup_off[seg];
     const u32 cnt = a.sup_off[seg + 1] - (u32)o0;
+    // beta 2: the superset entry alone decides class E (d_1 > theta, d_2 >= theta),
+    // so the segment's E slots come from one atomic per segment, counted first
+    // (a contended per-group atomic sat on every group's critical path)
+    u32 e_next = 0;
+    const bool seg_e = beta == 2;
+    if (seg_e) {
+      u32 ne = 0;
+      for (u32 j0 = 0; j0 < cnt; j0 += 32) {
+        const u32 j = j0 + lane;
+        const uint4 e = j < cnt ? a.sup_sid[in0 + j] : make_uint4(0u, 0u, 0u, 0u);
+        ne += __popc(__ballot_sync(FULL, j < cnt && e.y > theta && e.z >= theta));
+      }
+      if (ne) {
+        if (lane == 0) e_next = atomicAdd(&ctrl->nE, ne);
+        e_next = __shfl_sync(FULL, e_next, 0);
+      }
+    }
     constexpr int U = DTOPK_K3_U;  // 32-entry groups per warp step (1 measured fastest; 2, 4 slower)
     for (u32 j0 = 0; j0 < cnt; j0 += 32 * U) {
       u32 sid[U], d1[U], d2[U], dl[U], m[U];
@@ -160,9 +177,10 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
         if (be | bt) {
           u32 e0 = 0, t0 = 0;
           if (lane == 0) {
-            if (be) e0 = atomicAdd(&ctrl->nE, (u32)__popc(be));
+            if (be) e0 = seg_e ? e_next : atomicAdd(&ctrl->nE, (u32)__popc(be));
             if (bt) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
           }
+          e_next += __popc(be);
           e0 = __shfl_sync(FULL, e0, 0);
           t0 = __shfl_sync(FULL, t0, 0);
           if (cls == CLS_E) {
