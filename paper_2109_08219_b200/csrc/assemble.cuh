@@ -46,7 +46,10 @@ enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4, CLS_NONE
 #define DTOPK_K3_U 1
 #endif
 constexpr int K4_TILE = 8192;   // keys per K4 tile
-constexpr int K5_RPT = 4;      // consecutive records per K5 thread
+#ifndef DTOPK_K5_RPT
+#define DTOPK_K5_RPT 4
+#endif
+constexpr int K5_RPT = DTOPK_K5_RPT;  // consecutive records per K5 thread (A/B: 4 beats 2 and 8)
 constexpr int K5_TILE = 256 * K5_RPT;  // records per K5 tile
 constexpr int SMALL_POOL = 8192;  // pools up to this size are finished by one CTA (8 keys per thread)
 
