@@ -285,15 +285,7 @@ __device__ __forceinline__ void ladder_merge(u32 (&L)[B], const u32 (&R)[B]) {
   }
 }
 
-template <int B>
-__device__ __forceinline__ void ladder_shfl_merge(u32 (&L)[B], int off) {
-  u32 R[B];
-#pragma unroll
-  for (int i = 0; i < B; i++) R[i] = __shfl_xor_sync(FULL, L[i], off);
-  ladder_merge<B>(L, R);
-}
-
-// ---------------------------------------------------------------------------
+------------------------------------------------------
 // Block scans for 256-thread blocks.
 // ---------------------------------------------------------------------------
 template <typename T>

@@ -33,18 +33,6 @@ struct K2Args {
   u32* sup_off;  // [g2 * 8 + 1] exclusive prefix of sup_cnt (theta resolver)
 };
 
-// Warp-aggregated append of `x` (where pred) to buf[*counter++].
-__device__ __forceinline__ void warp_append(u32* buf, ull* counter, u32 x, bool pred) {
-  const u32 b = __ballot_sync(FULL, pred);
-  if (!b) return;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(b) - 1;
-  ull base = 0;
-  if (lane == leader) base = atomicAdd(counter, (ull)__popc(b));
-  base = __shfl_sync(FULL, base, leader);
-  if (pred) buf[base + __popc(b & lanemask_lt())] = x;
-}
-
 constexpr int K2_SEG_PER = 24;  // superset segments per thread in the prefix (8 warps x <= 768 K2 CTAs)
 
 // Exclusive prefix of the superset segment counts -> sup_off, sup_total (one CTA).
