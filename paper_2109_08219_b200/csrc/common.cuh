@@ -285,7 +285,7 @@ __device__ __forceinline__ void ladder_merge(u32 (&L)[B], const u32 (&R)[B]) {
   }
 }
 
-------------------------------------------------------
+// ---------------------------------------------------------------------------
 // Block scans for 256-thread blocks.
 // ---------------------------------------------------------------------------
 template <typename T>
