@@ -995,8 +995,12 @@ __global__ void __launch_bounds__(1024) finish_small(Ctrl* ctrl, const u32* __re
   // (the pool of a large-n top-k spans few bits, e.g. ~12 for n = 2^30, k = 1024)
   if (m <= 64)
     finish_small_r<MODE, 1>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+  else if (m <= 1024)
+    finish_small_radix<MODE, 1>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   else if (m <= 2048)
     finish_small_radix<MODE, 2>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
+  else if (m <= 4096)
+    finish_small_radix<MODE, 4>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   else
     finish_small_radix<MODE, 8>(ctrl, m, ko, G, theta, hi, gt_keys, gt_idx, ties, ov, oi, offset, sk);
   if (threadIdx.x == 0) ctrl->small_done = 1;
