@@ -158,6 +158,34 @@ __device__ __forceinline__ void acc_warp_b2(Acc<B>& A) {
   }
 }
 
+// Whole-warp top-B merge for B != 2: B rounds of a warp max over the lanes'
+// ladder heads (each lane's ladder is non-increasing); the first lane holding
+// the round's max advances, so duplicates count once per copy -- the top-B
+// multiset.  p comes from the first lane holding the overall max.  All 32
+// lanes must call.
+template <int B>
+__device__ __forceinline__ void acc_warp_merge(Acc<B>& A) {
+  const int lane = threadIdx.x & 31;
+  u32 out[B];
+  int ptr = 0;
+  u32 p0 = 0;
+#pragma unroll
+  for (int r = 0; r < B; r++) {
+    u32 head = 0;
+#pragma unroll
+    for (int i = 0; i < B; i++) head = ptr == i ? A.L[i] : head;
+    const u32 m = __reduce_max_sync(FULL, head);
+    const int first = __ffs(__ballot_sync(FULL, head == m)) - 1;
+    if (r == 0) p0 = __shfl_sync(FULL, A.p, first);
+    ptr += lane == first ? 1 : 0;
+    out[r] = m;
+  }
+  A.mn = __reduce_min_sync(FULL, A.mn);
+  A.p = p0;
+#pragma unroll
+  for (int i = 0; i < B; i++) A.L[i] = out[i];
+}
+
 // meta word of a subrange: bit 31 = constant subrange (every key equals d_1),
 // bits 0..30 = offset of an occurrence of d_1 inside the subrange (exact and
 // unique whenever d_2 < d_1).
@@ -350,6 +378,8 @@ __device__ __forceinline__ bool k1_warp_chunk(const K1Args& a, const u32* stage,
   const int G = alpha >= K1_LOG_CHUNK ? 32 : 1 << (alpha - 6);  // lanes per subrange (alpha == 6: 1)
   if (B == 2 && G == 32) {
     acc_warp_b2(A0);  // whole-warp subrange (alpha >= 11): warp reductions
+  } else if (B != 2 && G == 32) {
+    acc_warp_merge(A0);  // whole-warp subrange, beta != 2: B rounds of warp max over the lanes' ladder heads
   } else {
     for (int off = 1; off < G; off <<= 1) acc_shfl<B>(A0, off);
   }

@@ -28,6 +28,7 @@ ap.add_argument("--ks", default="1,16,256,1024,4096,16384,65536,262144,1048576")
 ap.add_argument("--dist", default="uniform")
 ap.add_argument("--alphas", default="", help="comma list of manual alphas per k (auto if empty)")
 ap.add_argument("--const", type=float, default=3.0, help="auto_alpha const_c")
+ap.add_argument("--beta", type=int, default=2)
 args = ap.parse_args()
 lib = _native.load()
 n = 1 << args.log2n
@@ -39,7 +40,8 @@ out = {}
 ks = [int(x) for x in args.ks.split(",")]
 alphas = [int(x) for x in args.alphas.split(",")] if args.alphas else [None] * len(ks)
 for k, al in zip(ks, alphas):
-    cfg = dtopk.PipelineConfig(k=k, const_c=args.const) if al is None else dtopk.PipelineConfig(k=k, alpha=al, auto_alpha=False)
+    cfg = (dtopk.PipelineConfig(k=k, const_c=args.const, beta=args.beta) if al is None
+           else dtopk.PipelineConfig(k=k, alpha=al, auto_alpha=False, beta=args.beta))
     p = DrTopK(n, cfg, _native.DTYPE_U32, torch.uint32, v.device, timed=False, use_graph=True)
     for _ in range(3):
         p.launch(v, s)
