@@ -21,6 +21,10 @@
 #include "scan.cuh"
 #include "select.cuh"
 
+#ifndef DTOPK_K2_CPS
+#define DTOPK_K2_CPS 4  // K2 CTAs (regions) per SM
+#endif
+
 using namespace dtopk;
 
 namespace {
@@ -73,7 +77,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.words = (L.S + 31) / 32;
   // K2 regions: one contiguous range of D per CTA
   // <= 768 CTAs: the superset prefix holds K2_SEG_PER (24) segments per thread
-  const u64 g2 = std::max<u64>(1, std::min<u64>(std::min<u64>((u64)num_sms() * 4, 768), (L.D_len + 4095) / 4096));
+  const u64 g2 = std::max<u64>(1, std::min<u64>(std::min<u64>((u64)num_sms() * DTOPK_K2_CPS, 768), (L.D_len + 4095) / 4096));
   L.g2 = (u32)g2;
   L.R2 = ((L.D_len + g2 - 1) / g2 + 511) / 512 * 512;
   L.k4_tiles = (L.cap_e * W + K4_TILE - 1) / K4_TILE;

@@ -33,6 +33,9 @@ struct K2Args {
   u32* sup_off;  // [g2 * 8 + 1] exclusive prefix of sup_cnt (theta resolver)
 };
 
+#ifndef DTOPK_K2_MINB
+#define DTOPK_K2_MINB 4  // K2 min CTAs per SM: caps registers so all DTOPK_K2_CPS regions of an SM are resident (single wave)
+#endif
 constexpr int K2_SEG_PER = 24;  // superset segments per thread in the prefix (8 warps x <= 768 K2 CTAs)
 
 // Exclusive prefix of the superset segment counts -> sup_off, sup_total (one CTA).
@@ -105,7 +108,7 @@ __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, co
 // A lane first tests its 16 keys against kmin through their maximum (for
 // beta = 2 the max delegates alone), so most steps cost ~1 op per key.
 template <int BETA2>
-__global__ void __launch_bounds__(256) k2_scan_delegates(K2Args a) {
+__global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a) {
   pdl_trigger();
   pdl_wait();
   __shared__ u32 shist[NBD2];
