@@ -42,6 +42,9 @@ namespace dtopk {
 
 enum Cls : u32 { CLS_A = 0, CLS_B = 1, CLS_C = 2, CLS_T = 3, CLS_E = 4, CLS_NONE = 5 };
 
+#ifndef DTOPK_K5E_MINB
+#define DTOPK_K5E_MINB 4  // k5_emit min CTAs per SM (register cap: 107 -> 64, one wave; k=2^20: 21 -> 16.5 us)
+#endif
 #ifndef DTOPK_K3_U
 #define DTOPK_K3_U 1
 #endif
@@ -718,7 +721,7 @@ __global__ void __launch_bounds__(256) k5_count(K5Args a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k5_emit(K5Args a) {
+__global__ void __launch_bounds__(256, DTOPK_K5E_MINB) k5_emit(K5Args a) {
   pdl_trigger();
   pdl_wait();
   __shared__ u64 scratch_g[8], scratch_e[8];
