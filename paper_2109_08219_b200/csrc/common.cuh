@@ -11,6 +11,10 @@
 
 #include "../../include/dtopk.h"
 
+#ifndef DTOPK_TAIL_MINB
+#define DTOPK_TAIL_MINB 4  // scan_emit min CTAs per SM (register cap 79 -> 64: one wave on large pools; capping k4_read too slowed small k)
+#endif
+
 namespace dtopk {
 
 using u32 = uint32_t;

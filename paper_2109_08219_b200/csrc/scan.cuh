@@ -41,7 +41,7 @@ struct ScanArgs {
 
 
 template <int MODE>
-__global__ void __launch_bounds__(256) scan_emit(ScanArgs a) {
+__global__ void __launch_bounds__(256, DTOPK_TAIL_MINB) scan_emit(ScanArgs a) {
   __shared__ DigitResult r3s;
   __shared__ ull scratch[8];
   __shared__ u32 s_wgt[8], s_weq[8];
