@@ -132,18 +132,26 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
     // beta 2: the superset entry alone decides class E (d_1 > theta, d_2 >= theta),
     // so the segment's E slots come from one atomic per segment, counted first
     // (a contended per-group atomic sat on every group's critical path)
-    u32 e_next = 0;
+    // Likewise the T slots: every entry with d_1 == d_2 == theta is T or C (C =
+    // constant subrange, known only from meta); all of them get a slot, C slots
+    // become holes (t_sid = ~0) that K4T skips.
+    u32 e_next = 0, t_next = 0, t_true = 0;
     const bool seg_e = beta == 2;
     if (seg_e) {
-      u32 ne = 0;
+      u32 ne = 0, ntc = 0;
       for (u32 j0 = 0; j0 < cnt; j0 += 32) {
         const u32 j = j0 + lane;
         const uint4 e = j < cnt ? a.sup_sid[in0 + j] : make_uint4(0u, 0u, 0u, 0u);
         ne += __popc(__ballot_sync(FULL, j < cnt && e.y > theta && e.z >= theta));
+        ntc += __popc(__ballot_sync(FULL, j < cnt && e.y == theta && e.z == theta));
       }
-      if (ne) {
-        if (lane == 0) e_next = atomicAdd(&ctrl->nE, ne);
+      if (ne | ntc) {
+        if (lane == 0) {
+          if (ne) e_next = atomicAdd(&ctrl->nE, ne);
+          if (ntc) t_next = atomicAdd(&ctrl->nTslots, ntc);
+        }
         e_next = __shfl_sync(FULL, e_next, 0);
+        t_next = __shfl_sync(FULL, t_next, 0);
       }
     }
     constexpr int U = DTOPK_K3_U;  // 32-entry groups per warp step (1 measured fastest; 2, 4 slower)
@@ -180,15 +188,16 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
         u32 x = cls | (fq ? 8u : 0u);
         // E / T list slots: one atomic per list and 32 entries, only when present
         const u32 be = __ballot_sync(FULL, cls == CLS_E), bt = __ballot_sync(FULL, cls == CLS_T);
-        if (be | bt) {
+        const u32 btc = seg_e ? __ballot_sync(FULL, keep && d1[u] == theta && d2[u] == theta) : 0u;  // T or C
+        if (be | bt | btc) {
           u32 e0 = 0, t0 = 0;
           if (lane == 0) {
             if (be) e0 = seg_e ? e_next : atomicAdd(&ctrl->nE, (u32)__popc(be));
-            if (bt) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
+            if (bt && !seg_e) t0 = atomicAdd(&ctrl->nT, (u32)__popc(bt));
           }
           e_next += __popc(be);
           e0 = __shfl_sync(FULL, e0, 0);
-          t0 = __shfl_sync(FULL, t0, 0);
+          t0 = seg_e ? t_next : __shfl_sync(FULL, t0, 0);
           if (cls == CLS_E) {
             const u32 e = e0 + __popc(be & lt);
             if (e < a.cap_e) {
@@ -196,11 +205,20 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
               a.e_epos[e] = ~0ull;  // k5_emit may skip this record's tile: then K5b must place nothing
             }
             x |= e << 4;
-          } else if (cls == CLS_T) {
+          } else if (seg_e && ((btc >> lane) & 1u)) {
+            const u32 t = t0 + __popc(btc & lt);
+            a.t_sid[t] = cls == CLS_T ? sid[u] : 0xffffffffu;  // a C entry leaves a hole
+            a.t_cnt[t] = 0;
+            if (cls == CLS_T) x |= t << 4;
+          } else if (!seg_e && cls == CLS_T) {
             const u32 t = t0 + __popc(bt & lt);
             a.t_sid[t] = sid[u];
             a.t_cnt[t] = 0;
             x |= t << 4;
+          }
+          if (seg_e) {
+            t_next += __popc(btc);
+            t_true += __popc(bt);
           }
         }
         if (valid) a.rec.r[o0 + j] = make_uint4(sid[u], d1[u], m[u], x);
@@ -212,6 +230,7 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
         if (cls == CLS_A || cls == CLS_E) gt_rec = max(gt_rec, o0 + j + 1);
       }
     }
+    if (t_true && lane == 0) atomicAdd(&ctrl->nT, t_true);
   }
   ull v[4] = {st_cand, st_fq, st_pq, st_a};
 #pragma unroll
@@ -493,8 +512,11 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
   const u64 gw = ((u64)blockIdx.x * 256 + threadIdx.x) >> 5;
   const u64 nw = ((u64)gridDim.x * 256) >> 5;
   if (nT <= K4T_PARALLEL_MAX || a.exact) {
-    for (u64 t = gw; t < nT; t += nw) {
-      const u32 c = count_ties_warp<MODE>(a.keys, a.n, a.alpha, a.t_sid[t], theta);
+    const u64 nslots = max(nT, (u64)ctrl->nTslots);  // beta 2: slots include C holes
+    for (u64 t = gw; t < nslots; t += nw) {
+      const u32 sid = a.t_sid[t];
+      if (sid == 0xffffffffu) continue;  // hole left by a C entry (K3)
+      const u32 c = count_ties_warp<MODE>(a.keys, a.n, a.alpha, sid, theta);
       if (lane == 0) a.t_cnt[t] = c;
     }
     return;

@@ -139,6 +139,7 @@ struct Ctrl {
   u32 k6_count;
   u32 small_done;  // finish_small wrote the answer
   u32 nT;          // class-T records (tie-only, counted by K4T)
+  u32 nTslots;     // T-list slots handed out by K3 (>= nT for beta 2: C entries leave holes)
   u32 k4t_ticket;
   ull k4t_eq_done; // ties of the word chunks K4T has completed
   // emit and sort of the answer
