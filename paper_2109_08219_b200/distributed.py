@@ -213,10 +213,24 @@ class ShardedTopK:
     device top-k of the concatenation (direct radix path of the same library),
     whose positions map back to global indices.  Rank order is global index
     order, so the tie rule (lowest index first) holds across ranks.
+
+    ``merge="select"`` (the default for k_local > 2^16 on more than one rank,
+    SURVEY.md section 8e step 5) replaces the all_gather of world*k pairs by a
+    distributed radix select over the candidates: three all_reduce(SUM) rounds
+    of a 2048-bin histogram (digits 11/11/10 bits of the order key) find the
+    global kth key and how many of its ties are taken; one all_gather of the
+    per-rank (above, equal) counts gives every rank its exact contribution
+    (its first above_r + take_r pairs, take_r assigned in rank = index order)
+    and its offset; an all_reduce(SUM) of two zeroed k-slot buffers, each
+    rank writing only its own slots, assembles exactly k pairs, which one
+    device radix sort orders.  Collective bytes per rank: ~12k instead of
+    12*world*k, and the final sort is over k keys instead of world*k.
+    Every step stays on the device (no host synchronisation).
     """
 
     def __init__(self, shard: torch.Tensor, n_total: int, k: int, cfg: PipelineConfig | None = None, *,
-                 group=None, index_offset: int | None = None, exchange_theta: bool = True):
+                 group=None, index_offset: int | None = None, exchange_theta: bool = True,
+                 merge: str = "auto"):
         from . import _device, _native
         from .pipeline import DrTopK
 
@@ -258,6 +272,20 @@ class ShardedTopK:
         self.cat_val = torch.empty(self.cat_n, dtype=torch.int32, device=dev)
         self.cat_idx = torch.empty(self.cat_n, dtype=torch.int64, device=dev)
         self.j = torch.arange(kl, dtype=torch.int64, device=dev).view(1, kl)
+        if merge == "auto":
+            merge = "select" if w > 1 and kl > (1 << 16) else "gather"
+        if merge not in ("gather", "select"):
+            raise ValueError(f"unknown merge {merge!r}")
+        self.merge_mode = merge
+        if merge == "select":
+            self.cat_n = self.k  # the assembled answer, sorted by the merge plan
+            self.g_cnt = torch.empty(2 * w, dtype=torch.int64, device=dev)
+            self.hist = torch.empty(_SEL_BINS, dtype=torch.int64, device=dev)
+            self.sel_val = torch.empty(self.k + 1, dtype=torch.int32, device=dev)  # slot k: sink for unused pairs
+            self.sel_idx = torch.empty(self.k + 1, dtype=torch.int64, device=dev)
+            self.cat_val = self.sel_val[: self.k]
+            self.cat_idx = self.sel_idx[: self.k]
+            self.zero1 = torch.zeros(1, dtype=torch.int64, device=dev)
         self.merge = DrTopK(self.cat_n, PipelineConfig(k=self.k, alpha=0, auto_alpha=False, largest=self.lcfg.largest),
                             dv.code, dv.out_dtype, dev, timed=False)
         self.values = self.merge.values
@@ -284,6 +312,9 @@ class ShardedTopK:
                 self.index_offset, p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None), "dtopk_select_finish")
         kl = self.k_local
         cnt = self.kout.clamp(max=kl) if not c.direct_fallback else torch.full_like(self.kout, kl)
+        if self.merge_mode == "select":
+            self._select_merge(cnt, s)
+            return
         _all_gather_flat(self.g_cnt, cnt, self.group)
         _all_gather_flat(self.g_val, p.values.view(torch.int32)[:kl], self.group)
         _all_gather_flat(self.g_idx, p.indices[:kl], self.group)
@@ -301,17 +332,71 @@ class ShardedTopK:
         self.merge.launch(self.cat_val.view(self.values.dtype), s)
         torch.index_select(self.cat_idx, 0, self.merge.indices, out=self.indices)
 
+    def _select_merge(self, cnt: torch.Tensor, s) -> None:
+        """Distributed radix select + exact-k assembly (class docstring)."""
+        p, kl, k = self.local, self.k_local, self.k
+        bits = p.values.view(torch.int32)[:kl]
+        key = _order_key(bits, self.dv.code, self.lcfg.largest)
+        jj = self.j.view(-1)
+        valid = jj < cnt
+        prefix = self.zero1.clone()
+        rem = torch.full_like(self.zero1, k)
+        for shift, nb in _SEL_DIGITS:
+            digit = (key >> shift) & ((1 << nb) - 1)
+            match = valid & ((key >> (shift + nb)) == prefix)
+            self.hist.zero_().scatter_add_(0, digit, match.to(torch.int64))
+            dist.all_reduce(self.hist, op=dist.ReduceOp.SUM, group=self.group)
+            # at_least[d] = #candidates (all ranks) in this prefix with digit >= d
+            at_least = torch.cat([self.hist.flip(0).cumsum(0).flip(0), self.zero1])
+            d = (at_least[:-1] >= rem).sum(0, keepdim=True) - 1
+            rem = rem - at_least.index_select(0, d + 1)
+            prefix = (prefix << nb) | d
+        kth = prefix
+        gt = (valid & (key > kth)).sum(0, keepdim=True)
+        eq = (valid & (key == kth)).sum(0, keepdim=True)
+        _all_gather_flat(self.g_cnt, torch.cat([gt, eq]), self.group)
+        g = self.g_cnt.view(-1, 2)
+        eq_before = torch.cumsum(g[:, 1], 0) - g[:, 1]
+        take = torch.minimum(torch.clamp(rem - eq_before, min=0), g[:, 1])
+        contrib = g[:, 0] + take
+        pre = torch.cumsum(contrib, 0) - contrib
+        mine = contrib[self.rank]
+        dest = torch.where(jj < mine, pre[self.rank] + jj, torch.full_like(jj, k))
+        self.sel_val.zero_().scatter_(0, dest, bits)
+        self.sel_idx.zero_().scatter_(0, dest, p.indices[:kl])
+        dist.all_reduce(self.sel_val, op=dist.ReduceOp.SUM, group=self.group)
+        dist.all_reduce(self.sel_idx, op=dist.ReduceOp.SUM, group=self.group)
+        self.merge.launch(self.cat_val.view(self.values.dtype), s)
+        torch.index_select(self.cat_idx, 0, self.merge.indices, out=self.indices)
+
     def result(self) -> TopKResult:
         """Synchronise and wrap the last step's answer (reads the merge header)."""
         from .core import WorkloadStats as _WS
 
         hdr = self.merge.header()
         stats = _WS()
-        stats.device = {"gathered_pairs": int(self.g_cnt.sum().item()), "theta_global": int(self.theta.item())}
+        pairs = self.k if self.merge_mode == "select" else int(self.g_cnt.sum().item())
+        stats.device = {"merge": self.merge_mode, "gathered_pairs": pairs, "theta_global": int(self.theta.item())}
         from . import _device
 
         thr = _device.key_to_value(int(hdr.kth_key), self.dv.code, self.lcfg.largest)
         return TopKResult(values=self.values, threshold=thr, stats=stats, indices=self.indices)
+
+
+_SEL_BINS = 2048
+_SEL_DIGITS = ((21, 11), (10, 11), (0, 10))  # (shift, bits) of the 32-bit order key, most significant first
+
+
+def _order_key(bits: torch.Tensor, code: int, largest: bool) -> torch.Tensor:
+    """int32 raw bits of u32/f32 values -> int64 order key in [0, 2^32), larger = better."""
+    from . import _native
+
+    kk = bits.to(torch.int64) & 0xFFFFFFFF
+    if code == _native.DTYPE_F32:
+        kk = torch.where(kk >> 31 == 1, kk ^ 0xFFFFFFFF, kk | 0x80000000)
+    if not largest:
+        kk = 0xFFFFFFFF - kk
+    return kk
 
 
 def _all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group) -> None:

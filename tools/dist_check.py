@@ -26,7 +26,9 @@ dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
 ok = True
 for dist_name, n_local, k, largest in [("uniform", 1 << 22, 1000, True), ("uniform", (1 << 22) + 37, 70000, True),
                                        ("few_distinct", 1 << 21, 5000, True), ("all_equal", 1 << 21, 3000, False),
-                                       ("normal_f32", 1 << 22, 4096, True), ("uniform", 1 << 20, 1 << 19, True)]:
+                                       ("normal_f32", 1 << 22, 4096, True), ("uniform", 1 << 20, 1 << 19, True),
+                                       ("all_equal", 1 << 20, 1 << 18, True), ("few_distinct", 1 << 20, 300001, False),
+                                       ("normal_f32", (1 << 20) + 5, 1 << 17, False)]:
     n_total = n_local * world
     full = data.generate(dist_name, n_total, seed=7, device=dev)
     lo, ln = dtopk.shard_bounds(n_total, world, rank)
@@ -36,6 +38,11 @@ for dist_name, n_local, k, largest in [("uniform", 1 << 22, 1000, True), ("unifo
     for _ in range(2):
         st.step()
     r = st.result()
+    other = "select" if st.merge_mode == "gather" else "gather"
+    st3 = dtopk.ShardedTopK(shard, n_total, k, cfg, merge=other)
+    for _ in range(2):
+        st3.step()
+    r3 = st3.result()
     r2 = dtopk.sharded_topk(shard, n_total, k, cfg)
     torch.cuda.synchronize()
     if rank == 0:
@@ -44,12 +51,13 @@ for dist_name, n_local, k, largest in [("uniform", 1 << 22, 1000, True), ("unifo
         host = full.cpu().numpy()
         keys = oracle.to_keys(host, largest)
         ek, ei = oracle.topk_with_indices(keys, k)
-        for name, res in (("ShardedTopK", r), ("sharded_topk", r2)):
+        for name, res in ((f"ShardedTopK/{st.merge_mode}", r), (f"ShardedTopK/{other}", r3),
+                          ("sharded_topk", r2)):
             gi = res.indices.cpu().numpy()
             gv = res.values.cpu().numpy()
             good = np.array_equal(gi, ei) and np.array_equal(oracle.to_keys(gv, largest), ek)
             ok &= good
-            print(f"{name:13s} {dist_name:12s} world={world} n_local={n_local} k={k} largest={largest}: "
+            print(f"{name:20s} {dist_name:12s} world={world} n_local={n_local} k={k} largest={largest}: "
                   f"{'OK' if good else 'MISMATCH'}", flush=True)
 dist.barrier()
 dist.destroy_process_group()
