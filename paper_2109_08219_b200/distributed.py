@@ -285,7 +285,6 @@ class ShardedTopK:
             self.sel_idx = torch.empty(self.k + 1, dtype=torch.int64, device=dev)
             self.cat_val = self.sel_val[: self.k]
             self.cat_idx = self.sel_idx[: self.k]
-            self.zero1 = torch.zeros(1, dtype=torch.int64, device=dev)
         self.merge = DrTopK(self.cat_n, PipelineConfig(k=self.k, alpha=0, auto_alpha=False, largest=self.lcfg.largest),
                             dv.code, dv.out_dtype, dev, timed=False)
         self.values = self.merge.values
@@ -338,30 +337,8 @@ class ShardedTopK:
         bits = p.values.view(torch.int32)[:kl]
         key = _order_key(bits, self.dv.code, self.lcfg.largest)
         jj = self.j.view(-1)
-        valid = jj < cnt
-        prefix = self.zero1.clone()
-        rem = torch.full_like(self.zero1, k)
-        for shift, nb in _SEL_DIGITS:
-            digit = (key >> shift) & ((1 << nb) - 1)
-            match = valid & ((key >> (shift + nb)) == prefix)
-            self.hist.zero_().scatter_add_(0, digit, match.to(torch.int64))
-            dist.all_reduce(self.hist, op=dist.ReduceOp.SUM, group=self.group)
-            # at_least[d] = #candidates (all ranks) in this prefix with digit >= d
-            at_least = torch.cat([self.hist.flip(0).cumsum(0).flip(0), self.zero1])
-            d = (at_least[:-1] >= rem).sum(0, keepdim=True) - 1
-            rem = rem - at_least.index_select(0, d + 1)
-            prefix = (prefix << nb) | d
-        kth = prefix
-        gt = (valid & (key > kth)).sum(0, keepdim=True)
-        eq = (valid & (key == kth)).sum(0, keepdim=True)
-        _all_gather_flat(self.g_cnt, torch.cat([gt, eq]), self.group)
-        g = self.g_cnt.view(-1, 2)
-        eq_before = torch.cumsum(g[:, 1], 0) - g[:, 1]
-        take = torch.minimum(torch.clamp(rem - eq_before, min=0), g[:, 1])
-        contrib = g[:, 0] + take
-        pre = torch.cumsum(contrib, 0) - contrib
-        mine = contrib[self.rank]
-        dest = torch.where(jj < mine, pre[self.rank] + jj, torch.full_like(jj, k))
+        mine, pre = select_contribution(key, cnt, k, self.rank, self.group, self.hist, self.g_cnt)
+        dest = torch.where(jj < mine, pre + jj, torch.full_like(jj, k))
         self.sel_val.zero_().scatter_(0, dest, bits)
         self.sel_idx.zero_().scatter_(0, dest, p.indices[:kl])
         dist.all_reduce(self.sel_val, op=dist.ReduceOp.SUM, group=self.group)
@@ -385,6 +362,47 @@ class ShardedTopK:
 
 _SEL_BINS = 2048
 _SEL_DIGITS = ((21, 11), (10, 11), (0, 10))  # (shift, bits) of the 32-bit order key, most significant first
+
+
+def select_contribution(key: torch.Tensor, cnt: torch.Tensor, k: int, rank: int, group,
+                        hist: torch.Tensor | None = None, g_cnt: torch.Tensor | None = None):
+    """Distributed radix select over per-rank candidate lists (ShardedTopK merge="select").
+
+    ``key``: this rank's candidates' int64 order keys (larger = better), the
+    first ``cnt`` (int64[1] tensor) of them valid and ordered (key desc, index
+    asc); the union over ranks holds the global top-k.  Returns (mine, pre),
+    int64[1] tensors: this rank contributes its first ``mine`` candidates at
+    offset ``pre`` of the k-slot answer.  Ranks are in global index order, so
+    kth-key ties are granted to lower ranks first.  No host synchronisation.
+    """
+    dev = key.device
+    hist = torch.empty(_SEL_BINS, dtype=torch.int64, device=dev) if hist is None else hist
+    world = dist.get_world_size(group)
+    g_cnt = torch.empty(2 * world, dtype=torch.int64, device=dev) if g_cnt is None else g_cnt
+    zero1 = torch.zeros(1, dtype=torch.int64, device=dev)
+    valid = torch.arange(key.numel(), device=dev) < cnt
+    prefix = zero1.clone()
+    rem = torch.full_like(zero1, k)
+    for shift, nb in _SEL_DIGITS:
+        digit = (key >> shift) & ((1 << nb) - 1)
+        match = valid & ((key >> (shift + nb)) == prefix)
+        hist.zero_().scatter_add_(0, digit, match.to(torch.int64))
+        dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+        # at_least[d] = #candidates (all ranks) under this prefix with digit >= d
+        at_least = torch.cat([hist.flip(0).cumsum(0).flip(0), zero1])
+        d = (at_least[:-1] >= rem).sum(0, keepdim=True) - 1
+        rem = rem - at_least.index_select(0, d + 1)
+        prefix = (prefix << nb) | d
+    kth = prefix
+    gt = (valid & (key > kth)).sum(0, keepdim=True)
+    eq = (valid & (key == kth)).sum(0, keepdim=True)
+    _all_gather_flat(g_cnt, torch.cat([gt, eq]), group)
+    g = g_cnt.view(-1, 2)
+    eq_before = torch.cumsum(g[:, 1], 0) - g[:, 1]
+    take = torch.minimum(torch.clamp(rem - eq_before, min=0), g[:, 1])
+    contrib = g[:, 0] + take
+    pre = torch.cumsum(contrib, 0) - contrib
+    return contrib[rank:rank + 1], pre[rank:rank + 1]
 
 
 def _order_key(bits: torch.Tensor, code: int, largest: bool) -> torch.Tensor:

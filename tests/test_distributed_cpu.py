@@ -92,3 +92,64 @@ def test_sharded_topk_gloo_world2(exchange, seed, k, oracle_mod):
     # the theta exchange can only shrink what is gathered
     if exchange:
         assert out[0][2]["theta_global"] >= 0
+
+
+def _select_worker(rank, world, port, n, k, seed, out):
+    """ShardedTopK merge="select" arithmetic on CPU tensors: per-rank candidate
+    lists (shard top-k, garbage past the count) -> select_contribution ->
+    all_reduce assembly of exactly k pairs -> stable order."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from oracle import oracle
+
+        import paper_2109_08219_b200 as dtopk
+        from paper_2109_08219_b200.distributed import select_contribution
+
+        v = oracle.generate_uniform(n, seed=seed) if seed >= 0 else (np.arange(n, dtype=np.uint32) % 13) << 28
+        lo, ln = dtopk.shard_bounds(n, world, rank)
+        sh = v[lo:lo + ln]
+        kl = min(k, ln)
+        # odd ranks hold fewer than kl valid pairs (a theta* cut): never below what the global top-k needs here
+        _, gi = oracle.topk_with_indices(v, k)
+        need = int(((gi >= lo) & (gi < lo + ln)).sum())
+        cnt = max(need, kl - (rank % 2))
+        order = np.lexsort((np.arange(ln), ~sh))[:cnt]
+        key = np.full(kl, 0xFFFFFFFF, dtype=np.int64)  # garbage past cnt must be ignored
+        key[:cnt] = sh[order]
+        idx = np.full(kl, -7, dtype=np.int64)
+        idx[:cnt] = order + lo
+        key_t, idx_t = torch.from_numpy(key), torch.from_numpy(idx)
+        mine, pre = select_contribution(key_t, torch.tensor([cnt]), k, rank, None)
+        j = torch.arange(kl)
+        dest = torch.where(j < mine, pre + j, torch.full_like(j, k))
+        vals = torch.zeros(k + 1, dtype=torch.int64).scatter_(0, dest, key_t)
+        ids = torch.zeros(k + 1, dtype=torch.int64).scatter_(0, dest, idx_t)
+        dist.all_reduce(vals)
+        dist.all_reduce(ids)
+        vals, ids = vals[:k], ids[:k]
+        o = torch.sort(vals, descending=True, stable=True).indices
+        out[rank] = (vals[o].numpy().astype(np.uint32), ids[o].numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("seed,k", [(8, 5000), (9, 1), (-1, 4000)])
+def test_select_merge_gloo(world, seed, k, oracle_mod):
+    n = 30_011
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.start_processes(_select_worker, args=(world, port, n, k, seed, out), nprocs=world, join=True,
+                       start_method="spawn")
+    v = oracle_mod.generate_uniform(n, seed=seed) if seed >= 0 else (np.arange(n, dtype=np.uint32) % 13) << 28
+    ek, ei = oracle_mod.topk_with_indices(v, k)
+    for r in range(world):
+        vals, idx = out[r]
+        np.testing.assert_array_equal(idx, ei)
+        np.testing.assert_array_equal(vals, ek)
