@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, SortBufs b, int 
 #define DTOPK_BK_TARGET 1024
 #endif
 #ifndef DTOPK_BK_SUB_BITS
-#define DTOPK_BK_SUB_BITS 11
+#define DTOPK_BK_SUB_BITS 10
 #endif
 constexpr int BK_MAX = 4096;      // buckets
 constexpr int BK_CHUNKS = DTOPK_BK_CHUNKS;    // count / scatter CTAs
