@@ -421,10 +421,10 @@ __global__ void __launch_bounds__(256) sort_scatter(Ctrl* ctrl, SortBufs b, int 
 // A bucket above BK_CAP (skewed keys) sends the sort to the LSD radix sort.
 // ---------------------------------------------------------------------------
 #ifndef DTOPK_BK_CHUNKS
-#define DTOPK_BK_CHUNKS 64
+#define DTOPK_BK_CHUNKS 128
 #endif
 #ifndef DTOPK_BK_TARGET
-#define DTOPK_BK_TARGET 1024
+#define DTOPK_BK_TARGET 2048
 #endif
 #ifndef DTOPK_BK_SUB_BITS
 #define DTOPK_BK_SUB_BITS 10
