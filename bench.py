@@ -125,30 +125,48 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_baseline(k: int, log2n: int):
-    """Oracle port (C restatement of pipeline.dr_topk) on 1 host core, bounded sample."""
+def cpu_baseline(k: int, log2n: int, gpu_values=None, gpu_stats=None):
+    """Oracle port (C restatement of pipeline.dr_topk) on 1 host core, timed on
+    the SAME bytes as the GPU step (host twin of the device generator, seed 0):
+    the full 2^30 workload, repeated for >= 10 s.  Also the checker of the
+    timed GPU answer: the reference counters of both skip_last settings are
+    reported beside the device's ("side by side")."""
     from oracle import oracle
 
     oracle.build()
-    ns = 1 << min(log2n, 28)
-    v = oracle.generate_uniform(ns, seed=0)
-    alpha = oracle.auto_alpha(ns, k)
-    oracle.dr_topk(v, k, alpha, 2)  # warm
+    n = 1 << log2n
+    v = oracle.generate_uniform(n, seed=0)
+    alpha = oracle.auto_alpha(n, k)
+    ov0, st0 = oracle.dr_topk(v, k, alpha, 2, skip_last=False)
     reps, t0 = 0, time.perf_counter()
     while reps < 3 or time.perf_counter() - t0 < 10.0:
-        oracle.dr_topk(v, k, alpha, 2)
+        ov1, st1 = oracle.dr_topk(v, k, alpha, 2)  # the reference default (skip_last_iteration=True)
         reps += 1
         if time.perf_counter() - t0 > 30.0:
             break
     dt = (time.perf_counter() - t0) / reps
-    return {
-        "value": ns / dt,
+
+    def counters(st):
+        return {"delegate_vector_len": int(st.delegate_vector_len), "fully_qualified": int(st.fully_qualified_subranges),
+                "partially_qualified": int(st.partially_qualified_subranges),
+                "concatenated_len": int(st.concatenated_len), "theta": int(st.theta),
+                "workload_ratio": (int(st.delegate_vector_len) + int(st.concatenated_len)) / n}
+
+    out = {
+        "value": n / dt,
         "unit": UNIT,
         "cores": 1,
         "kind": "port",
-        "sample": f"2^{int(math.log2(ns))} uniform u32 keys, k={k}, alpha={alpha}, beta=2, {reps} reps "
-                  f"(C restatement of pipeline.dr_topk, oracle/dtopk_oracle.c)",
+        "sample": f"the full workload on the same bytes: 2^{log2n} uniform u32 keys (splitmix64 seed 0), k={k}, "
+                  f"alpha={alpha}, beta=2, {reps} reps (C restatement of pipeline.dr_topk, oracle/dtopk_oracle.c)",
+        "reference_counters": {"skip_last_true": counters(st1), "skip_last_false": counters(st0)},
     }
+    if gpu_values is not None:
+        out["parity"] = {"values_equal_reference": bool(np.array_equal(gpu_values, ov1)),
+                         "device_counters": gpu_stats,
+                         "device_counters_equal_skip_last_false": gpu_stats == {
+                             f: out["reference_counters"]["skip_last_false"][f] for f in gpu_stats}}
+    return out
 
 
 def run_reference(args):
@@ -160,7 +178,7 @@ def run_reference(args):
 
     oracle.build()
     cores = oracle.cpu_count()
-    n = 1 << args.log2n
+    n = (1 << args.log2n) * max(1, world)  # our arm's whole-job workload: n per GPU x world
     v = oracle.generate_uniform(n, seed=0, threads=cores)
     k = args.k
     for _ in range(args.warmup):
@@ -177,7 +195,9 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (splitmix64 uniform, host-generated)",
         "impl": "reference",
-        "config": {"workload": f"BASELINE config 2: N=2^{args.log2n} uint32 uniform, k={k}, auto alpha (const 3), beta=2",
+        "config": {"workload": f"BASELINE config {'2' if world == 1 else '5'}: N=2^{int(math.log2(n))} uint32 "
+                               f"uniform, k={k}, auto alpha (const 3), beta=2 (same bytes as --impl ours: "
+                               f"splitmix64 seed 0)",
                    "n": n, "k": k},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"full workload, {args.steps} steps: oracle_dr_topk_partitioned "
@@ -188,6 +208,73 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+def time_plan(p, v, stream, reps: int, batches: int = 5) -> float:
+    """Median over `batches` of back-to-back plan replays (ms per step)."""
+    import torch
+
+    for _ in range(3):
+        p.launch(v, stream)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = []
+    for _ in range(batches):
+        a.record(stream)
+        for _ in range(reps):
+            p.launch(v, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b) / reps)
+    return statistics.median(out)
+
+
+def bench_configs(dev, stream, peak: float, args):
+    """BASELINE configs 3 (f32 normal / Pareto, beta 1-3, k=2^10), 4 (ascending,
+    all-equal, few-distinct, k=2^16) and 5 on one GPU (2^33 uniform, k=2^10 and
+    2^20): CUDA-graph plans on resident inputs (>> L2), median of 5 batches."""
+    import torch
+
+    import paper_2109_08219_b200 as dtopk
+    from paper_2109_08219_b200 import _native, data
+    from paper_2109_08219_b200.pipeline import DrTopK
+
+    n = 1 << args.log2n
+    reps = max(5, args.steps // 10)
+    cases = [(f"config3 {d} beta={b}", d, 1 << 10, b) for d in ("normal_f32", "pareto_f32") for b in (1, 2, 3)]
+    cases += [(f"config4 {d}", d, 1 << 16, 2) for d in ("ascending", "all_equal", "few_distinct")]
+    res, cur, v = [], None, None
+    for name, d, k, beta in cases:
+        if d != cur:
+            v = None
+            torch.cuda.empty_cache()
+            v = data.generate(d, n, seed=1, device=dev)
+            cur = d
+        code = _native.DTYPE_F32 if v.dtype == torch.float32 else _native.DTYPE_U32
+        p = DrTopK(n, dtopk.PipelineConfig(k=k, beta=beta), code, v.dtype, dev, timed=False, use_graph=True)
+        t = time_plan(p, v, stream, reps)
+        h = p.header()
+        res.append({"case": name, "n": n, "k": k, "alpha": p.cfg.alpha, "beta": p.cfg.beta, "ms": round(t, 4),
+                    "keys_per_s": n / (t * 1e-3), "frac_of_peak": (n * 4 / (t * 1e-3) / 1e9) / peak,
+                    "workload_ratio": (p.cfg.beta * -(-n // (1 << p.cfg.alpha)) + int(h.concatenated_len)) / n,
+                    "path": int(h.path), "pool_gt": int(h.pool_gt), "reread": int(h.elements_reread)})
+        del p
+    v = None
+    torch.cuda.empty_cache()
+    if not args.no_big:
+        nb = 1 << 33
+        v = data.generate("uniform", nb, seed=1, device=dev)
+        for k in (1 << 10, 1 << 20):
+            p = DrTopK(nb, dtopk.PipelineConfig(k=k), _native.DTYPE_U32, torch.uint32, dev, timed=False,
+                       use_graph=True)
+            t = time_plan(p, v, stream, 3, batches=3)
+            res.append({"case": "config5 2^33 uniform, one GPU", "n": nb, "k": k, "alpha": p.cfg.alpha,
+                        "beta": p.cfg.beta, "ms": round(t, 4), "keys_per_s": nb / (t * 1e-3),
+                        "frac_of_peak": (nb * 4 / (t * 1e-3) / 1e9) / peak})
+            del p
+        v = None
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     import torch
 
@@ -208,7 +295,9 @@ def run_ours(args):
     lib = _native.load()
     n = 1 << args.log2n
     k = args.k
-    v = data.generate("uniform", n, seed=1000 + rank, device=dev)
+    # the same bytes as the reference arm: the counter-based uniform generator
+    # (host twin oracle.generate_uniform), seed 0, rank r holding [r*n, (r+1)*n)
+    v = data.generate("uniform", n, seed=0, device=dev, offset=rank * n)
     torch.cuda.synchronize()
 
     def barrier():
@@ -390,6 +479,24 @@ def run_ours(args):
         out["k_sweep"] = sweep
         out["k_sweep_min_frac"] = min(s["frac_of_peak"] for s in sweep)
 
+    # ---- BASELINE configs 3-5 on one GPU (extra field, not the headline)
+    if world == 1 and not args.no_configs and rank == 0:
+        out["configs"] = bench_configs(dev, stream, peak, args)
+
+    # ---- the timed answer's reference counters (exact mode), checked in cpu_baseline
+    gpu_values = gpu_stats = None
+    if world == 1:
+        r = dtopk.dr_topk(v, cfg, exact_stats=True)
+        st = r.stats
+        gpu_values = r.values.cpu().numpy()
+        gpu_stats = {"delegate_vector_len": st.delegate_vector_len, "fully_qualified": st.fully_qualified_subranges,
+                     "partially_qualified": st.partially_qualified_subranges,
+                     "concatenated_len": st.concatenated_len, "theta": int(st.device["theta_local"]),
+                     "workload_ratio": (st.delegate_vector_len + st.concatenated_len) / n}
+        if rank == 0:
+            out["workload_ratio"] = gpu_stats["workload_ratio"]
+            out["counters"] = gpu_stats
+
     # ---- e2e through the public API with host buffers
     if not args.no_e2e:
         host = torch.empty(n, dtype=torch.uint32, pin_memory=True)
@@ -422,7 +529,7 @@ def run_ours(args):
         for h in e:
             lib.dtopk_event_destroy(h)
     if rank == 0 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(k, args.log2n)
+        out["cpu_baseline"] = cpu_baseline(k, args.log2n, gpu_values, gpu_stats)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -441,6 +548,8 @@ def main():
     ap.add_argument("--sweep-stride", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE config 3-5 extra field")
+    ap.add_argument("--no-big", action="store_true", help="skip the 2^33 single-GPU case of the configs field")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA-graph plan")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -13,6 +13,9 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 #include "assemble.cuh"
@@ -137,16 +140,34 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
 }
 
 
+// Opt a kernel into `bytes` of dynamic shared memory on the current device.
+// The attribute is per (function, device context): a process that runs on
+// cuda:0 and then cuda:1 must set it once on each, so the guard is keyed by
+// both and taken under a lock (run_distributed lanes launch concurrently).
+template <typename F>
+void ensure_smem(F* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::pair<const void*, int> key{reinterpret_cast<const void*>(fn), dev};
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(key)) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) done.insert(key);
+}
+
 int num_sms() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-  if (!cache[dev]) {
+  int c = cache[dev].load(std::memory_order_relaxed);
+  if (!c) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = v > 0 ? v : 148;
+    c = v > 0 ? v : 148;
+    cache[dev].store(c, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return c;
 }
 
 // Launch with programmatic stream serialization (PDL, see common.cuh): the
@@ -194,11 +215,7 @@ inline int key_mode(int dtype, int largest) { return (dtype == DTOPK_F32 ? 2 : 0
 // ---------------------------------------------------------------------------
 template <int MODE, int B>
 void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k1_delegates<MODE, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1_SMEM);
-    attr = true;
-  }
+  ensure_smem(k1_delegates<MODE, B>, (int)K1_SMEM);
   k1_delegates<MODE, B><<<grid_for(nch, nsm * K1_CPS), K1_THREADS, K1_SMEM, s>>>(a);
   counted();
   if (a.alpha > K1_LOG_CHUNK) {
@@ -412,11 +429,7 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
     gc->ok = gc->ok && cond_end(gc->s2);
     cs = s;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sort_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SORT * 8);
-    attr = true;
-  }
+  ensure_smem(sort_small<MODE>, SMALL_SORT * 8);
   sort_small<MODE><<<1, 1024, SMALL_SORT * 8, s>>>(ctrl, sb, reinterpret_cast<u32*>(out_values),
                                                    reinterpret_cast<long long*>(out_indices), (long long)offset);
   counted();
@@ -523,11 +536,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
                                                                       k5.d_need, k5.ties);
   counted();
   rec(ev, 3, s);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(finish_small<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_POOL * 8);
-    attr = true;
-  }
+  ensure_smem(finish_small<MODE>, SMALL_POOL * 8);
   const bool need_tail = std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL;  // pools beyond SMALL_POOL possible
   const bool cond = gc && need_tail;
   launch_pdl(finish_small<MODE>, dim3(1), dim3(1024), SMALL_POOL * 8, s, ctrl, k5.gt_keys, k5.gt_idx, k5.ties,
@@ -637,11 +646,15 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
   }
   const Layout L = direct ? make_layout(n, k, 0, 1, 1) : make_layout(n, k, alpha, beta, 0);
   if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
-  // run once eagerly: sets kernel attributes and validates the configuration
+  // Run once eagerly: sets kernel attributes and validates the configuration.
+  // The warm-up writes the workspace and reads the keys, so it must not race
+  // work the caller queued on its own (possibly non-blocking) streams, e.g. a
+  // replay of another plan sharing this workspace: drain the device first.
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_status();
   st = dtopk_select(keys, n, dtype, k, largest, alpha, beta, direct, flags, out_values, out_indices, index_offset, ws,
                     ws_bytes, nullptr, nullptr);
   if (st != DTOPK_OK) return st;
-  if (cudaStreamSynchronize(nullptr) != cudaSuccess) return cuda_status();
+  if (cudaDeviceSynchronize() != cudaSuccess) return cuda_status();
   dtopk_plan_s* p = new dtopk_plan_s();
   GraphCtx gc;
   bool ok = cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) == cudaSuccess &&

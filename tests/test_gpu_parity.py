@@ -483,13 +483,22 @@ def test_config5_single_gpu_2pow33_properties(cuda):
     assert torch.unique(idx).numel() == k
     kk = vi[idx].to(torch.int64) & 0xFFFFFFFF
     assert bool((kk[:-1] >= kk[1:]).all())
+    same = kk[:-1] == kk[1:]
+    assert bool((idx[:-1][same] < idx[1:][same]).all())
     kth = int(kk[-1])
     gt = ge = 0
+    ties = []
     for c in range(0, n, 1 << 30):
         ch = vi[c:c + (1 << 30)].to(torch.int64) & 0xFFFFFFFF
         gt += int((ch > kth).sum())
         ge += int((ch >= kth).sum())
+        ties.append(torch.nonzero(ch == kth).flatten() + c)
         del ch
     assert gt < k <= ge
+    assert int((kk > kth).sum()) == gt  # every key above the k-th is in the answer
+    # lowest-index ties first: the taken kth ties are the first ones in index order
+    taken = torch.sort(idx[kk == kth]).values
+    all_ties = torch.cat(ties)
+    assert torch.equal(taken, all_ties[: taken.numel()])
     del v, vi
     torch.cuda.empty_cache()
