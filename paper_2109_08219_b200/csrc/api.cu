@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "assemble.cuh"
 #include "delegate.cuh"
+#include "fast.cuh"
 #include "generate.cuh"
 #include "scan.cuh"
 #include "select.cuh"
@@ -255,40 +256,55 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
   }
 }
 
-template <int MODE>
-void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, const Layout& L, cudaStream_t s, int nsm,
-               void* const* ev) {
-  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
-  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
-  rec(ev, 0, s);
-  u32* D = reinterpret_cast<u32*>(ws + L.D);
-  stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm);
-  rec(ev, 1, s);
-  K2Args k2{D,
-            L.D_len,
-            k,
-            ctrl,
-            reinterpret_cast<u32*>(ws + L.selbuf),
-            reinterpret_cast<u32*>(ws + L.region_cnt),
-            L.R2,
-            beta,
-            reinterpret_cast<uint4*>(ws + L.sup_sid),
-            reinterpret_cast<u32*>(ws + L.sup_in),
-            reinterpret_cast<u32*>(ws + L.sup_cnt),
-            reinterpret_cast<u32*>(ws + L.sup_off)};
-  if (beta == 2)
-    launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
-  else
-    launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, s, k2);
-  counted();
-  launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2, k2.sup_cnt,
-                                                    reinterpret_cast<u32*>(ws + L.sup_off), D, L.D_len);
+K2Args k2_args(char* ws, const Layout& L, u64 k, int beta) {
+  return K2Args{reinterpret_cast<u32*>(ws + L.D),
+                L.D_len,
+                k,
+                reinterpret_cast<Ctrl*>(ws + L.ctrl),
+                reinterpret_cast<u32*>(ws + L.selbuf),
+                reinterpret_cast<u32*>(ws + L.region_cnt),
+                L.R2,
+                beta,
+                reinterpret_cast<uint4*>(ws + L.sup_sid),
+                reinterpret_cast<u32*>(ws + L.sup_in),
+                reinterpret_cast<u32*>(ws + L.sup_cnt),
+                reinterpret_cast<u32*>(ws + L.sup_off),
+                reinterpret_cast<const u32*>(ws + L.meta)};
+}
+
+// K2 pass 3 (theta from the bucket members) and K2b (the exact superset of a
+// large-bucket call).
+void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, int nsm) {
+  const K2Args k2 = k2_args(ws, L, k, beta);
+  launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2,
+             k2.sup_cnt, k2.sup_off, k2.D, L.D_len);
   counted();
   if (beta == 2)
     launch_pdl(k2b_superset<1>, dim3(L.g2), dim3(256), 0, s, k2);
   else
     launch_pdl(k2b_superset<0>, dim3(L.g2), dim3(256), 0, s, k2);
   counted();
+}
+
+// Delegates (K1) and the delegate scan (K2).  `fused` (a whole dtopk_select or
+// plan): theta is resolved by fast_tail, or by K2 pass 3 inside the general
+// chain when fast_tail declines.  Otherwise (dtopk_select_begin) pass 3 and K2b
+// run here, so that theta_slot holds theta when the call returns.
+template <int MODE>
+void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, const Layout& L, cudaStream_t s, int nsm,
+               void* const* ev, bool fused = false) {
+  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
+  rec(ev, 0, s);
+  u32* D = reinterpret_cast<u32*>(ws + L.D);
+  stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm);
+  rec(ev, 1, s);
+  const K2Args k2 = k2_args(ws, L, k, beta);
+  if (beta == 2)
+    launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
+  else
+    launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, s, k2);
+  counted();
+  if (!fused) theta_resolve(ws, L, k, beta, s, nsm);
   rec(ev, 2, s);
 }
 
@@ -323,8 +339,9 @@ void run_sort(Ctrl* ctrl, const SortBufs& b, const Layout& L, cudaStream_t s, in
 // LSD fallback sort, so only the stages a run needs are launched.
 struct GraphCtx {
   cudaGraph_t graph = nullptr;
-  cudaGraphConditionalHandle cond{};
-  cudaStream_t s2 = nullptr, s3 = nullptr;
+  cudaGraphConditionalHandle cond{};  // large-pool tail (set by finish_small)
+  cudaGraphConditionalHandle gen{};   // general chain K3..finish_small (set by fast_tail)
+  cudaStream_t s2 = nullptr, s3 = nullptr, s4 = nullptr, s5 = nullptr;
   unsigned long long main_kernels = 0, body_kernels = 0;
   bool ok = true;
 };
@@ -466,8 +483,50 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
 template <int MODE>
 void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, const int64_t* theta_override,
                 void* out_values, int64_t* out_indices, int64_t offset, char* ws, const Layout& L, cudaStream_t s,
-                int nsm, void* const* ev, GraphCtx* gc = nullptr) {
+                int nsm, void* const* ev, GraphCtx* gc = nullptr, bool fused = false) {
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  // fast_tail: the whole post-theta work of a small call in one CTA (fast.cuh);
+  // the general chain below runs only when it declines (graph: conditional node,
+  // eager: every chain kernel returns when ctrl->small_done is set)
+  const bool fast = alpha <= FT_MAX_ALPHA;
+  const bool g = gc != nullptr;
+  if (fast) {
+    ensure_smem(fast_tail<MODE>, (int)FT_SMEM);
+    FTArgs fa{ctrl,
+              keys,
+              n,
+              alpha,
+              beta,
+              k,
+              L.D_len,
+              reinterpret_cast<const u32*>(ws + L.D),
+              reinterpret_cast<const uint4*>(ws + L.sup_sid),
+              reinterpret_cast<const u32*>(ws + L.sup_in),
+              reinterpret_cast<const u32*>(ws + L.sup_cnt),
+              reinterpret_cast<const u32*>(ws + L.sup_off),
+              (u32)(L.g2 * 8),
+              fused ? 1 : 0,
+              reinterpret_cast<const u32*>(ws + L.selbuf),
+              reinterpret_cast<const u32*>(ws + L.region_cnt),
+              L.g2,
+              L.R2,
+              theta_override,
+              reinterpret_cast<u32*>(out_values),
+              reinterpret_cast<long long*>(out_indices),
+              (long long)offset,
+              g ? gc->gen : cudaGraphConditionalHandle{},
+              g ? 1 : 0};
+    launch_pdl(fast_tail<MODE>, dim3(1), dim3(FT_THREADS), FT_SMEM, s, fa);
+    counted();
+    if (g) {
+      gc->main_kernels = dtopk_launch_count_internal();  // always executed: K1 .. fast_tail
+      gc->ok = gc->ok && cond_begin(s, gc->gen, gc->s4);
+    }
+  }
+  cudaStream_t s_outer = s;
+  if (g && fast) s = gc->s4;  // the general chain is the body of the conditional node
+  // fused call: theta was left to fast_tail; the general chain resolves it itself
+  if (fused) theta_resolve(ws, L, k, beta, s, nsm);
   Records rc{reinterpret_cast<uint4*>(ws + L.rec)};
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
   u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);
@@ -535,50 +594,32 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   launch_pdl(k6_ties<MODE>, dim3(grid_for((L.cap_d + 7) / 8, nsm * 4)), dim3(256), 0, s, ctrl, keys, n, alpha, k5.d_sid, k5.d_pos,
                                                                       k5.d_need, k5.ties);
   counted();
-  rec(ev, 3, s);
+  rec(ev, 3, s_outer);
   ensure_smem(finish_small<MODE>, SMALL_POOL * 8);
   const bool need_tail = std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL;  // pools beyond SMALL_POOL possible
-  const bool cond = gc && need_tail;
+  const bool cond = g && need_tail;
   launch_pdl(finish_small<MODE>, dim3(1), dim3(1024), SMALL_POOL * 8, s, ctrl, k5.gt_keys, k5.gt_idx, k5.ties,
                                                      reinterpret_cast<u32*>(out_values),
                                                      reinterpret_cast<long long*>(out_indices), (long long)offset,
                                                      cond ? gc->cond : cudaGraphConditionalHandle{}, cond ? 1 : 0);
   counted();
-  if (!need_tail) {
-    rec(ev, 4, s);
-    return;
+  if (need_tail) {
+    if (!g) {
+      big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices,
+                     offset, ws, L, s, nsm);
+    } else {
+      // graph mode: the large-pool tail is the body of a conditional node set by finish_small
+      gc->ok = gc->ok && cond_begin(s, gc->cond, gc->s5);
+      big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices,
+                     offset, ws, L, gc->s5, nsm, gc);
+      gc->ok = gc->ok && cond_end(gc->s5);
+    }
   }
-  if (!gc) {
-    big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices,
-                   offset, ws, L, s, nsm);
-    rec(ev, 4, s);
-    return;
+  if (g && fast) {
+    gc->ok = gc->ok && cond_end(gc->s4);
+    gc->body_kernels = dtopk_launch_count_internal() - gc->main_kernels;  // the general chain (conditional)
   }
-  // graph mode: finish the main capture with a conditional node; capture the tail into its body
-  cudaStreamCaptureStatus cst;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t ndeps = 0;
-  cudaGraph_t cg = nullptr;
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = gc->cond;
-  cp.conditional.type = cudaGraphCondTypeIf;
-  cp.conditional.size = 1;
-  cudaGraphNode_t cnode;
-  gc->ok = gc->ok && cudaStreamGetCaptureInfo(s, &cst, nullptr, &cg, &deps, &ndeps) == cudaSuccess;
-  gc->ok = gc->ok && cudaGraphAddNode(&cnode, gc->graph, deps, ndeps, &cp) == cudaSuccess;
-  gc->ok = gc->ok && cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies) == cudaSuccess;
-  cudaGraph_t done = nullptr;
-  gc->ok = gc->ok && cudaStreamEndCapture(s, &done) == cudaSuccess;
-  gc->main_kernels = dtopk_launch_count_internal();
-  gc->ok = gc->ok &&
-           cudaStreamBeginCaptureToGraph(s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                         cudaStreamCaptureModeRelaxed) == cudaSuccess;
-  big_tail<MODE>(k, k5.gt_keys, k5.gt_idx, (const ull*)&ctrl->res.pool_gt, 0, 0, out_values, out_indices, offset,
-                 ws, L, s, nsm, gc);
-  cudaGraph_t body = nullptr;
-  gc->ok = gc->ok && cudaStreamEndCapture(s, &body) == cudaSuccess;
-  gc->body_kernels = dtopk_launch_count_internal() - gc->main_kernels;
+  rec(ev, 4, s_outer);
 }
 
 template <int MODE>
@@ -660,8 +701,11 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
   bool ok = cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&gc.s2, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&gc.s3, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&gc.s4, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&gc.s5, cudaStreamNonBlocking) == cudaSuccess &&
             cudaGraphCreate(&p->graph, 0) == cudaSuccess &&
             cudaGraphConditionalHandleCreate(&gc.cond, p->graph, 0, cudaGraphCondAssignDefault) == cudaSuccess &&
+            cudaGraphConditionalHandleCreate(&gc.gen, p->graph, 1, cudaGraphCondAssignDefault) == cudaSuccess &&
             cudaStreamBeginCaptureToGraph(p->cap, p->graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
                 cudaSuccess;
   if (ok) {
@@ -671,27 +715,24 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
     const u32* kp = reinterpret_cast<const u32*>(keys);
     char* w = reinterpret_cast<char*>(ws);
     cudaStream_t s = p->cap;
-    bool captured_tail = false;
     if (direct) {
       DISPATCH_MODE(key_mode(dtype, largest), run_direct, kp, n, k, out_values, out_indices, index_offset, w, L, s,
                     nsm, nullptr);
     } else {
-      DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, nullptr);
+      const bool fused = alpha <= FT_MAX_ALPHA;
+      DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, nullptr, fused);
       DISPATCH_MODE(key_mode(dtype, largest), run_finish, kp, n, k, alpha, beta, flags, nullptr, out_values,
-                    out_indices, index_offset, w, L, s, nsm, nullptr, &gc);
-      captured_tail = gc.main_kernels != 0;
+                    out_indices, index_offset, w, L, s, nsm, nullptr, &gc, fused);
     }
-    if (!captured_tail) {
-      cudaGraph_t g = nullptr;
-      ok = cudaStreamEndCapture(s, &g) == cudaSuccess;
-      gc.main_kernels = t_launches;
-    }
+    cudaGraph_t g = nullptr;
+    ok = cudaStreamEndCapture(s, &g) == cudaSuccess;
+    if (gc.main_kernels == 0) gc.main_kernels = t_launches;
     ok = ok && gc.ok && cap_ok(cudaGraphInstantiate(&p->exec, p->graph, 0), "instantiate");
     p->main_kernels = gc.main_kernels;
     p->body_kernels = gc.body_kernels;
   }
-  if (gc.s2) cudaStreamDestroy(gc.s2);
-  if (gc.s3) cudaStreamDestroy(gc.s3);
+  for (cudaStream_t x : {gc.s2, gc.s3, gc.s4, gc.s5})
+    if (x) cudaStreamDestroy(x);
   if (!ok) {
     cudaGetLastError();
     dtopk_plan_destroy(p);
@@ -811,10 +852,19 @@ dtopk_status dtopk_select(const void* keys, uint64_t n, int dtype, uint64_t k, i
                   stage_events);
     return cuda_status();
   }
-  st = dtopk_select_begin(keys, n, dtype, k, largest, alpha, beta, flags, ws, ws_bytes, stream, stage_events);
-  if (st != DTOPK_OK) return st;
-  return dtopk_select_finish(keys, n, dtype, k, largest, alpha, beta, flags, nullptr, out_values, out_indices,
-                             index_offset, ws, ws_bytes, stream, stage_events);
+  if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
+  if ((u64)beta * ((n + (1ull << alpha) - 1) >> alpha) < k) return DTOPK_INVALID_K;
+  const Layout L = make_layout(n, k, alpha, beta, 0);
+  if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nsm = num_sms();
+  const u32* kp = reinterpret_cast<const u32*>(keys);
+  char* w = reinterpret_cast<char*>(ws);
+  const bool fused = alpha <= FT_MAX_ALPHA;
+  DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, stage_events, fused);
+  DISPATCH_MODE(key_mode(dtype, largest), run_finish, kp, n, k, alpha, beta, flags, nullptr, out_values, out_indices,
+                index_offset, w, L, s, nsm, stage_events, nullptr, fused);
+  return cuda_status();
 }
 
 dtopk_status dtopk_extract_delegates(const void* keys, uint64_t n, int dtype, int largest, int alpha, int beta,

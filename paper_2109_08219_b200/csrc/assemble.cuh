@@ -72,7 +72,7 @@ struct K3Args {
   Ctrl* ctrl;
   const int64_t* theta_override;
   Records rec;          // [sup_total] one record per superset entry, subrange order
-  const uint4* sup_sid;  // K2 superset: {sid, d_1, d_2, d_beta} (beta 2) or {sid, d_1, -, -}, per segment
+  const uint4* sup_sid;  // K2 superset: {sid, d_1, d_2, meta} (beta 2) or {sid, d_1, -, meta}, per segment
   const u32* sup_in;    // [nseg] first superset slot of each segment
   const u32* sup_off;   // [nseg + 1] first record of each segment (K2 pass 3)
   u64 nseg;
@@ -108,6 +108,7 @@ __device__ __forceinline__ u32 classify(u32 d1, u32 d2, u32 m, u32 theta, int be
 __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
   pdl_trigger();
   pdl_wait();
+  if (ld_volatile_u32(&a.ctrl->small_done)) return;  // finished by fast_tail
   __shared__ ull s_stat[4][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
@@ -164,18 +165,15 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
         sid[u] = e.x;
         d1[u] = e.y;
         d2[u] = e.z;
-        dl[u] = e.w;
+        dl[u] = e.z;  // beta 2: d_beta = d_2
+        m[u] = e.w;   // K1 meta, copied by K2
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const u32 j = j0 + u * 32 + lane;
-        m[u] = 0;
-        if (j < cnt && d1[u] >= theta) {  // D and meta gathered for qualifying entries only
-          if (beta != 2) {
-            d2[u] = beta >= 2 ? a.D[(u64)sid[u] * beta + 1] : d1[u];
-            dl[u] = a.D[(u64)sid[u] * beta + beta - 1];
-          }
-          m[u] = a.meta[sid[u]];
+        if (j < cnt && d1[u] >= theta && beta != 2) {  // D gathered for qualifying entries only
+          d2[u] = beta >= 2 ? a.D[(u64)sid[u] * beta + 1] : d1[u];
+          dl[u] = a.D[(u64)sid[u] * beta + beta - 1];
         }
       }
 #pragma unroll
@@ -279,6 +277,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k4_read(K4Args a) {
   pdl_trigger();
   pdl_wait();
+  if (ld_volatile_u32(&a.ctrl->small_done)) return;  // finished by fast_tail
   __shared__ u32 s_wg[8], s_we[8];
   __shared__ u32 s_seg_g[K4_TILE / 4], s_seg_e[K4_TILE / 4];
   __shared__ u32 s_max[8];
@@ -502,6 +501,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
   pdl_trigger();
   pdl_wait();
+  if (ld_volatile_u32(&a.ctrl->small_done)) return;  // finished by fast_tail
   __shared__ u64 s_chunk;
   __shared__ u32 s_eq[8];
   Ctrl* ctrl = a.ctrl;
@@ -652,6 +652,7 @@ __device__ __forceinline__ void k5_tile_counts(const K5Args& a, u64 i0, u64 tota
 __global__ void __launch_bounds__(256) k5_count(K5Args a) {
   pdl_trigger();
   pdl_wait();
+  if (ld_volatile_u32(&a.ctrl->small_done)) return;  // finished by fast_tail
   __shared__ u64 scratch_g[8], scratch_e[8];
   __shared__ ull s_cc[8];
   __shared__ int am_last;
@@ -746,6 +747,7 @@ __global__ void __launch_bounds__(256) k5_count(K5Args a) {
 __global__ void __launch_bounds__(256, DTOPK_K5E_MINB) k5_emit(K5Args a) {
   pdl_trigger();
   pdl_wait();
+  if (ld_volatile_u32(&a.ctrl->small_done)) return;  // finished by fast_tail
   __shared__ u64 scratch_g[8], scratch_e[8];
   const int tid = threadIdx.x;
   Ctrl* ctrl = a.ctrl;
@@ -809,6 +811,7 @@ __global__ void __launch_bounds__(256) k5b_copy(Ctrl* ctrl, int alpha, u64 k, co
                                                 u64* __restrict__ gt_idx, u64* __restrict__ ties) {
   pdl_trigger();
   pdl_wait();
+  if (ld_volatile_u32(&ctrl->small_done)) return;  // finished by fast_tail
   const int lane = threadIdx.x & 31;
   const u64 nE = min((u64)ctrl->nE, cap_e);
   const int lseg = alpha < 13 ? alpha : 13;
@@ -844,6 +847,7 @@ __global__ void __launch_bounds__(256) k6_ties(Ctrl* ctrl, const u32* __restrict
                                                const u32* __restrict__ d_need, u64* __restrict__ ties) {
   pdl_trigger();
   pdl_wait();
+  if (ld_volatile_u32(&ctrl->small_done)) return;  // finished by fast_tail
   const int lane = threadIdx.x & 31;
   const u32 theta = ctrl->res.theta;
   const u32 cnt = ctrl->k6_count;
@@ -1008,6 +1012,10 @@ __global__ void __launch_bounds__(1024) finish_small(Ctrl* ctrl, const u32* __re
   pdl_trigger();
   pdl_wait();
   extern __shared__ unsigned long long sk[];
+  if (ld_volatile_u32(&ctrl->small_done)) {  // finished by fast_tail
+    if (use_cond && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+    return;
+  }
   const u32 path = ctrl->res.path;
   const u64 G = ctrl->res.pool_gt;
   const u64 m = path == PATH_SELECT ? G : ctrl->res.k_out;

@@ -201,6 +201,22 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, u32 byte
       : "memory");
 }
 
+// The same copy with an L2 cache-policy hint (createpolicy): K1 streams the
+// whole input once, so its lines are marked evict_first and do not push the
+// delegates, the workspace and the kernels' code out of the 126 MB L2.
+__device__ __forceinline__ u64 l2_policy_evict_first() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, u32 bytes, u64* bar, u64 policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
 // Bulk prefetch of global memory into L2 (no shared-memory destination).
 __device__ __forceinline__ void l2_prefetch_bulk(const void* src, u32 bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -339,6 +355,36 @@ __device__ void find_digit(const ull* hist, ull k_rem, DigitResult* out, ull* sc
   }
 #pragma unroll
   for (int i = 0; i < PER; i++) sum += loc[i];
+  if (t == 0) out->valid = 0;
+  const ull incl = block_incl_scan_256<ull>(sum, scratch);
+  ull run = incl - sum;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int b = NB - 1 - (t * PER + i);
+    if (run < k_rem && run + loc[i] >= k_rem) {
+      out->digit = (u32)b;
+      out->rem = k_rem - run;
+      out->cnt = loc[i];
+      out->above = run;
+      out->valid = 1;
+    }
+    run += loc[i];
+  }
+  __syncthreads();
+}
+
+// find_digit over a shared-memory u32 histogram (same contract as find_digit).
+template <int NB>
+__device__ void find_digit_sm(const u32* sh, ull k_rem, DigitResult* out, ull* scratch) {
+  constexpr int PER = NB / 256;
+  const int t = threadIdx.x;
+  u32 loc[PER];
+  ull sum = 0;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    loc[i] = sh[NB - 1 - (t * PER + i)];
+    sum += loc[i];
+  }
   if (t == 0) out->valid = 0;
   const ull incl = block_incl_scan_256<ull>(sum, scratch);
   ull run = incl - sum;

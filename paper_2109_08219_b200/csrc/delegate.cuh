@@ -407,6 +407,10 @@ __device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stag
   k1_warp_chunk<MODE, B, true>(a, stage, c, shist, nullptr);
 }
 
+#ifndef DTOPK_K1_EVICT_FIRST
+#define DTOPK_K1_EVICT_FIRST 1  // K1's input stream is marked L2 evict_first
+#endif
+
 template <int MODE, int B>
 __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   pdl_trigger();
@@ -433,6 +437,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   if (warp == K1_CWARPS) {
     if (lane == 0) {
       u64 i = 0;
+      const u64 pol = l2_policy_evict_first();
       for (u64 c = blockIdx.x; c < nch; c += gridDim.x, i++) {
         const u32 s = (u32)(i % K1_STAGES);
         const u32 ph = (u32)(i / K1_STAGES) & 1u;
@@ -446,7 +451,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
         }
         if (bytes) {
           mbar_arrive_expect_tx(&full[s], bytes);
-          tma_load_1d(stages + (size_t)s * K1_CHUNK, a.keys + start, bytes, &full[s]);
+          if constexpr (DTOPK_K1_EVICT_FIRST)
+            tma_load_1d_hint(stages + (size_t)s * K1_CHUNK, a.keys + start, bytes, &full[s], pol);
+          else
+            tma_load_1d(stages + (size_t)s * K1_CHUNK, a.keys + start, bytes, &full[s]);
         } else {
           mbar_arrive(&full[s]);
         }

@@ -27,10 +27,11 @@ struct K2Args {
   // candidate superset (delegate path): subranges whose max delegate lies in
   // theta's top-11-bit bucket or above, in subrange order per warp segment
   int beta;
-  uint4* sup_sid;  // [S] {sid, d_1, d_2, d_beta} (beta 2; else {sid, d_1, 0, 0}): segment (cta, warp) from sup_in[seg]
+  uint4* sup_sid;  // [S] {sid, d_1, d_2, meta} (beta 2; else {sid, d_1, 0, meta}): segment (cta, warp) from sup_in[seg]
   u32* sup_in;   // [g2 * 8] first slot of each segment
   u32* sup_cnt;  // [g2 * 8] entries of each segment
   u32* sup_off;  // [g2 * 8 + 1] exclusive prefix of sup_cnt (theta resolver)
+  const u32* meta;  // [S] K1 meta words, copied into the superset entries
 };
 
 #ifndef DTOPK_K2_MINB
@@ -76,13 +77,17 @@ __device__ void k2_superset_prefix(Ctrl* ctrl, u32 nregions, const u32* __restri
   }
 }
 
-// Resolve theta from the digit-3 histogram (ctrl->selD.hist3) and publish the
-// exclusive prefix of the superset segment counts.  One CTA (256 threads).
+// Resolve theta from the digit-3 histogram (ctrl->selD.hist3, or the CTA's
+// shared-memory histogram when `sh3` is set) and publish the exclusive prefix
+// of the superset segment counts.  One CTA (256 threads).
 __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, const DigitResult& r2, u32 nregions,
                                  const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off, DigitResult* r3,
-                                 ull* scratch, u64 nD) {
+                                 ull* scratch, u64 nD, const u32* sh3 = nullptr) {
   const int tid = threadIdx.x;
-  find_digit<NBD3>(ctrl->selD.hist3, r2.rem, r3, scratch);
+  if (sh3)
+    find_digit_sm<NBD3>(sh3, r2.rem, r3, scratch);
+  else
+    find_digit<NBD3>(ctrl->selD.hist3, r2.rem, r3, scratch);
   if (tid == 0) {
     const u32 kth = kmin + (r2.digit << DSH3) + r3->digit;
     ctrl->selD.r3 = *r3;
@@ -189,7 +194,8 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
           if ((mc >> j) & 1u) {
             // beta 2: (d1, d2) sit in this lane's registers (pairs start at even j)
             const u32 d2 = BETA2 ? v[j | 1] : 0u;
-            a.sup_sid[o++] = make_uint4((u32)((i0 + j) / beta), v[j], d2, d2);
+            const u32 sid = (u32)((i0 + j) / beta);
+            a.sup_sid[o++] = make_uint4(sid, v[j], d2, __ldg(a.meta + sid));
           }
         }
       }
@@ -227,6 +233,10 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
   }
 }
 
+constexpr int P3_SMALL = 8192;   // bucket members resolved by one CTA
+constexpr int P3_RPT = 3;        // regions per thread in that CTA's prefix
+constexpr int P3_REGIONS = 256 * P3_RPT;
+
 // Pass 3 of kth(D) over the compacted bucket regions;
 // the last CTA resolves theta and the superset record offsets.
 __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
@@ -239,15 +249,66 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   __shared__ DigitResult r3;
   __shared__ ull scratch[8];
   __shared__ int am_last;
+  __shared__ u32 s_rcnt[P3_REGIONS];
   const int tid = threadIdx.x;
-  for (int i = tid; i < NBD3; i += 256) shist[i] = 0;
   __shared__ DigitResult r2;
+  if (ld_volatile_u32(&ctrl->small_done)) return;  // fast_tail resolved theta and finished the call
   const DigitResult r1 = ctrl->selD.r1;
+  // a small compacted bucket (small k): one CTA resolves theta from the members
+  // directly, without the grid-wide histogram flush and last-CTA hand-off
+  const bool small = r1.cnt * 4 <= nD && r1.cnt <= (ull)P3_SMALL && nregions <= (u32)P3_REGIONS;
+  if (small && blockIdx.x != 0) return;
+  for (int i = tid; i < NBD3; i += 256) shist[i] = 0;
   u32 kmin, kmax;
   dbucket_range(r1.digit, kmin, kmax);
   find_digit<NBD2>(ctrl->selD.hist2, r1.rem, &r2, scratch);
   if (blockIdx.x == 0 && tid == 0) ctrl->selD.r2 = r2;
   const u32 b2 = r2.digit;
+  if (small) {
+    // region counts -> exclusive prefix (thread t owns regions t*P3_RPT ..), then
+    // a flat loop over the members: member i lives in the region whose prefix
+    // interval holds i (binary search in shared memory)
+    u32 c[P3_RPT], sum = 0;
+#pragma unroll
+    for (int q = 0; q < P3_RPT; q++) {
+      const u32 g = (u32)tid * P3_RPT + q;
+      c[q] = g < nregions ? region_cnt[g] : 0u;
+      sum += c[q];
+    }
+    const u32 incl = block_incl_scan_256<u32>(sum, reinterpret_cast<u32*>(scratch));
+    u32 run = incl - sum;
+#pragma unroll
+    for (int q = 0; q < P3_RPT; q++) {
+      s_rcnt[tid * P3_RPT + q] = run;  // exclusive prefix of region tid*P3_RPT+q
+      run += c[q];
+    }
+    __shared__ u32 s_total;
+    if (tid == 255) s_total = incl;
+    __syncthreads();
+    const u32 total = s_total;
+    for (u32 i0 = 0; i0 < total; i0 += 256 * 4) {
+      u32 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const u32 i = i0 + u * 256 + tid;
+        x[u] = 0xffffffffu;
+        if (i < total) {
+          u32 lo = 0, hi = nregions;  // last region with prefix <= i
+          while (hi - lo > 1) {
+            const u32 mid = (lo + hi) >> 1;
+            if (s_rcnt[mid] <= i) lo = mid; else hi = mid;
+          }
+          x[u] = selbuf[(u64)lo * R + (i - s_rcnt[lo])] - kmin;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (x[u] != 0xffffffffu && (x[u] >> DSH3) == b2) atomicAdd(&shist[x[u] & ((1u << DSH3) - 1u)], 1u);
+    }
+    __syncthreads();
+    k2_resolve_theta(ctrl, kmin, r1, r2, nregions, sup_cnt, sup_off, &r3, scratch, nD, shist);
+    return;
+  }
   if (r1.cnt * 4 > nD) {
     // K2 did not compact this (large) bucket: scan D, four uint4 per thread and step
     const u32 span = kmax - kmin;
@@ -314,6 +375,7 @@ __global__ void __launch_bounds__(256) k2b_superset(K2Args a) {
   __shared__ int am_last;
   __shared__ uint4 stage[8][BETA2 ? 256 : 1];
   Ctrl* ctrl = a.ctrl;
+  if (ld_volatile_u32(&ctrl->small_done)) return;  // finished by fast_tail
   const DigitResult r1 = ctrl->selD.r1;
   if (a.sup_sid == nullptr || r1.cnt * 4 <= a.nD) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -360,7 +422,10 @@ __global__ void __launch_bounds__(256) k2b_superset(K2Args a) {
       u32 t = incl - nc;
 #pragma unroll
       for (int j = 0; j < 16; j += 2)
-        if ((mc >> j) & 1u) stage[warp][t++] = make_uint4((u32)((i0 + j) >> 1), v[j], v[j + 1], v[j + 1]);
+        if ((mc >> j) & 1u) {
+          const u32 sid = (u32)((i0 + j) >> 1);
+          stage[warp][t++] = make_uint4(sid, v[j], v[j + 1], __ldg(a.meta + sid));
+        }
       __syncwarp();
       for (u32 q = lane; q < tot; q += 32) a.sup_sid[out0 + run + q] = stage[warp][q];
       __syncwarp();
@@ -368,7 +433,10 @@ __global__ void __launch_bounds__(256) k2b_superset(K2Args a) {
       u64 o = out0 + run + incl - nc;
 #pragma unroll
       for (int j = 0; j < 16; j++)
-        if ((mc >> j) & 1u) a.sup_sid[o++] = make_uint4((u32)((i0 + j) / beta), v[j], 0u, 0u);
+        if ((mc >> j) & 1u) {
+          const u32 sid = (u32)((i0 + j) / beta);
+          a.sup_sid[o++] = make_uint4(sid, v[j], 0u, __ldg(a.meta + sid));
+        }
     }
     run += tot;
   }
