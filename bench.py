@@ -275,6 +275,63 @@ def bench_configs(dev, stream, peak: float, args):
     return res
 
 
+def bench_sharded_world1(dev, stream, v, n, args):
+    """The multi-GPU step (ShardedTopK over NCCL) on a single-rank communicator:
+    its fixed per-step cost next to the plain 1-GPU plan, with and without the
+    theta exchange, eager and captured as one CUDA graph (kernels + NCCL)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2109_08219_b200 as dtopk
+    from paper_2109_08219_b200 import _native
+    from paper_2109_08219_b200.pipeline import DrTopK
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
+    out = {"backend": "nccl", "world": 1, "nccl_version": ".".join(map(str, torch.cuda.nccl.version())), "cases": []}
+    reps = max(10, min(args.steps, 50))
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    try:
+        for k in (1024, 1 << 20):
+            cfg = dtopk.PipelineConfig(k=k)
+            p = DrTopK(n, cfg, _native.DTYPE_U32, torch.uint32, dev, timed=False, use_graph=True)
+            base = timeit(lambda: p.launch(v, stream))
+            case = {"k": k, "plan_ms": round(base, 4)}
+            for merge in ("gather", "select"):
+                for exch in (True, False):
+                    st = dtopk.ShardedTopK(v, n, k, cfg, merge=merge, exchange_theta=exch)
+                    eager = timeit(st.step)
+                    st.capture()
+                    graph = timeit(st.step)
+                    r = st.result()
+                    same = bool(torch.equal(r.indices, p.indices))
+                    case[f"{merge}_x{int(exch)}"] = {"eager_ms": round(eager, 4), "graph_ms": round(graph, 4),
+                                                     "graph_overhead_us": round((graph - base) * 1e3, 1),
+                                                     "same_answer_as_plan": same}
+                    del st
+            out["cases"].append(case)
+            del p
+    finally:
+        dist.destroy_process_group()
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -322,6 +379,8 @@ def run_ours(args):
         # weak scaling: rank r owns keys [r*n, (r+1)*n) of one n*world vector; K1-K2 locally,
         # theta all-reduce(MAX), K3.. with theta*, all-gather of <= k pairs per rank, device merge
         sharded = dtopk.ShardedTopK(v, n * world, k, cfg, index_offset=rank * n)
+        if backend == "nccl":
+            sharded.capture()  # kernels + NCCL collectives of one step in one CUDA graph
 
         def step(ev=None):
             sharded.step()
@@ -483,6 +542,13 @@ def run_ours(args):
     if world == 1 and not args.no_configs and rank == 0:
         out["configs"] = bench_configs(dev, stream, peak, args)
 
+    # ---- the multi-GPU step's fixed cost on one GPU (single-rank NCCL communicator)
+    if world == 1 and not args.no_sharded and rank == 0:
+        try:
+            out["sharded_world1"] = bench_sharded_world1(dev, stream, v, n, args)
+        except Exception as exc:  # reported, not fatal: the headline does not depend on it
+            out["sharded_world1"] = {"error": repr(exc)[:300]}
+
     # ---- the timed answer's reference counters (exact mode), checked in cpu_baseline
     gpu_values = gpu_stats = None
     if world == 1:
@@ -551,6 +617,7 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE config 3-5 extra field")
     ap.add_argument("--no-big", action="store_true", help="skip the 2^33 single-GPU case of the configs field")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA-graph plan")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the single-rank NCCL ShardedTopK field")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

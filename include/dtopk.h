@@ -147,6 +147,42 @@ dtopk_status dtopk_extract_delegates(const void* keys, uint64_t n, int dtype, in
 dtopk_status dtopk_kth_largest(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t* out_kth,
                                void* ws, size_t ws_bytes, void* stream);
 
+/* ---- Multi-GPU candidate merge (distributed.py:191-251 coordinator merge) ----
+ * Every rank's candidates are (value bits, global index) lists ordered
+ * (key desc, index asc); ranks own contiguous shards in rank order.
+ *
+ * dtopk_merge_lists: exact first `cap` pairs of the merge of n_lists such lists
+ * (list j at offset o_j = in_off[j], or j * in_stride when in_off is null;
+ * in_len[j * len_stride] valid pairs, device int64), by a tree of pairwise merge-path
+ * rounds; equal keys keep list (= index) order.  Indices of list j start at
+ * in_idx + o_j; its values at in_val + o_j * vmul (u32 words), one value every
+ * vstride words (vstride 2: the low word of int64 slots).  tmp_val / tmp_idx hold dtopk_merge_tmp_pairs(n_lists, cap) pairs,
+ * tmp_len 2 * n_lists int64.  Writes exactly min(cap, sum in_len) pairs. */
+size_t dtopk_merge_tmp_pairs(int n_lists, uint64_t cap);
+dtopk_status dtopk_merge_lists(int dtype, int largest, const uint32_t* in_val, int vmul, int vstride,
+                               const int64_t* in_idx, const int64_t* in_off, int64_t in_stride,
+                               const int64_t* in_len, int64_t len_stride, int n_lists, uint64_t cap,
+                               uint32_t* out_val,
+                               int64_t* out_idx, uint32_t* tmp_val, int64_t* tmp_idx, int64_t* tmp_len,
+                               void* stream);
+
+/* Distributed radix select over per-rank candidate lists (merge="select"):
+ *   dtopk_dsel_init(state[2], hist[2048], k)
+ *   for pass in 0..2: dtopk_dsel_hist -> all_reduce(SUM, hist) -> dtopk_dsel_digit
+ *     (after pass 2, gt_eq[0..1] = this rank's candidates above / equal to kth)
+ *   all_gather(gt_eq) -> gathered[2 * world]
+ *   dtopk_dsel_place -> slots[2k] (own pairs in own slots, zero elsewhere) and the
+ *     rank segment table; all_reduce(SUM, slots) assembles the answer, which
+ *     dtopk_merge_lists(vstride 2, in_off = seg_off, in_len = seg_len) orders. */
+dtopk_status dtopk_dsel_init(int64_t* state, int64_t* hist, uint64_t k, void* stream);
+dtopk_status dtopk_dsel_hist(int dtype, int largest, const uint32_t* bits, const int64_t* cnt, uint64_t cap,
+                             const int64_t* state, int pass, int64_t* hist, void* stream);
+dtopk_status dtopk_dsel_digit(int dtype, int largest, int64_t* state, int64_t* hist, int pass,
+                              const uint32_t* bits, const int64_t* cnt, int64_t* gt_eq, void* stream);
+dtopk_status dtopk_dsel_place(const int64_t* gathered, const int64_t* state, int rank, int world, uint64_t k,
+                              const uint32_t* bits, const int64_t* idx, int64_t* slots, int64_t* seg_off,
+                              int64_t* seg_len, void* stream);
+
 /* CUDA timing events for stage_events (cudaEventCreate / Destroy /
  * ElapsedTime; elapsed synchronises on `end`). */
 void* dtopk_event_create(void);

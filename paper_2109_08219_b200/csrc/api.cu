@@ -22,6 +22,7 @@
 #include "delegate.cuh"
 #include "fast.cuh"
 #include "generate.cuh"
+#include "merge.cuh"
 #include "scan.cuh"
 #include "select.cuh"
 
@@ -647,6 +648,72 @@ dtopk_status check_delegate(u64 n, int alpha, int beta) {
   return DTOPK_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Multi-GPU candidate merge (merge.cuh): ShardedTopK's device-side glue.
+// ---------------------------------------------------------------------------
+template <int M>
+void run_merge_lists(const uint32_t* in_val, int vmul, int vstride, const int64_t* in_idx, const int64_t* in_off,
+                     int64_t in_stride, const int64_t* in_len, int64_t len_stride, int n_lists, int64_t cap,
+                     uint32_t* out_val,
+                     int64_t* out_idx, uint32_t* tmp_val, int64_t* tmp_idx, int64_t* tmp_len, cudaStream_t s) {
+  // tmp_* hold two ping-pong levels of ceil(n_lists / 2) lists of `cap` pairs
+  const int half = (n_lists + 1) / 2;
+  const int64_t level = (int64_t)half * cap;
+  MergeArgs a{};
+  a.in_val = in_val;
+  a.vmul = vmul;
+  a.vstride = vstride;
+  a.in_idx = reinterpret_cast<const long long*>(in_idx);
+  a.in_off = reinterpret_cast<const long long*>(in_off);
+  a.in_stride = in_stride;
+  a.in_len = reinterpret_cast<const long long*>(in_len);
+  a.len_stride = len_stride;
+  a.n_lists = n_lists;
+  a.cap = cap;
+  int lvl = 0;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, (cap + MG_TILE - 1) / MG_TILE);
+  for (;;) {
+    const int pairs = (a.n_lists + 1) / 2;
+    const bool last = pairs == 1;
+    a.out_val = last ? out_val : tmp_val + lvl * level;
+    a.out_idx = reinterpret_cast<long long*>(last ? out_idx : tmp_idx + lvl * level);
+    a.out_stride = last ? 0 : cap;
+    a.out_len = reinterpret_cast<long long*>(tmp_len + lvl * half);
+    launch_pdl(merge_round<M>, dim3(gx, pairs), dim3(MG_THREADS), 0, s, a);
+    counted();
+    if (last) break;
+    a.in_val = a.out_val;
+    a.vmul = 1;
+    a.vstride = 1;
+    a.in_idx = a.out_idx;
+    a.in_off = nullptr;
+    a.in_stride = cap;
+    a.in_len = a.out_len;
+    a.len_stride = 1;
+    a.n_lists = pairs;
+    lvl ^= 1;
+  }
+}
+template <int M>
+void run_dsel_hist(const uint32_t* bits, const int64_t* cnt, const int64_t* state, int pass, int64_t* hist,
+                   uint64_t cap, cudaStream_t s) {
+  const int g = grid_for((cap + 256 * 16 - 1) / (256 * 16), num_sms() * 4);
+  launch_pdl(dsel_hist<M>, dim3(g), dim3(256), 0, s, bits, reinterpret_cast<const long long*>(cnt),
+             reinterpret_cast<const long long*>(state), pass, reinterpret_cast<long long*>(hist));
+  counted();
+}
+
+template <int M>
+void run_dsel_digit(int64_t* state, int64_t* hist, int pass, const uint32_t* bits, const int64_t* cnt,
+                    int64_t* gt_eq, cudaStream_t s) {
+  launch_pdl(dsel_digit<M>, dim3(1), dim3(1024), 0, s, reinterpret_cast<long long*>(state),
+             reinterpret_cast<long long*>(hist), pass, bits, reinterpret_cast<const long long*>(cnt),
+             reinterpret_cast<long long*>(gt_eq));
+  counted();
+}
+
+
 #define DISPATCH_MODE(mode, FN, ...)  \
   switch (mode) {                     \
     case 0: FN<0>(__VA_ARGS__); break; \
@@ -904,6 +971,64 @@ dtopk_status dtopk_kth_largest(const uint32_t* keys, uint64_t n, uint64_t k, uin
   sel_pass3<<<gs, 256, 0, s>>>(sd);
   counted();
   sel_finalize<<<1, 256, 0, s>>>(&ctrl->selP, out_kth);
+  counted();
+  return cuda_status();
+}
+
+size_t dtopk_merge_tmp_pairs(int n_lists, uint64_t cap) { return 2ull * (uint64_t)((n_lists + 1) / 2) * cap; }
+
+dtopk_status dtopk_merge_lists(int dtype, int largest, const uint32_t* in_val, int vmul, int vstride,
+                               const int64_t* in_idx,
+                               const int64_t* in_off, int64_t in_stride, const int64_t* in_len,
+                               int64_t len_stride, int n_lists, uint64_t cap, uint32_t* out_val, int64_t* out_idx, uint32_t* tmp_val, int64_t* tmp_idx,
+                               int64_t* tmp_len, void* stream) {
+  if (dtype != DTOPK_U32 && dtype != DTOPK_F32) return DTOPK_INVALID_ARG;
+  if (n_lists < 1 || cap < 1 || (vstride != 1 && vstride != 2) || vmul < 1) return DTOPK_INVALID_ARG;
+  if (!in_val || !in_idx || !in_len || !out_val || !out_idx || !tmp_len) return DTOPK_INVALID_ARG;
+  if (n_lists > 1 && (!tmp_val || !tmp_idx)) return DTOPK_INVALID_ARG;
+  if ((!in_off && in_stride < 0) || len_stride < 1) return DTOPK_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DISPATCH_MODE(key_mode(dtype, largest), run_merge_lists, in_val, vmul, vstride, in_idx, in_off, in_stride, in_len, len_stride,
+                n_lists, (int64_t)cap, out_val, out_idx, tmp_val, tmp_idx, tmp_len, s);
+  return cuda_status();
+}
+
+dtopk_status dtopk_dsel_init(int64_t* state, int64_t* hist, uint64_t k, void* stream) {
+  if (!state || !hist || k < 1) return DTOPK_INVALID_ARG;
+  launch_pdl(dsel_init, dim3(1), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+             reinterpret_cast<long long*>(state), reinterpret_cast<long long*>(hist), (long long)k);
+  counted();
+  return cuda_status();
+}
+
+dtopk_status dtopk_dsel_hist(int dtype, int largest, const uint32_t* bits, const int64_t* cnt, uint64_t cap,
+                             const int64_t* state, int pass, int64_t* hist, void* stream) {
+  if (dtype != DTOPK_U32 && dtype != DTOPK_F32) return DTOPK_INVALID_ARG;
+  if (!bits || !cnt || !state || !hist || pass < 0 || pass > 2) return DTOPK_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DISPATCH_MODE(key_mode(dtype, largest), run_dsel_hist, bits, cnt, state, pass, hist, cap, s);
+  return cuda_status();
+}
+
+dtopk_status dtopk_dsel_digit(int dtype, int largest, int64_t* state, int64_t* hist, int pass, const uint32_t* bits,
+                              const int64_t* cnt, int64_t* gt_eq, void* stream) {
+  if (dtype != DTOPK_U32 && dtype != DTOPK_F32) return DTOPK_INVALID_ARG;
+  if (!state || !hist || !bits || !cnt || !gt_eq || pass < 0 || pass > 2) return DTOPK_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DISPATCH_MODE(key_mode(dtype, largest), run_dsel_digit, state, hist, pass, bits, cnt, gt_eq, s);
+  return cuda_status();
+}
+
+dtopk_status dtopk_dsel_place(const int64_t* gathered, const int64_t* state, int rank, int world, uint64_t k,
+                              const uint32_t* bits, const int64_t* idx, int64_t* slots, int64_t* seg_off,
+                              int64_t* seg_len, void* stream) {
+  if (!gathered || !state || !bits || !idx || !slots || !seg_off || !seg_len) return DTOPK_INVALID_ARG;
+  if (world < 1 || rank < 0 || rank >= world || k < 1) return DTOPK_INVALID_ARG;
+  const int g = grid_for((k + 255) / 256, num_sms() * 4);
+  launch_pdl(dsel_place, dim3(g), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+             reinterpret_cast<const long long*>(gathered), reinterpret_cast<const long long*>(state), rank, world,
+             (long long)k, bits, reinterpret_cast<const long long*>(idx), reinterpret_cast<long long*>(slots),
+             reinterpret_cast<long long*>(seg_off), reinterpret_cast<long long*>(seg_len));
   counted();
   return cuda_status();
 }

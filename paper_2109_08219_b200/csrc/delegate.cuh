@@ -41,8 +41,15 @@ constexpr int K1_CPS = DTOPK_K1_CPS;        // resident CTAs per SM
 #endif
 constexpr int K1_STAGES = DTOPK_K1_STAGES;  // stages in flight (a multiple of the consumer warps)
 constexpr int K1_PREFETCH = DTOPK_K1_PREFETCH;  // chunks prefetched into L2 ahead of the TMA ring
+#ifndef DTOPK_K1_HCOPIES
+#define DTOPK_K1_HCOPIES 1
+#endif
+// copies of the shared first-digit histogram, picked by lane: at small alpha
+// every lane emits its own subrange, and the delegates (maxima) crowd into a
+// few log-scale bins, so same-address atomics serialise inside a warp
+constexpr int K1_HCOPIES = DTOPK_K1_HCOPIES;
 constexpr int K1_THREADS = (K1_CWARPS + 1) * 32;
-constexpr size_t K1_SMEM = (size_t)K1_STAGES * K1_CHUNK * 4 + 2 * K1_STAGES * 8 + NBD1 * 4;
+constexpr size_t K1_SMEM = (size_t)K1_STAGES * K1_CHUNK * 4 + 2 * K1_STAGES * 8 + (size_t)NBD1 * 4 * K1_HCOPIES;
 
 struct K1Args {
   const u32* keys;
@@ -210,11 +217,12 @@ template <int B>
 __device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 sid, bool leader,
                                               const u32 (&L)[B], u32 meta, bool one_writer = false) {
   const bool w = leader && sid < a.S;
-  if (w) {
+  if (w && DTOPK_K1_EXP != 4) {
     store_delegates<B>(a.D, sid, L);
     a.meta[sid] = meta;
   }
   if (a.do_hist && DTOPK_K1_EXP != 3) {
+    if constexpr (K1_HCOPIES > 1) shist += (threadIdx.x & (K1_HCOPIES - 1)) * NBD1;
     if (one_writer) {  // a single emitting lane: no aggregation needed
       if (w) {
 #pragma unroll
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
 
   const u64 nch = (a.n + K1_CHUNK - 1) >> K1_LOG_CHUNK;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < NBD1; i += K1_THREADS) shist[i] = 0;
+  for (int i = tid; i < NBD1 * K1_HCOPIES; i += K1_THREADS) shist[i] = 0;
   if (tid == 0) {
     for (int s = 0; s < K1_STAGES; s++) {
       mbar_init(&full[s], 1);
@@ -486,7 +494,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   __syncthreads();
   if (a.do_hist) {
     for (int i = tid; i < NBD1; i += K1_THREADS) {
-      const u32 v = shist[i];
+      u32 v = 0;
+#pragma unroll
+      for (int h = 0; h < K1_HCOPIES; h++) v += shist[h * NBD1 + i];
       if (v) atomicAdd(&a.hist1[i], (ull)v);
     }
   }

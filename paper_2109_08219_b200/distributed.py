@@ -155,6 +155,8 @@ def sharded_topk(shard, n_total: int, k: int, cfg: PipelineConfig | None = None,
     Every rank passes its own shard (``shard_bounds`` layout unless
     ``index_offset`` is given) and receives the global answer.
     """
+    from .core import EmptyInput
+
     ops = ops or DeviceOps()
     cfg = cfg or PipelineConfig(k=k)
     world = dist.get_world_size(group)
@@ -162,21 +164,41 @@ def sharded_topk(shard, n_total: int, k: int, cfg: PipelineConfig | None = None,
     n_local = int(shard.numel())
     if index_offset is None:
         index_offset, _ = shard_bounds(n_total, world, rank)
+    # global validation, identical on every rank, before any collective
+    if n_total < 1:
+        raise EmptyInput("input vector must hold at least one element")
     if not 1 <= k <= n_total:
         raise InvalidK(f"k={k} outside [1, {n_total}]")
+    validate_config(replace(cfg, k=k), n_total)
     k_local = min(k, n_local)
-    lcfg = validate_config(replace(cfg, k=k_local), n_local)
-    try:
-        state, theta = ops.begin(shard, lcfg)
-    except Exception as exc:  # surfaced like the reference's WorkerFailed (distributed.py:238-241)
-        raise WorkerFailed(f"rank {rank} failed in begin: {exc!r}") from exc
-    # Every rank must join the collective; direct-path ranks contribute theta = 0.
-    t = theta if theta is not None else torch.zeros(1, dtype=torch.int64, device=_dev_of(shard))
+    dev = _dev_of(shard)
+    state = theta = err = None
+    lcfg = cfg
+    if n_local > 0:
+        try:
+            lcfg = validate_config(replace(cfg, k=k_local), n_local)
+            state, theta = ops.begin(shard, lcfg)
+        except Exception as exc:  # surfaced like the reference's WorkerFailed (distributed.py:238-241)
+            err = exc
+    # a rank that failed must not leave its peers blocked in a collective:
+    # every rank learns of any failure before the exchange
+    flag = torch.tensor([1 if err is not None else 0], dtype=torch.int64, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if int(flag.item()):
+        if err is not None:
+            raise WorkerFailed(f"rank {rank} failed in begin: {err!r}") from err
+        raise WorkerFailed("another rank failed in begin")
+    # Every rank must join the collective; direct-path and empty ranks contribute theta = 0.
+    t = theta if theta is not None else torch.zeros(1, dtype=torch.int64, device=dev)
     if exchange_theta:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-    vals, idx = ops.finish(state, t if (theta is not None and exchange_theta) else theta, index_offset)
+    if n_local > 0:
+        vals, idx = ops.finish(state, t if (theta is not None and exchange_theta) else theta, index_offset)
+    else:
+        vdt = torch.float32 if shard.dtype == torch.float32 else torch.uint32
+        vals = torch.empty(0, dtype=vdt, device=dev)
+        idx = torch.empty(0, dtype=torch.int64, device=dev)
     # all_gather counts, then fixed-size candidate buffers
-    dev = vals.device
     cnt = torch.tensor([vals.numel()], dtype=torch.int64, device=dev)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(counts, cnt, group=group)
@@ -192,7 +214,7 @@ def sharded_topk(shard, n_total: int, k: int, cfg: PipelineConfig | None = None,
     dist.all_gather(ig, ibuf, group=group)
     cat_v = torch.cat([g[:c] for g, c in zip(vg, counts)])
     cat_i = torch.cat([g[:c] for g, c in zip(ig, counts)])
-    values, indices = ops.merge(cat_v, cat_i, k, lcfg.largest)
+    values, indices = ops.merge(cat_v, cat_i, k, cfg.largest)
     stats = WorkloadStats()
     stats.device = {"gathered_pairs": int(sum(counts)), "gathered_bytes": int(sum(counts)) * (vals.element_size() + 8),
                     "theta_global": int(t.item()) if exchange_theta else None}
@@ -204,159 +226,227 @@ class ShardedTopK:
     """Planned ``sharded_topk`` for one rank (fixed shard size, k, config, dtype).
 
     The benchmark and serving path: workspaces and buffers are allocated once,
-    and a step never synchronises the host.  Per step, on the current stream:
-    K1-K2 (``dtopk_select_begin``) -> all_reduce(MAX) of the int64 theta slot,
-    in place in the workspace -> K3.. (``dtopk_select_finish`` with theta*) ->
-    all_gather of the device-side pair count and of the fixed-size (value,
-    global index) buffers -> device compaction that moves every rank's valid
-    pairs to the front in rank order (padding after them, worst key) -> exact
-    device top-k of the concatenation (direct radix path of the same library),
-    whose positions map back to global indices.  Rank order is global index
-    order, so the tie rule (lowest index first) holds across ranks.
+    a step never synchronises the host, and with the NCCL backend the whole
+    step can be captured in one CUDA graph (``capture``).  Per step, on the
+    current stream:
 
-    ``merge="select"`` (the default for k_local > 2^16 on more than one rank,
-    SURVEY.md section 8e step 5) replaces the all_gather of world*k pairs by a
-    distributed radix select over the candidates: three all_reduce(SUM) rounds
-    of a 2048-bin histogram (digits 11/11/10 bits of the order key) find the
-    global kth key and how many of its ties are taken; one all_gather of the
-    per-rank (above, equal) counts gives every rank its exact contribution
-    (its first above_r + take_r pairs, take_r assigned in rank = index order)
-    and its offset; an all_reduce(SUM) of two zeroed k-slot buffers, each
-    rank writing only its own slots, assembles exactly k pairs, which one
-    device radix sort orders.  Collective bytes per rank: ~12k instead of
-    12*world*k, and the final sort is over k keys instead of world*k.
-    Every step stays on the device (no host synchronisation).
+    1. K1-K2 (``dtopk_select_begin``) -> theta_r in the workspace's int64 slot;
+    2. ``all_reduce(MAX)`` of that slot in place (``exchange_theta``; ranks on
+       the direct path or with an empty shard contribute 0 from a zeroed slot);
+    3. K3.. (``dtopk_select_finish`` with theta*) writes <= k_r (value, global
+       index) pairs ordered (key desc, index asc) straight into this rank's
+       send buffer ``[count | indices | value bits]``;
+    4. merge="gather": ONE ``all_gather`` of the send buffers, then
+       ``dtopk_merge_lists`` -- a tree of pairwise merge-path rounds on the
+       device -- takes the exact first k pairs of the rank lists.  Shards are
+       contiguous in rank order, so on equal keys the lower rank (= lower
+       global index) comes first: the tie rule holds without a sort.
+       merge="select" (default for k_local > 2^16 on more than one rank,
+       SURVEY.md section 8e step 5): a distributed radix select over the
+       candidates (``dtopk_dsel_*``: 3 histogram all-reduces + one all_gather
+       of per-rank (above, equal) counts) decides every rank's contribution;
+       each rank writes its pairs into its slots of a zeroed k-slot buffer,
+       one all_reduce(SUM) assembles the answer and ``dtopk_merge_lists``
+       merges the rank segments.  ~16k bytes per rank instead of 12*world*k.
+
+    Every rank validates the global shape (n_total, k, cfg) identically before
+    any collective, and every rank joins every collective whatever its shard
+    (ragged last shard, empty shard, direct-path shard): the gather width is
+    the global k_local = min(k, ceil(n_total / world)).
     """
 
     def __init__(self, shard: torch.Tensor, n_total: int, k: int, cfg: PipelineConfig | None = None, *,
                  group=None, index_offset: int | None = None, exchange_theta: bool = True,
                  merge: str = "auto"):
         from . import _device, _native
+        from .core import EmptyInput
         from .pipeline import DrTopK
 
         cfg = cfg or PipelineConfig(k=k)
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        dv = _device.to_device(shard)
-        if dv.kind != "torch_cuda":
-            raise ValueError("ShardedTopK needs the shard resident on this rank's GPU")
-        self.dv = dv
-        self.n_local = dv.n
+        # global validation: identical on every rank, before any collective
+        if n_total < 1:
+            raise EmptyInput("input vector must hold at least one element")
         if not 1 <= k <= n_total:
             raise InvalidK(f"k={k} outside [1, {n_total}]")
+        validate_config(replace(cfg, k=k), n_total)  # InvalidBeta / backend errors on every rank alike
+        if merge not in ("auto", "gather", "select"):
+            raise ValueError(f"unknown merge {merge!r}")
+        if not isinstance(shard, torch.Tensor) or not shard.is_cuda:
+            raise ValueError("ShardedTopK needs the shard resident on this rank's GPU")
+        self.lib = _native.load()
+        dev = shard.device
+        self.device = dev
+        self.n_local = int(shard.numel())
         if index_offset is None:
             index_offset, _ = shard_bounds(n_total, self.world, self.rank)
         self.index_offset = int(index_offset)
         self.k = int(k)
-        self.k_local = min(self.k, self.n_local)
-        self.lcfg = validate_config(replace(cfg, k=self.k_local), self.n_local)
+        w = self.world
+        self.kl = min(self.k, -(-int(n_total) // w))  # global gather width
+        self.k_loc = min(self.kl, self.n_local)
         self.exchange_theta = exchange_theta
-        dev = dv.device
-        self.local = DrTopK(self.n_local, self.lcfg, dv.code, dv.out_dtype, dev, timed=False)
-        self.lib = self.local.lib
-        ws = self.local.ws
-        off = _native.DtopkResult.theta_slot.offset
-        self.theta = ws[off:off + 8].view(torch.int64)
-        koff = _native.DtopkResult.k_out.offset
-        self.kout = ws[koff:koff + 8].view(torch.int64)
-        w, kl = self.world, self.k_local
-        self.cat_n = w * kl
-        # worst key of the merge order, as the raw bits of the output dtype
-        worst = {(_native.DTYPE_U32, True): 0, (_native.DTYPE_U32, False): -1,
-                 (_native.DTYPE_F32, True): -1, (_native.DTYPE_F32, False): 0x7FFFFFFF}[(dv.code, self.lcfg.largest)]
-        self.pad_bits = torch.tensor(worst, dtype=torch.int32, device=dev)
-        self.g_cnt = torch.empty(w, dtype=torch.int64, device=dev)
-        self.g_val = torch.empty(self.cat_n, dtype=torch.int32, device=dev)
-        self.g_idx = torch.empty(self.cat_n, dtype=torch.int64, device=dev)
-        self.cat_val = torch.empty(self.cat_n, dtype=torch.int32, device=dev)
-        self.cat_idx = torch.empty(self.cat_n, dtype=torch.int64, device=dev)
-        self.j = torch.arange(kl, dtype=torch.int64, device=dev).view(1, kl)
+        if shard.dtype == torch.float32:
+            code, out_dtype = _native.DTYPE_F32, torch.float32
+        else:
+            code, out_dtype = _native.DTYPE_U32, torch.uint32
+        self.code, self.out_dtype = code, out_dtype
+        self.largest = bool(cfg.largest)
+        self.local = None
+        self.dv = None
+        if self.n_local > 0:
+            self.dv = _device.to_device(shard)
+            self.lcfg = validate_config(replace(cfg, k=self.k_loc), self.n_local)
+            self.local = DrTopK(self.n_local, self.lcfg, code, out_dtype, dev, timed=False)
+        else:
+            self.lcfg = None
+        kl = self.kl
+        # send buffer (int64 words): [count, 0, indices[kl], value bits[kl] as u32 pairs]
+        self.pw = 2 + kl + (kl + 1) // 2
+        self.send = torch.zeros(self.pw, dtype=torch.int64, device=dev)
+        self.s_idx = self.send[2:2 + kl]
+        self.s_val = self.send[2 + kl:].view(torch.int32)[:kl]
+        self.direct = self.local is not None and self.lcfg.direct_fallback
+        if self.local is not None and not self.direct:
+            ws = self.local.ws
+            off = _native.DtopkResult.theta_slot.offset
+            self.theta = ws[off:off + 8].view(torch.int64)
+        else:
+            self.theta = torch.zeros(1, dtype=torch.int64, device=dev)
+        if self.local is not None:
+            koff = _native.DtopkResult.k_out.offset
+            self.kout = self.local.ws[koff:koff + 8].view(torch.int64)
         if merge == "auto":
             merge = "select" if w > 1 and kl > (1 << 16) else "gather"
-        if merge not in ("gather", "select"):
-            raise ValueError(f"unknown merge {merge!r}")
         self.merge_mode = merge
-        if merge == "select":
-            self.cat_n = self.k  # the assembled answer, sorted by the merge plan
-            self.g_cnt = torch.empty(2 * w, dtype=torch.int64, device=dev)
-            self.hist = torch.empty(_SEL_BINS, dtype=torch.int64, device=dev)
-            self.sel_val = torch.empty(self.k + 1, dtype=torch.int32, device=dev)  # slot k: sink for unused pairs
-            self.sel_idx = torch.empty(self.k + 1, dtype=torch.int64, device=dev)
-            self.cat_val = self.sel_val[: self.k]
-            self.cat_idx = self.sel_idx[: self.k]
-        self.merge = DrTopK(self.cat_n, PipelineConfig(k=self.k, alpha=0, auto_alpha=False, largest=self.lcfg.largest),
-                            dv.code, dv.out_dtype, dev, timed=False)
-        self.values = self.merge.values
+        self.values = torch.empty(self.k, dtype=out_dtype, device=dev)
         self.indices = torch.empty(self.k, dtype=torch.int64, device=dev)
+        nl = w
+        tmp_pairs = int(self.lib.dtopk_merge_tmp_pairs(nl, self.k))
+        self.tmp_val = torch.empty(max(1, tmp_pairs), dtype=torch.int32, device=dev)
+        self.tmp_idx = torch.empty(max(1, tmp_pairs), dtype=torch.int64, device=dev)
+        self.tmp_len = torch.empty(2 * nl, dtype=torch.int64, device=dev)
+        if merge == "gather":
+            self.gathered = torch.empty(w * self.pw, dtype=torch.int64, device=dev)
+        else:
+            self.state = torch.empty(2, dtype=torch.int64, device=dev)
+            self.hist = torch.empty(_SEL_BINS, dtype=torch.int64, device=dev)
+            self.gt_eq = torch.zeros(2, dtype=torch.int64, device=dev)
+            self.g_cnt = torch.empty(2 * w, dtype=torch.int64, device=dev)
+            self.seg = torch.empty(2 * w, dtype=torch.int64, device=dev)
+            self.slots = torch.empty(2 * self.k, dtype=torch.int64, device=dev)
+        self.graph = None
+
+    # -- one step ----------------------------------------------------------
+    def _local(self, keys, s) -> None:
+        from . import _native
+
+        p, c, lib = self.local, self.lcfg, self.lib
+        kl = self.k_loc
+        if self.direct:
+            if self.exchange_theta:
+                self.theta.zero_()
+                dist.all_reduce(self.theta, op=dist.ReduceOp.MAX, group=self.group)
+            p.launch(keys, s, index_offset=self.index_offset)
+            self.s_val[:kl].copy_(p.values.view(torch.int32)[:kl])
+            self.s_idx[:kl].copy_(p.indices[:kl])
+            self.send[0:1].fill_(kl)
+            return
+        _native.check(lib.dtopk_select_begin(keys.data_ptr(), self.n_local, self.code, c.k, int(c.largest), c.alpha,
+                                             c.beta, p.flags, p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None),
+                      "dtopk_select_begin")
+        if self.exchange_theta:
+            dist.all_reduce(self.theta, op=dist.ReduceOp.MAX, group=self.group)
+        _native.check(lib.dtopk_select_finish(
+            keys.data_ptr(), self.n_local, self.code, c.k, int(c.largest), c.alpha, c.beta, p.flags,
+            self.theta.data_ptr() if self.exchange_theta else None, self.s_val.data_ptr(), self.s_idx.data_ptr(),
+            self.index_offset, p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None), "dtopk_select_finish")
+        self.send[0:1].copy_(self.kout)
 
     def step(self, keys: torch.Tensor | None = None) -> None:
         """One sharded top-k; results in ``self.values`` / ``self.indices`` (stream-ordered)."""
+        if self.graph is not None and keys is None:
+            self.graph.replay()
+            return
         from . import _native
 
-        keys = self.dv.keys if keys is None else keys
-        p, c = self.local, self.lcfg
-        s = torch.cuda.current_stream(self.dv.device)
-        if c.direct_fallback:
-            p.launch(keys, s, index_offset=self.index_offset)
-        else:
-            _native.check(p.lib.dtopk_select_begin(keys.data_ptr(), self.n_local, self.dv.code, c.k, int(c.largest),
-                                                   c.alpha, c.beta, p.flags, p.ws.data_ptr(), p.ws_bytes,
-                                                   s.cuda_stream, None), "dtopk_select_begin")
-            if self.exchange_theta:
-                dist.all_reduce(self.theta, op=dist.ReduceOp.MAX, group=self.group)
-            _native.check(p.lib.dtopk_select_finish(
-                keys.data_ptr(), self.n_local, self.dv.code, c.k, int(c.largest), c.alpha, c.beta, p.flags,
-                self.theta.data_ptr() if self.exchange_theta else None, p.values.data_ptr(), p.indices.data_ptr(),
-                self.index_offset, p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None), "dtopk_select_finish")
-        kl = self.k_local
-        cnt = self.kout.clamp(max=kl) if not c.direct_fallback else torch.full_like(self.kout, kl)
-        if self.merge_mode == "select":
-            self._select_merge(cnt, s)
+        s = torch.cuda.current_stream(self.device)
+        if self.local is not None:
+            self._local(self.dv.keys if keys is None else keys, s)
+        elif self.exchange_theta:  # empty shard: joins the exchange with theta = 0, sends no pairs
+            self.theta.zero_()
+            dist.all_reduce(self.theta, op=dist.ReduceOp.MAX, group=self.group)
+        lib, w, kl = self.lib, self.world, self.kl
+        largest = int(self.largest)
+        if self.merge_mode == "gather":
+            _all_gather_flat(self.gathered, self.send, self.group)
+            g = self.gathered
+            _native.check(lib.dtopk_merge_lists(
+                self.code, largest, g.data_ptr() + 8 * (2 + kl), 2, 1, g.data_ptr() + 16, None, self.pw, g.data_ptr(),
+                self.pw, w, self.k, self.values.data_ptr(), self.indices.data_ptr(), self.tmp_val.data_ptr(),
+                self.tmp_idx.data_ptr(), self.tmp_len.data_ptr(), s.cuda_stream), "dtopk_merge_lists")
             return
-        _all_gather_flat(self.g_cnt, cnt, self.group)
-        _all_gather_flat(self.g_val, p.values.view(torch.int32)[:kl], self.group)
-        _all_gather_flat(self.g_idx, p.indices[:kl], self.group)
-        # compaction: rank r's first cnt_r pairs to [pre_r, pre_r + cnt_r), padding to the tail
-        cnt_r = self.g_cnt.view(-1, 1)
-        valid = self.j < cnt_r
-        pre = torch.cumsum(self.g_cnt, 0) - self.g_cnt
-        total = self.g_cnt.sum()
-        inval = kl - self.g_cnt
-        pre_inv = torch.cumsum(inval, 0) - inval
-        dest = torch.where(valid, pre.view(-1, 1) + self.j, total + pre_inv.view(-1, 1) + (self.j - cnt_r))
-        vals = torch.where(valid.view(-1), self.g_val, self.pad_bits)
-        self.cat_val.scatter_(0, dest.view(-1), vals)
-        self.cat_idx.scatter_(0, dest.view(-1), self.g_idx)
-        self.merge.launch(self.cat_val.view(self.values.dtype), s)
-        torch.index_select(self.cat_idx, 0, self.merge.indices, out=self.indices)
+        self._select_merge(s)
 
-    def _select_merge(self, cnt: torch.Tensor, s) -> None:
+    def _select_merge(self, s) -> None:
         """Distributed radix select + exact-k assembly (class docstring)."""
-        p, kl, k = self.local, self.k_local, self.k
-        bits = p.values.view(torch.int32)[:kl]
-        key = _order_key(bits, self.dv.code, self.lcfg.largest)
-        jj = self.j.view(-1)
-        mine, pre = select_contribution(key, cnt, k, self.rank, self.group, self.hist, self.g_cnt)
-        dest = torch.where(jj < mine, pre + jj, torch.full_like(jj, k))
-        self.sel_val.zero_().scatter_(0, dest, bits)
-        self.sel_idx.zero_().scatter_(0, dest, p.indices[:kl])
-        dist.all_reduce(self.sel_val, op=dist.ReduceOp.SUM, group=self.group)
-        dist.all_reduce(self.sel_idx, op=dist.ReduceOp.SUM, group=self.group)
-        self.merge.launch(self.cat_val.view(self.values.dtype), s)
-        torch.index_select(self.cat_idx, 0, self.merge.indices, out=self.indices)
+        from . import _native
+
+        lib, cs = self.lib, s.cuda_stream
+        cnt = self.send.data_ptr()
+        bits = self.s_val.data_ptr()
+        largest = int(self.largest)
+        _native.check(lib.dtopk_dsel_init(self.state.data_ptr(), self.hist.data_ptr(), self.k, cs), "dsel_init")
+        for pas in range(3):
+            _native.check(lib.dtopk_dsel_hist(self.code, largest, bits, cnt, self.kl, self.state.data_ptr(), pas,
+                                              self.hist.data_ptr(), cs), "dsel_hist")
+            dist.all_reduce(self.hist, op=dist.ReduceOp.SUM, group=self.group)
+            _native.check(lib.dtopk_dsel_digit(self.code, largest, self.state.data_ptr(), self.hist.data_ptr(), pas,
+                                               bits, cnt, self.gt_eq.data_ptr(), cs), "dsel_digit")
+        _all_gather_flat(self.g_cnt, self.gt_eq, self.group)
+        w, k = self.world, self.k
+        _native.check(lib.dtopk_dsel_place(self.g_cnt.data_ptr(), self.state.data_ptr(), self.rank, w, k, bits,
+                                           self.s_idx.data_ptr(), self.slots.data_ptr(), self.seg.data_ptr(),
+                                           self.seg.data_ptr() + 8 * w, cs), "dsel_place")
+        dist.all_reduce(self.slots, op=dist.ReduceOp.SUM, group=self.group)
+        sl = self.slots
+        _native.check(lib.dtopk_merge_lists(
+            self.code, largest, sl.data_ptr(), 2, 2, sl.data_ptr() + 8 * k, self.seg.data_ptr(), 0,
+            self.seg.data_ptr() + 8 * w, 1, w, k, self.values.data_ptr(), self.indices.data_ptr(),
+            self.tmp_val.data_ptr(), self.tmp_idx.data_ptr(), self.tmp_len.data_ptr(), cs), "dtopk_merge_lists")
+
+    def capture(self, warmup: int = 2) -> None:
+        """Capture one whole step (kernels + NCCL collectives) in a CUDA graph;
+        later ``step()`` calls (without new keys) replay it."""
+        if dist.get_backend(self.group) != "nccl":
+            raise RuntimeError("graph capture of the sharded step needs the NCCL backend")
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.step()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.step()
+        torch.cuda.synchronize(self.device)
+        self.graph = g
 
     def result(self) -> TopKResult:
-        """Synchronise and wrap the last step's answer (reads the merge header)."""
-        from .core import WorkloadStats as _WS
+        """Synchronise and wrap the last step's answer."""
+        from . import _native
 
-        hdr = self.merge.header()
-        stats = _WS()
-        pairs = self.k if self.merge_mode == "select" else int(self.g_cnt.sum().item())
+        stats = WorkloadStats()
+        if self.merge_mode == "gather":
+            pairs = int(self.gathered.view(self.world, self.pw)[:, 0].sum().item())
+        else:
+            pairs = self.k
         stats.device = {"merge": self.merge_mode, "gathered_pairs": pairs, "theta_global": int(self.theta.item())}
-        from . import _device
-
-        thr = _device.key_to_value(int(hdr.kth_key), self.dv.code, self.lcfg.largest)
+        last = self.values[-1:]
+        thr = float(last.item()) if self.code == _native.DTYPE_F32 else int(last.view(torch.int32).item()) & 0xFFFFFFFF
         return TopKResult(values=self.values, threshold=thr, stats=stats, indices=self.indices)
 
 

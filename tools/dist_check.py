@@ -24,26 +24,37 @@ dev = torch.device("cuda", local % torch.cuda.device_count())
 torch.cuda.set_device(dev)
 dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
 ok = True
-for dist_name, n_local, k, largest in [("uniform", 1 << 22, 1000, True), ("uniform", (1 << 22) + 37, 70000, True),
-                                       ("few_distinct", 1 << 21, 5000, True), ("all_equal", 1 << 21, 3000, False),
-                                       ("normal_f32", 1 << 22, 4096, True), ("uniform", 1 << 20, 1 << 19, True),
-                                       ("all_equal", 1 << 20, 1 << 18, True), ("few_distinct", 1 << 20, 300001, False),
-                                       ("normal_f32", (1 << 20) + 5, 1 << 17, False)]:
-    n_total = n_local * world
+# (distribution, n_total, k, largest): n_total need not divide by world (ragged last
+# shard, shards shorter than k, an empty shard when n_total < world)
+CASES = [("uniform", (1 << 22) * world, 1000, True), ("uniform", ((1 << 22) + 37) * world, 70000, True),
+         ("few_distinct", (1 << 21) * world, 5000, True), ("all_equal", (1 << 21) * world, 3000, False),
+         ("normal_f32", (1 << 22) * world, 4096, True), ("uniform", (1 << 20) * world, 1 << 19, True),
+         ("all_equal", (1 << 20) * world, 1 << 18, True), ("few_distinct", (1 << 20) * world, 300001, False),
+         ("normal_f32", ((1 << 20) + 5) * world, 1 << 17, False),
+         ("uniform", 4 * 100003 * world + 1, 100003 * world + 1, True),   # ragged: k above the short shard
+         ("uniform", 4 * 100003 * world + 1, 150000, True),
+         ("uniform", world - 1 if world > 1 else 1, 1, True),              # an empty shard
+         ("uniform", 5000 * world + 3, 7, False)]                          # tiny shards: direct path
+for dist_name, n_total, k, largest in CASES:
     full = data.generate(dist_name, n_total, seed=7, device=dev)
     lo, ln = dtopk.shard_bounds(n_total, world, rank)
     shard = full[lo:lo + ln].clone()
     cfg = dtopk.PipelineConfig(k=k, largest=largest)
-    st = dtopk.ShardedTopK(shard, n_total, k, cfg)
-    for _ in range(2):
-        st.step()
-    r = st.result()
-    other = "select" if st.merge_mode == "gather" else "gather"
-    st3 = dtopk.ShardedTopK(shard, n_total, k, cfg, merge=other)
-    for _ in range(2):
-        st3.step()
-    r3 = st3.result()
-    r2 = dtopk.sharded_topk(shard, n_total, k, cfg)
+    runs = []
+    for merge in ("gather", "select"):
+        for exch in (True, False):
+            st = dtopk.ShardedTopK(shard, n_total, k, cfg, merge=merge, exchange_theta=exch)
+            for _ in range(2):
+                st.step()
+            r = st.result()
+            runs.append((f"ShardedTopK/{merge}/x{int(exch)}", (r.values.clone(), r.indices.clone())))
+            if backend == "nccl" and exch:
+                st.capture()
+                st.step()
+                r = st.result()
+                runs.append((f"ShardedTopK/{merge}/graph", (r.values.clone(), r.indices.clone())))
+    r = dtopk.sharded_topk(shard, n_total, k, cfg)
+    runs.append(("sharded_topk", (r.values, r.indices)))
     torch.cuda.synchronize()
     if rank == 0:
         from oracle import oracle
@@ -51,13 +62,12 @@ for dist_name, n_local, k, largest in [("uniform", 1 << 22, 1000, True), ("unifo
         host = full.cpu().numpy()
         keys = oracle.to_keys(host, largest)
         ek, ei = oracle.topk_with_indices(keys, k)
-        for name, res in ((f"ShardedTopK/{st.merge_mode}", r), (f"ShardedTopK/{other}", r3),
-                          ("sharded_topk", r2)):
-            gi = res.indices.cpu().numpy()
-            gv = res.values.cpu().numpy()
+        for name, (rv, ri) in runs:
+            gi = ri.cpu().numpy()
+            gv = rv.cpu().numpy()
             good = np.array_equal(gi, ei) and np.array_equal(oracle.to_keys(gv, largest), ek)
             ok &= good
-            print(f"{name:20s} {dist_name:12s} world={world} n_local={n_local} k={k} largest={largest}: "
+            print(f"{name:24s} {dist_name:12s} world={world} n_total={n_total} k={k} largest={largest}: "
                   f"{'OK' if good else 'MISMATCH'}", flush=True)
 dist.barrier()
 dist.destroy_process_group()
