@@ -584,7 +584,7 @@ def run_ours(args):
         e2e_s = max_over_ranks((time.perf_counter() - t0) / reps)
         if rank == 0:
             out["e2e"] = {"value": n * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 4,
-                          "d2h_bytes_per_step": k * (4 + 8) + (104 if world == 1 else 0), "ms_per_step": e2e_s * 1e3,
+                          "d2h_bytes_per_step": k * (4 + 8) + (112 if world == 1 else 0), "ms_per_step": e2e_s * 1e3,
                           "path": ("paper_2109_08219_b200.dr_topk(pinned host tensor) -> numpy-style host results"
                                    if world == 1 else
                                    "pinned host shard -> HBM, ShardedTopK.step (NCCL theta all-reduce + pair "

@@ -74,6 +74,8 @@ typedef struct {
   uint32_t kth_key;               /* exact k-th key of the answer                      */
   uint32_t path;                  /* 1 = radix select over the pool, 2 = merge, 3 = direct */
   int64_t theta_slot;             /* theta_local as int64, target of an all-reduce(MAX) */
+  uint32_t filtered;              /* 1: K1 stored only records of subranges above a sampled floor */
+  uint32_t filter_fallback;       /* 1: that floor missed theta's bucket; full K1 + K2 re-ran     */
 } dtopk_result;
 
 /* Bytes of workspace needed by dtopk_select for these parameters. */

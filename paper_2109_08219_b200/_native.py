@@ -57,6 +57,8 @@ class DtopkResult(ctypes.Structure):
         ("kth_key", ctypes.c_uint32),
         ("path", ctypes.c_uint32),
         ("theta_slot", ctypes.c_int64),
+        ("filtered", ctypes.c_uint32),
+        ("filter_fallback", ctypes.c_uint32),
     ]
 
 

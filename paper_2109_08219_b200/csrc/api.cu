@@ -51,11 +51,25 @@ struct Layout {
   size_t ctrl, lb_emg, lb_eme, zero_bytes, k5_tg, k5_te;
   size_t D, meta, partial, pmeta, selbuf, region_cnt, sup_sid, sup_in, sup_cnt, sup_off, rec, e_sid, t_sid, t_cnt,
       stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, e_gpos, e_epos, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
-      digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, total;
-  u64 S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
+      digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, chunk_cnt, total;
+  u64 fcap, S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
       sort_cap;
   u32 g2;
 };
+
+// Filtered delegate pass (K0 sample -> K1 records -> K2 over records): where
+// K1's D + meta writes are a measurable share of the stream (alpha 6..8: 12 B
+// per 256..1024 B read) and the records carry everything the rest of the
+// pipeline reads (beta <= 2).
+inline bool filt_possible(u64 S, int alpha, int beta, int direct) {
+#ifdef DTOPK_NO_FILTER
+  return false;
+#endif
+  return !direct && alpha >= 6 && alpha <= 8 && beta <= 2 && S >= (1ull << 16);
+}
+
+inline int grid_for(u64 work_items, int cap);
+inline u32 k1_grid(u64 nch) { return (u32)grid_for(nch, num_sms() * K1_CPS); }
 
 Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   Layout L{};
@@ -85,6 +99,11 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   const u64 g2 = std::max<u64>(1, std::min<u64>(std::min<u64>((u64)num_sms() * DTOPK_K2_CPS, 768), (L.D_len + 4095) / 4096));
   L.g2 = (u32)g2;
   L.R2 = ((L.D_len + g2 - 1) / g2 + 511) / 512 * 512;
+  const bool filt = filt_possible(L.S, alpha, beta, direct);
+  if (filt) {  // K2 over records: a CTA owns 8 warps x ceil(nch / (8 g2)) chunks of 2048 >> alpha subranges
+    const u64 cpw = (L.nch + 8 * g2 - 1) / (8 * g2);
+    L.R2 = std::max<u64>(L.R2, (8 * cpw * (2048ull >> alpha) * (u64)beta + 511) / 512 * 512);
+  }
   L.k4_tiles = (L.cap_e * W + K4_TILE - 1) / K4_TILE;
   L.k5_tiles = std::max<u64>(1, (L.S + K5_TILE - 1) / K5_TILE);  // records <= S
   L.em_tiles = (L.m_emit + SC_TILE - 1) / SC_TILE;
@@ -107,7 +126,9 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.sup_in = take((u64)L.g2 * 8 * 4);
   L.sup_cnt = take(std::max<u64>((u64)L.g2 * 8, 256 * K2_SEG_PER) * 4);  // padded: read as uint4 by thread
   L.sup_off = take(((u64)L.g2 * 8 + 1) * 4);
-  L.rec = take(L.S * 16);
+  // K3 records; in a filtered call first K1's per-warp record streams (K1 grid x 8 warps x fcap)
+  L.fcap = filt ? (L.nch + (u64)k1_grid(L.nch) * 8 - 1) / ((u64)k1_grid(L.nch) * 8) * (2048ull >> alpha) : 0;
+  L.rec = take(std::max<u64>(L.S, (u64)k1_grid(L.nch) * 8 * L.fcap) * 16);
   L.k5_tg = take(L.k5_tiles * 8);
   L.k5_te = take(L.k5_tiles * 8);
   L.e_sid = take(L.cap_e * 4);
@@ -137,6 +158,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.bk_start = take(bk ? (BK_MAX + 1) * 4 : 0);
   L.bk_info = take(4 * 4);
   L.bk_comp = take(bk ? L.sort_cap * 8 : 0);
+  L.chunk_cnt = take(filt ? L.nch * 4 : 0);
   L.total = off;
   return L;
 }
@@ -229,7 +251,7 @@ void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch) {
 
 template <int MODE>
 void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* ws, const Layout& L, cudaStream_t s,
-                     int nsm) {
+                     int nsm, int fmode = 0) {
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
   K1Args a{keys,
            n,
@@ -238,9 +260,15 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
            D,
            reinterpret_cast<u32*>(ws + L.partial),
            ctrl->selD.hist1,
-           alpha <= K1_LOG_CHUNK ? 1 : 0,
+           // the fallback pass keeps the filtered pass's (complete) histogram
+           (alpha <= K1_LOG_CHUNK && fmode != 2) ? 1 : 0,
            reinterpret_cast<u32*>(ws + L.meta),
-           reinterpret_cast<u32*>(ws + L.pmeta)};
+           reinterpret_cast<u32*>(ws + L.pmeta),
+           ctrl,
+           fmode,
+           reinterpret_cast<uint4*>(ws + L.rec),
+           reinterpret_cast<u32*>(ws + L.chunk_cnt),
+           L.fcap};
   switch (beta) {
     case 1: launch_k1<MODE, 1>(a, s, nsm, L.nch); break;
     case 2: launch_k1<MODE, 2>(a, s, nsm, L.nch); break;
@@ -257,7 +285,8 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
   }
 }
 
-K2Args k2_args(char* ws, const Layout& L, u64 k, int beta) {
+K2Args k2_args(char* ws, const Layout& L, u64 k, int beta, int alpha = 0, int fmode = 0,
+               cudaGraphConditionalHandle fb = {}, int fb_graph = 0) {
   return K2Args{reinterpret_cast<u32*>(ws + L.D),
                 L.D_len,
                 k,
@@ -270,67 +299,16 @@ K2Args k2_args(char* ws, const Layout& L, u64 k, int beta) {
                 reinterpret_cast<u32*>(ws + L.sup_in),
                 reinterpret_cast<u32*>(ws + L.sup_cnt),
                 reinterpret_cast<u32*>(ws + L.sup_off),
-                reinterpret_cast<const u32*>(ws + L.meta)};
-}
-
-// K2 pass 3 (theta from the bucket members) and K2b (the exact superset of a
-// large-bucket call).
-void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, int nsm) {
-  const K2Args k2 = k2_args(ws, L, k, beta);
-  launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2,
-             k2.sup_cnt, k2.sup_off, k2.D, L.D_len);
-  counted();
-  if (beta == 2)
-    launch_pdl(k2b_superset<1>, dim3(L.g2), dim3(256), 0, s, k2);
-  else
-    launch_pdl(k2b_superset<0>, dim3(L.g2), dim3(256), 0, s, k2);
-  counted();
-}
-
-// Delegates (K1) and the delegate scan (K2).  `fused` (a whole dtopk_select or
-// plan): theta is resolved by fast_tail, or by K2 pass 3 inside the general
-// chain when fast_tail declines.  Otherwise (dtopk_select_begin) pass 3 and K2b
-// run here, so that theta_slot holds theta when the call returns.
-template <int MODE>
-void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, const Layout& L, cudaStream_t s, int nsm,
-               void* const* ev, bool fused = false) {
-  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
-  rec(ev, 0, s);
-  u32* D = reinterpret_cast<u32*>(ws + L.D);
-  stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm);
-  rec(ev, 1, s);
-  const K2Args k2 = k2_args(ws, L, k, beta);
-  if (beta == 2)
-    launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
-  else
-    launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, s, k2);
-  counted();
-  if (!fused) theta_resolve(ws, L, k, beta, s, nsm);
-  rec(ev, 2, s);
-}
-
-SortBufs sort_bufs(char* ws, const Layout& L, bool direct) {
-  SortBufs b;
-  b.ka = reinterpret_cast<u32*>(ws + (direct ? L.sak : L.gt_keys));
-  b.ia = reinterpret_cast<u64*>(ws + (direct ? L.sai : L.gt_idx));
-  b.kb = reinterpret_cast<u32*>(ws + L.sbk);
-  b.ib = reinterpret_cast<u64*>(ws + L.sbi);
-  b.counts = reinterpret_cast<u32*>(ws + L.counts);
-  b.digit_base = reinterpret_cast<u32*>(ws + L.digit_base);
-  b.digit_tot = reinterpret_cast<u32*>(ws + L.digit_tot);
-  return b;
-}
-
-void run_sort(Ctrl* ctrl, const SortBufs& b, const Layout& L, cudaStream_t s, int nsm) {
-  const int g = grid_for(L.sort_tiles, nsm * 4);
-  for (int p = 0; p < 4; p++) {
-    sort_hist<<<g, 256, 0, s>>>(ctrl, b, p);
-    counted();
-    sort_scan<<<32, 256, 0, s>>>(ctrl, b, p);
-    counted();
-    sort_scatter<<<g, 256, 0, s>>>(ctrl, b, p);
-    counted();
-  }
+                reinterpret_cast<const u32*>(ws + L.meta),
+                fmode,
+                reinterpret_cast<const u32*>(ws + L.chunk_cnt),
+                reinterpret_cast<const uint4*>(ws + L.rec),
+                L.fcap,
+                k1_grid(L.nch),
+                L.nch,
+                alpha,
+                fb,
+                fb_graph};
 }
 
 // Graph capture context: when `graph` is set, run_finish ends the main
@@ -342,7 +320,8 @@ struct GraphCtx {
   cudaGraph_t graph = nullptr;
   cudaGraphConditionalHandle cond{};  // large-pool tail (set by finish_small)
   cudaGraphConditionalHandle gen{};   // general chain K3..finish_small (set by fast_tail)
-  cudaStream_t s2 = nullptr, s3 = nullptr, s4 = nullptr, s5 = nullptr;
+  cudaGraphConditionalHandle fb{};    // full K1 + K2 rerun after a failed filtered pass (set by K2)
+  cudaStream_t s2 = nullptr, s3 = nullptr, s4 = nullptr, s5 = nullptr, s6 = nullptr;
   unsigned long long main_kernels = 0, body_kernels = 0;
   bool ok = true;
 };
@@ -381,6 +360,95 @@ bool cond_begin(cudaStream_t s, cudaGraphConditionalHandle h, cudaStream_t inner
 bool cond_end(cudaStream_t inner) {
   cudaGraph_t g = nullptr;
   return cap_ok(cudaStreamEndCapture(inner, &g), "end body capture");
+}
+
+// K2 pass 3 (theta from the bucket members) and K2b (the exact superset of a
+// large-bucket call).
+void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, int nsm) {
+  const K2Args k2 = k2_args(ws, L, k, beta);
+  launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2,
+             k2.sup_cnt, k2.sup_off, k2.D, L.D_len);
+  counted();
+  if (beta == 2)
+    launch_pdl(k2b_superset<1>, dim3(L.g2), dim3(256), 0, s, k2);
+  else
+    launch_pdl(k2b_superset<0>, dim3(L.g2), dim3(256), 0, s, k2);
+  counted();
+}
+
+// Delegates (K1) and the delegate scan (K2).  `fused` (a whole dtopk_select or
+// plan): theta is resolved by fast_tail, or by K2 pass 3 inside the general
+// chain when fast_tail declines.  Otherwise (dtopk_select_begin) pass 3 and K2b
+// run here, so that theta_slot holds theta when the call returns.
+template <int MODE>
+void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, const Layout& L, cudaStream_t s, int nsm,
+               void* const* ev, bool fused = false, GraphCtx* gc = nullptr) {
+  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
+  rec(ev, 0, s);
+  u32* D = reinterpret_cast<u32*>(ws + L.D);
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  const bool filt = filt_possible(L.S, alpha, beta, 0);
+  if (filt) {
+    const int g0 = grid_for(((L.S - 1) / K0_GROUP + 255) / 256, nsm * 8);
+    if (beta == 2)
+      k0_sample<MODE, 2><<<g0, 256, 0, s>>>(keys, alpha, L.S, k, L.D_len, ctrl);
+    else
+      k0_sample<MODE, 1><<<g0, 256, 0, s>>>(keys, alpha, L.S, k, L.D_len, ctrl);
+    counted();
+  }
+  stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm, filt ? 1 : 0);
+  rec(ev, 1, s);
+  const bool g = gc != nullptr && filt;
+  const K2Args k2 = k2_args(ws, L, k, beta, alpha, filt ? 1 : 0, g ? gc->fb : cudaGraphConditionalHandle{}, g ? 1 : 0);
+  if (beta == 2)
+    launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
+  else
+    launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, s, k2);
+  counted();
+  if (filt) {
+    // the sampled floor missed theta's bucket: full K1 (D + meta) and K2 again.
+    // Graph: the body of a conditional node K2 sets; eager: both exit at once
+    // unless ctrl->filt_fail is set.
+    cudaStream_t fs = s;
+    if (g) {
+      gc->ok = gc->ok && cond_begin(s, gc->fb, gc->s6);
+      fs = gc->s6;
+    }
+    stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, fs, nsm, 2);
+    const K2Args k2f = k2_args(ws, L, k, beta, alpha, 2);
+    if (beta == 2)
+      launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, fs, k2f);
+    else
+      launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, fs, k2f);
+    counted();
+    if (g) gc->ok = gc->ok && cond_end(gc->s6);
+  }
+  if (!fused) theta_resolve(ws, L, k, beta, s, nsm);
+  rec(ev, 2, s);
+}
+
+SortBufs sort_bufs(char* ws, const Layout& L, bool direct) {
+  SortBufs b;
+  b.ka = reinterpret_cast<u32*>(ws + (direct ? L.sak : L.gt_keys));
+  b.ia = reinterpret_cast<u64*>(ws + (direct ? L.sai : L.gt_idx));
+  b.kb = reinterpret_cast<u32*>(ws + L.sbk);
+  b.ib = reinterpret_cast<u64*>(ws + L.sbi);
+  b.counts = reinterpret_cast<u32*>(ws + L.counts);
+  b.digit_base = reinterpret_cast<u32*>(ws + L.digit_base);
+  b.digit_tot = reinterpret_cast<u32*>(ws + L.digit_tot);
+  return b;
+}
+
+void run_sort(Ctrl* ctrl, const SortBufs& b, const Layout& L, cudaStream_t s, int nsm) {
+  const int g = grid_for(L.sort_tiles, nsm * 4);
+  for (int p = 0; p < 4; p++) {
+    sort_hist<<<g, 256, 0, s>>>(ctrl, b, p);
+    counted();
+    sort_scan<<<32, 256, 0, s>>>(ctrl, b, p);
+    counted();
+    sort_scatter<<<g, 256, 0, s>>>(ctrl, b, p);
+    counted();
+  }
 }
 
 template <int MODE>
@@ -770,9 +838,12 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
             cudaStreamCreateWithFlags(&gc.s3, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&gc.s4, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&gc.s5, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&gc.s6, cudaStreamNonBlocking) == cudaSuccess &&
             cudaGraphCreate(&p->graph, 0) == cudaSuccess &&
             cudaGraphConditionalHandleCreate(&gc.cond, p->graph, 0, cudaGraphCondAssignDefault) == cudaSuccess &&
             cudaGraphConditionalHandleCreate(&gc.gen, p->graph, 1, cudaGraphCondAssignDefault) == cudaSuccess &&
+            (!filt_possible(L.S, alpha, beta, direct) ||
+             cudaGraphConditionalHandleCreate(&gc.fb, p->graph, 0, cudaGraphCondAssignDefault) == cudaSuccess) &&
             cudaStreamBeginCaptureToGraph(p->cap, p->graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
                 cudaSuccess;
   if (ok) {
@@ -787,7 +858,7 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
                     nsm, nullptr);
     } else {
       const bool fused = alpha <= FT_MAX_ALPHA;
-      DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, nullptr, fused);
+      DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, nullptr, fused, &gc);
       DISPATCH_MODE(key_mode(dtype, largest), run_finish, kp, n, k, alpha, beta, flags, nullptr, out_values,
                     out_indices, index_offset, w, L, s, nsm, nullptr, &gc, fused);
     }
@@ -798,7 +869,7 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
     p->main_kernels = gc.main_kernels;
     p->body_kernels = gc.body_kernels;
   }
-  for (cudaStream_t x : {gc.s2, gc.s3, gc.s4, gc.s5})
+  for (cudaStream_t x : {gc.s2, gc.s3, gc.s4, gc.s5, gc.s6})
     if (x) cudaStreamDestroy(x);
   if (!ok) {
     cudaGetLastError();

@@ -171,8 +171,11 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const u32 j = j0 + u * 32 + lane;
-        if (j < cnt && d1[u] >= theta && beta != 2) {  // D gathered for qualifying entries only
-          d2[u] = beta >= 2 ? a.D[(u64)sid[u] * beta + 1] : d1[u];
+        if (beta == 1) {  // d_beta = d_1 (D may be unwritten: filtered K1 pass)
+          d2[u] = d1[u];
+          dl[u] = d1[u];
+        } else if (j < cnt && d1[u] >= theta && beta != 2) {  // D gathered for qualifying entries only
+          d2[u] = a.D[(u64)sid[u] * beta + 1];
           dl[u] = a.D[(u64)sid[u] * beta + beta - 1];
         }
       }

@@ -152,6 +152,12 @@ struct Ctrl {
   u32 sort_done;   // last-block counter of sort_scan
   u32 lsd_fallback;
   u32 bk_ticket;     // last-block counter of bucket_scan  // large answer too skewed for the bucket sort: LSD radix sort instead
+  // filtered delegate pass (K0 sample -> K1 records -> K2 over records; delegate.cuh)
+  u32 filt_on;    // K0: K1 writes records of subranges with d_1 >= filt_t instead of D / meta
+  u32 filt_t;     // K0: floor of the sample bucket at ~1.25 k delegates (a lower bound of theta's bucket floor)
+  u32 filt_fail;  // K2: the floor was above theta's bucket (or the bucket is huge): full K1 + K2 rerun
+  u32 samp_done;  // K0 last-CTA counter
+  alignas(16) ull samp_hist[NBD1];  // K0: first-digit histogram of the sampled subranges' delegates
 };
 
 enum BigMode : u32 { BIG_NONE = 0, BIG_MERGE = 1, BIG_SORT_POOL = 2, BIG_SELECT = 3 };

@@ -62,6 +62,14 @@ struct K1Args {
   int do_hist;
   u32* meta;     // [S] (min(c1, 0xffff) << 16) | (p1 & 0xffff): count and position of the max
   u32* pmeta;    // [2 * nchunks] c1 / p1 of the chunk partials (alpha > K1_LOG_CHUNK)
+  // filtered mode (alpha 6..8, beta <= 2; see k0_sample): fmode 0 = always full
+  // (D + meta), 1 = records {sid, d_1, d_2, meta} of the subranges with d_1 >=
+  // ctrl->filt_t when ctrl->filt_on (else full), 2 = full, only if ctrl->filt_fail
+  Ctrl* ctrl;
+  int fmode;
+  uint4* frec;     // per consumer warp of the grid, a contiguous stream of fcap records
+  u32* chunk_cnt;  // [nchunks] (offset of chunk c's records in its warp's stream << 6) | count
+  u64 fcap;        // records per warp stream: ceil(nchunks / (grid * 8)) * (2048 >> alpha)
 };
 
 // Per-lane accumulator: top-B ladder, uint4 index p of the running maximum
@@ -238,6 +246,33 @@ __device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 s
   }
 }
 
+// Filtered emission (alpha >= 6: one call per chunk, every lane calls): the
+// delegates still feed the first-digit histogram, but only subranges whose max
+// delegate reaches the sampled floor `ft` are stored, as superset-format
+// records appended to the warp's own contiguous stream (`wrun` records so far);
+// lane 0 stores the chunk's (stream offset, count).  D and meta are not written
+// at all.  Measured (tools/k1_alpha.py): at alpha 6 the full D + meta writes
+// cost K1 ~90 us, chunk-strided record slots (one partial line per chunk) ~43
+// us; dense per-warp streams touch ~4x fewer lines.
+template <int B>
+__device__ __forceinline__ void emit_filtered(const K1Args& a, u32* shist, u64 c, u64 sid, bool leader,
+                                              const u32 (&L)[B], u32 meta, u32 ft, u32& wrun) {
+  const bool w = leader && sid < a.S;
+  const bool keep = w && L[0] >= ft;
+  const u32 q = __ballot_sync(FULL, keep);
+  const u32 base = (blockIdx.x * K1_CWARPS + (threadIdx.x >> 5)) * (u32)a.fcap;
+  if (keep && DTOPK_K1_EXP != 6)
+    a.frec[(u64)base + wrun + __popc(q & lanemask_lt())] = make_uint4((u32)sid, L[0], B >= 2 ? L[1] : 0u, meta);
+  if ((threadIdx.x & 31) == 0 && DTOPK_K1_EXP != 5) a.chunk_cnt[c] = (wrun << 6) | __popc(q);
+  wrun += __popc(q);
+  if (a.do_hist) {
+    if constexpr (K1_HCOPIES > 1) shist += (threadIdx.x & (K1_HCOPIES - 1)) * NBD1;
+#pragma unroll
+    for (int i = 0; i < B; i++)
+      if (w) atomicAdd(&shist[ddig1(L[i])], 1u);
+  }
+}
+
 template <int MODE, bool TAIL>
 __device__ __forceinline__ u32 k1_fetch(const K1Args& a, u64 start, u32 e, u32 cnt, u32 tcnt, u32 smv) {
   if constexpr (!TAIL) {
@@ -288,7 +323,8 @@ __device__ __forceinline__ u32 finalize_meta(const K1Args& a, const uint4* st4, 
 // done -- before the subrange butterflies and the delegate stores -- and then
 // returns true; otherwise the caller releases it.
 template <int MODE, int B, bool TAIL>
-__device__ __forceinline__ bool k1_warp_chunk(const K1Args& a, const u32* stage, u64 c, u32* shist, u64* rel) {
+__device__ __forceinline__ bool k1_warp_chunk(const K1Args& a, const u32* stage, u64 c, u32* shist, u64* rel,
+                                              bool filt, u32 ft, u32& wrun) {
   const int lane = threadIdx.x & 31;
   const u64 start = c << K1_LOG_CHUNK;
   const u32 cnt = TAIL ? (u32)min((u64)K1_CHUNK, a.n - start) : (u32)K1_CHUNK;
@@ -394,7 +430,10 @@ __device__ __forceinline__ bool k1_warp_chunk(const K1Args& a, const u32* stage,
   const u64 wmask = (1ull << alpha) - 1;
   if (alpha <= K1_LOG_CHUNK) {
     const u32 meta = pack_meta(A0.mn == A0.L[0], (u32)((start + A0.p) & wmask));
-    emit_subrange<B>(a, shist, (start + q0 * 4u) >> alpha, (lane & (G - 1)) == 0, A0.L, meta, G == 32);
+    if (B <= 2 && filt)
+      emit_filtered<B>(a, shist, c, (start + q0 * 4u) >> alpha, (lane & (G - 1)) == 0, A0.L, meta, ft, wrun);
+    else
+      emit_subrange<B>(a, shist, (start + q0 * 4u) >> alpha, (lane & (G - 1)) == 0, A0.L, meta, G == 32);
   } else {
     // W > 2048: this chunk is one part of a subrange -> partial ladder + the
     // exact offset of its max inside the subrange + its minimum
@@ -411,8 +450,9 @@ __device__ __forceinline__ bool k1_warp_chunk(const K1Args& a, const u32* stage,
 // The (single) ragged last chunk goes through an out-of-line copy so the bounds
 // checks do not inflate the register budget of the steady-state loop.
 template <int MODE, int B>
-__device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stage, u64 c, u32* shist) {
-  k1_warp_chunk<MODE, B, true>(a, stage, c, shist, nullptr);
+__device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stage, u64 c, u32* shist, bool filt,
+                                                u32 ft, u32& wrun) {
+  k1_warp_chunk<MODE, B, true>(a, stage, c, shist, nullptr, filt, ft, wrun);
 }
 
 #ifndef DTOPK_K1_EVICT_FIRST
@@ -422,6 +462,14 @@ __device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stag
 template <int MODE, int B>
 __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   pdl_trigger();
+  if (a.fmode == 2 && !ld_volatile_u32(&a.ctrl->filt_fail)) return;  // fallback pass not needed
+#ifdef DTOPK_K1_FORCE_FT  // profiling only (tools/k1_alpha.py): filtered emission with a fixed floor
+  const bool filt = a.alpha >= 6 && a.alpha <= 11;
+  const u32 ft = DTOPK_K1_FORCE_FT;
+#else
+  const bool filt = a.fmode == 1 && ld_volatile_u32(&a.ctrl->filt_on) != 0;
+  const u32 ft = filt ? ld_volatile_u32(&a.ctrl->filt_t) : 0u;
+#endif
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   u32* stages = reinterpret_cast<u32*>(smem_raw);
   u64* full = reinterpret_cast<u64*>(smem_raw + (size_t)K1_STAGES * K1_CHUNK * 4);
@@ -470,6 +518,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
     }
   } else {
     u64 i = warp;
+    u32 wrun = 0;  // records in this warp's stream (filtered mode)
     for (u64 c = blockIdx.x + (u64)warp * gridDim.x; c < nch; c += (u64)K1_CWARPS * gridDim.x, i += K1_CWARPS) {
       const u32 s = (u32)(i % K1_STAGES);
       const u32 ph = (u32)(i / K1_STAGES) & 1u;
@@ -482,9 +531,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
       }
       bool released = false;
       if (((c + 1) << K1_LOG_CHUNK) <= a.n)
-        released = k1_warp_chunk<MODE, B, false>(a, st, c, shist, &empty[s]);
+        released = k1_warp_chunk<MODE, B, false>(a, st, c, shist, &empty[s], filt, ft, wrun);
       else
-        k1_warp_chunk_tail<MODE, B>(a, st, c, shist);
+        k1_warp_chunk_tail<MODE, B>(a, st, c, shist, filt, ft, wrun);
       if (!released) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -499,6 +548,76 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
       for (int h = 0; h < K1_HCOPIES; h++) v += shist[h * NBD1 + i];
       if (v) atomicAdd(&a.hist1[i], (ull)v);
     }
+  }
+}
+
+// K0: sample for the filtered delegate pass.  One subrange per group of
+// K0_GROUP (position hashed inside the group) is reduced to its top-B
+// delegates (16 loads in flight per thread) and histogrammed on the first radix
+// digit; the last CTA picks the
+// floor of the bucket holding sample rank r_s ~ (1.25 k + 64) * f (+4 sigma),
+// f = sampled share of D.  With probability ~1 that floor lies at or below
+// theta's bucket floor (K2 verifies it exactly and falls back to the full
+// pass otherwise), so K1 need only store subranges whose max delegate reaches
+// it.  The filter stays off when the chosen buckets hold more than a quarter
+// of the sample (tie-heavy / narrow-range input: the floor would keep most
+// subranges).  Reads 1/K0_GROUP of the input.
+constexpr int K0_GROUP = 128;
+
+template <int MODE, int B>
+__global__ void __launch_bounds__(256) k0_sample(const u32* __restrict__ keys, int alpha, u64 S, u64 k, u64 nD,
+                                                 Ctrl* ctrl) {
+  __shared__ u32 sh[NBD1];
+  __shared__ ull scratch[8];
+  __shared__ DigitResult res;
+  __shared__ int am_last;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NBD1; i += 256) sh[i] = 0;
+  __syncthreads();
+  const u64 ng = (S - 1) / K0_GROUP;  // whole groups, the (possibly ragged) last subrange excluded
+  const u32 nq = 1u << (alpha - 2);   // uint4 per subrange (a multiple of 16 for alpha >= 6)
+  for (u64 g = (u64)blockIdx.x * 256 + tid; g < ng; g += (u64)gridDim.x * 256) {
+    const u64 sid = g * K0_GROUP + (((u32)g * 0x9E3779B1u) >> 25);
+    const uint4* p = reinterpret_cast<const uint4*>(keys + (sid << alpha));
+    u32 L0 = 0, L1 = 0;
+    for (u32 q = 0; q < nq; q += 16) {  // 16 independent 16-byte loads in flight per thread
+      uint4 v[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) v[j] = ld_nc_v4(p + q + j);
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const u32 x[4] = {to_key<MODE>(v[j].x), to_key<MODE>(v[j].y), to_key<MODE>(v[j].z), to_key<MODE>(v[j].w)};
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          if (B >= 2) L1 = max(L1, min(L0, x[c]));
+          L0 = max(L0, x[c]);
+        }
+      }
+    }
+    atomicAdd(&sh[ddig1(L0)], 1u);
+    if (B >= 2) atomicAdd(&sh[ddig1(L1)], 1u);
+  }
+  __syncthreads();
+  for (int i = tid; i < NBD1; i += 256)
+    if (sh[i]) atomicAdd(&ctrl->samp_hist[i], (ull)sh[i]);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = atomicAdd(&ctrl->samp_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  const ull ns = ng * (u64)B;
+  const double f = (double)ns / (double)nD;
+  const double R = (double)k * 1.25 + 64.0;
+  const ull rs = (ull)ceil(R * f + 4.0 * sqrt(R * f) + 8.0);
+  find_digit<NBD1>(ctrl->samp_hist, rs, &res, scratch);
+  if (tid == 0) {
+    const bool on = ns > 0 && rs <= ns && res.valid && (res.above + res.cnt) * 4 <= ns;
+    u32 kmin, kmax;
+    dbucket_range(res.digit, kmin, kmax);
+    ctrl->filt_t = kmin;
+    ctrl->filt_on = on ? 1u : 0u;
+    ctrl->res.filtered = on ? 1u : 0u;
   }
 }
 

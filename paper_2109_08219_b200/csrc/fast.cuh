@@ -441,8 +441,11 @@ __global__ void __launch_bounds__(FT_THREADS, 1) fast_tail(FTArgs a) {
 #pragma unroll
     for (int q = 0; q < FT_RPT; q++) {
       if (keep[q]) {
-        if (beta != 2) {
-          d2[q] = beta >= 2 ? a.D[(u64)sid[q] * beta + 1] : d1[q];
+        if (beta == 1) {  // d_beta = d_1 (D may be unwritten: filtered K1 pass)
+          d2[q] = d1[q];
+          dl[q] = d1[q];
+        } else if (beta != 2) {
+          d2[q] = a.D[(u64)sid[q] * beta + 1];
           dl[q] = a.D[(u64)sid[q] * beta + beta - 1];
         }
         nk++;

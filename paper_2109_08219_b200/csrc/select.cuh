@@ -16,6 +16,8 @@
 
 namespace dtopk {
 
+constexpr int K1_LOG_CHUNK_ = 11;  // keys per K1 chunk = 2^11 (delegate.cuh K1_LOG_CHUNK)
+
 struct K2Args {
   const u32* D;
   u64 nD;      // beta * S delegates
@@ -32,6 +34,17 @@ struct K2Args {
   u32* sup_cnt;  // [g2 * 8] entries of each segment
   u32* sup_off;  // [g2 * 8 + 1] exclusive prefix of sup_cnt (theta resolver)
   const u32* meta;  // [S] K1 meta words, copied into the superset entries
+  // filtered delegate pass (K1 fmode): 1 = scan K1's records when ctrl->filt_on,
+  // 2 = fallback full scan, only when ctrl->filt_fail
+  int fmode;
+  const u32* chunk_cnt;  // [nch] (offset << 6) | count of K1 chunk c's records in its warp's stream
+  const uint4* frec;     // K1 record streams: chunk c was reduced by warp (c % g1, (c / g1) % 8)
+  u64 fcap;              // records per stream
+  u32 g1;                // K1 grid
+  u64 nch;
+  int alpha;
+  cudaGraphConditionalHandle fb;  // graph: set when the fallback must run
+  int fb_graph;
 };
 
 #ifndef DTOPK_K2_MINB
@@ -100,6 +113,75 @@ __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, co
   k2_superset_prefix(ctrl, nregions, sup_cnt, sup_off, scratch);
 }
 
+// K2 over K1's records (filtered pass): warp w of the grid owns a contiguous
+// range of K1 chunks; per 32 chunks the lanes read the (offset, count) words, a
+// warp scan flattens the counts, and lane l handles records l, l+32, ... (its
+// chunk by a 5-step shuffle search over the exclusive prefix).  Chunk c's
+// records sit in the stream of the K1 warp that reduced it.  Superset entries
+// (d_1 >= kmin) are compacted, in subrange order, into the warp's superset
+// segment; bucket members (d_1, d_2 in [kmin, kmax]) feed the digit-2
+// histogram and the CTA's selbuf region exactly as in the scan of D.
+template <int BETA2>
+__device__ __noinline__ void k2_records(const K2Args& a, u32 kmin, u32 span, u32* shist, u32* s_cnt, u32* region,
+                                        u64& out0_o, u32& run_o) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const u64 nseg = (u64)gridDim.x * 8;
+  const u64 seg = (u64)blockIdx.x * 8 + warp;
+  const u64 cpw = (a.nch + nseg - 1) / nseg;
+  const u64 c0 = min(a.nch, seg * cpw), c1 = min(a.nch, c0 + cpw);
+  const int lspc = K1_LOG_CHUNK_ - a.alpha;
+  const u64 out0 = c0 << lspc;
+  const u32 lt = lanemask_lt();
+  u32 run = 0;
+  for (u64 cb = c0; cb < c1; cb += 32) {
+    const u64 c = cb + lane;
+    const u32 word = c < c1 ? __ldcg(a.chunk_cnt + c) : 0u;
+    const u32 cnt = word & 63u;
+    // start of chunk c's records: its K1 warp's stream + the offset in it
+    const u64 src = ((u64)((c % a.g1) * 8 + (c / a.g1) % 8)) * a.fcap + (word >> 6);
+    const u32 incl = warp_incl_scan<u32>(cnt);
+    const u32 excl = incl - cnt;
+    const u32 tot = __shfl_sync(FULL, incl, 31);
+    for (u32 r0 = 0; r0 < tot; r0 += 32) {
+      const u32 r = r0 + lane;
+      int j = 0;
+#pragma unroll
+      for (int st = 16; st; st >>= 1) {
+        const u32 e = __shfl_sync(FULL, excl, j + st);
+        if (e <= r) j += st;
+      }
+      const u32 ej = __shfl_sync(FULL, excl, j);
+      const u64 sj = __shfl_sync(FULL, src, j);
+      const bool v = r < tot;
+      uint4 e = make_uint4(0u, 0u, 0u, 0u);
+      if (v) e = __ldcg(&a.frec[sj + (r - ej)]);
+      const bool keep = v && e.y >= kmin;
+      const u32 qk = __ballot_sync(FULL, keep);
+      if (keep) a.sup_sid[out0 + run + __popc(qk & lt)] = e;
+      run += __popc(qk);
+      const bool m1 = v && e.y - kmin <= span;
+      const bool m2 = BETA2 && v && e.z - kmin <= span;
+      const u32 nb = (m1 ? 1u : 0u) + (m2 ? 1u : 0u);
+      const u32 wnb = __reduce_add_sync(FULL, nb);
+      if (wnb == 0) continue;
+      const u32 inb = warp_incl_scan<u32>(nb);
+      u32 o = 0;
+      if (lane == 31) o = atomicAdd(s_cnt, inb);
+      o = __shfl_sync(FULL, o, 31) + inb - nb;
+      if (m1) {
+        atomicAdd(&shist[(e.y - kmin) >> DSH3], 1u);
+        region[o++] = e.y;
+      }
+      if (m2) {
+        atomicAdd(&shist[(e.z - kmin) >> DSH3], 1u);
+        region[o] = e.z;
+      }
+    }
+  }
+  out0_o = out0;
+  run_o = run;
+}
+
 // K2: pass 2 of kth(D) -- one read of D.  CTA c owns the contiguous range
 // [c*R, (c+1)*R) of D and each of its warps one eighth of it.  A warp step is
 // 512 delegates, 16 consecutive ones per lane (four uint4).  theta's digit-1
@@ -121,6 +203,8 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
   __shared__ ull scratch[8];
   __shared__ u32 s_cnt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.fmode == 2 && !ld_volatile_u32(&a.ctrl->filt_fail)) return;  // fallback scan not needed
+  const bool records = a.fmode == 1 && ld_volatile_u32(&a.ctrl->filt_on) != 0;
   for (int i = tid; i < NBD2; i += 256) shist[i] = 0;
   if (tid == 0) s_cnt = 0;
   find_digit<NBD1>(a.ctrl->selD.hist1, a.k, &r1, scratch);
@@ -128,12 +212,23 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
   u32 kmin, kmax;
   dbucket_range(r1.digit, kmin, kmax);
   const u32 span = kmax - kmin;
+  if (records && (ld_volatile_u32(&a.ctrl->filt_t) > kmin || r1.cnt * 4 > a.nD)) {
+    // the sampled floor missed theta's bucket (or the bucket is a large share of
+    // D, which pass 3 / K2b resolve from D itself): D was not written, so the
+    // full K1 + K2 run again (fmode 2 launches) -- nothing is written here
+    if (blockIdx.x == 0 && tid == 0) {
+      a.ctrl->filt_fail = 1u;
+      a.ctrl->res.filter_fallback = 1u;
+      if (a.fb_graph) cudaGraphSetConditional(a.fb, 1u);
+    }
+    return;
+  }
   const u64 lo = (u64)blockIdx.x * a.R;
   const u64 hi = min(a.nD, lo + a.R);
   const u64 wlen = a.R / 8;
   const u64 wlo = min(hi, lo + (u64)warp * wlen), whi = min(hi, wlo + wlen);
   const u64 beta = BETA2 ? 2u : (u64)a.beta;
-  const u64 out0 = (wlo + beta - 1) / beta;  // first subrange whose d_1 lies in [wlo, whi)
+  u64 out0 = (wlo + beta - 1) / beta;  // first subrange whose d_1 lies in [wlo, whi)
   u32* region = a.selbuf + lo;
   // a bucket holding a large share of D (tie-heavy / narrow range): the bucket
   // floor says little, so the superset is left to K2b, which filters D with
@@ -143,7 +238,8 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
   // not copy it into the regions; pass 3 scans D itself (same bytes, no writes)
   const bool compact = r1.cnt * 4 <= a.nD;
   u32 run = 0;
-  for (u64 base = wlo; base < whi; base += 512) {
+  if (records) k2_records<BETA2>(a, kmin, span, shist, &s_cnt, region, out0, run);
+  for (u64 base = records ? whi : wlo; base < whi; base += 512) {
     const u64 i0 = base + (u64)lane * 16;
     u32 v[16];
 #pragma unroll

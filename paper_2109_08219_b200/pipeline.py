@@ -13,7 +13,7 @@ caller's current CUDA stream:
   SecondK       radix select over the pool when it exceeds k, ordered emit,
                 stable radix sort by key, write-out in the input dtype
 
-and synchronises once, to read the 104-byte result header.  There is no CPU
+and synchronises once, to read the 112-byte result header.  There is no CPU
 fallback: without libdtopk.so or a CUDA device the call raises.
 
 The stage-inspection functions ``first_topk`` / ``concatenate_filtered``

@@ -1,0 +1,121 @@
+"""GPU parity of the filtered delegate pass (K0 sample -> K1 records -> K2 over
+records, csrc/delegate.cuh / select.cuh) and of its fallback.
+
+For alpha 6..8 and beta <= 2, K1 stores only the subranges whose max delegate
+reaches a floor sampled from 1/128 of the subranges; K2 checks that the floor
+lies at or below theta's first-digit bucket and otherwise re-runs the full K1 +
+K2.  Either way the answer must equal the oracle's bit for bit (values,
+indices, the reference counters of pipeline.py:87-159).  The fallback is forced
+with inputs whose sampled subranges hold the largest keys, so the sample
+overestimates theta.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2109_08219_b200 as dtopk
+from paper_2109_08219_b200 import _native, data
+from paper_2109_08219_b200.pipeline import DrTopK
+
+from test_gpu_parity import check_topk
+
+pytestmark = pytest.mark.gpu
+
+K0_GROUP = 128
+
+
+def sampled_sids(S: int) -> np.ndarray:
+    """Subranges K0 samples (k0_sample: one per group of 128, hashed position)."""
+    g = np.arange((S - 1) // K0_GROUP, dtype=np.uint64)
+    off = ((g.astype(np.uint32) * np.uint32(0x9E3779B1)) >> np.uint32(25)).astype(np.uint64)
+    return (g * K0_GROUP + off).astype(np.int64)
+
+
+def adversarial_for_sample(n: int, alpha: int, cuda, dtype=torch.uint32):
+    """Uniform keys below 2^31, except the sampled subranges, lifted above 2^31."""
+    v = data.generate("uniform", n, seed=3, device=cuda)
+    vi = v.view(torch.int32)
+    vi &= 0x7FFFFFFF
+    sids = torch.from_numpy(sampled_sids(-(-n >> alpha))).to(cuda)
+    W = 1 << alpha
+    rows = vi[: (n >> alpha) << alpha].view(-1, W)
+    rows[sids] |= torch.tensor(-0x80000000, dtype=torch.int32, device=cuda)
+    return v
+
+
+def header(r):
+    return r.stats.device
+
+
+@pytest.mark.parametrize("alpha,k", [(6, 4096), (7, 3000), (8, 1000), (6, 8192)])
+@pytest.mark.parametrize("beta", [1, 2])
+def test_filtered_pass_matches_oracle(alpha, k, beta, oracle_mod, cuda):
+    n = (1 << 24) + 4099  # ragged tail chunk and tail subrange
+    v = data.generate("uniform", n, seed=alpha * 7 + beta, device=cuda)
+    r = check_topk(v, k, oracle_mod, alpha=alpha, auto_alpha=False, beta=beta)
+    assert header(r)["filtered"] == 1 and header(r)["filter_fallback"] == 0
+
+
+@pytest.mark.parametrize("largest", [True, False])
+def test_filtered_pass_f32(largest, oracle_mod, cuda):
+    """float32 at alpha 7 (the first digit is log-scale from the top of the key
+    range, so N(0,1) keys may share one bucket and keep the filter off: parity
+    either way)."""
+    v = data.generate("normal_f32", 1 << 24, seed=5, device=cuda)
+    check_topk(v, 30000, oracle_mod, largest=largest, alpha=7, auto_alpha=False)
+
+
+@pytest.mark.parametrize("alpha,k", [(6, 20000), (8, 4000)])
+def test_filter_fallback_eager(alpha, k, oracle_mod, cuda):
+    v = adversarial_for_sample(1 << 24, alpha, cuda)
+    r = check_topk(v, k, oracle_mod, alpha=alpha, auto_alpha=False)
+    assert header(r)["filtered"] == 1 and header(r)["filter_fallback"] == 1
+
+
+def test_filter_fallback_graph_plan(oracle_mod, cuda):
+    """The fallback as a conditional node of the plan's CUDA graph; the same plan
+    then replays on data where the sample is representative (no fallback)."""
+    n, alpha, k = 1 << 24, 6, 20000
+    v = adversarial_for_sample(n, alpha, cuda)
+    cfg = dtopk.PipelineConfig(k=k, alpha=alpha, auto_alpha=False)
+    p = DrTopK(n, cfg, _native.DTYPE_U32, torch.uint32, cuda, use_graph=True)
+    for adversarial in (True, False, True):
+        v.copy_(adversarial_for_sample(n, alpha, cuda) if adversarial else data.generate("uniform", n, seed=9,
+                                                                                         device=cuda))
+        p.launch(v)
+        torch.cuda.synchronize()
+        keys = v.cpu().numpy()
+        ek, ei = oracle_mod.topk_with_indices(keys, k)
+        np.testing.assert_array_equal(p.indices.cpu().numpy(), ei)
+        np.testing.assert_array_equal(p.values.cpu().numpy(), ek)
+        assert int(p.header().filter_fallback) == (1 if adversarial else 0)
+
+
+def test_filter_off_on_ties(oracle_mod, cuda):
+    """Tie-heavy input: the sampled bucket holds most of the sample, the filter
+    stays off and the full pass runs."""
+    v = data.generate("few_distinct", 1 << 24, seed=1, device=cuda)
+    r = check_topk(v, 1 << 15, oracle_mod, alpha=6, auto_alpha=False)
+    assert header(r)["filtered"] == 0
+
+
+def test_sharded_begin_uses_filter(oracle_mod, cuda):
+    """dtopk_select_begin / finish (the multi-GPU split) with the filtered pass."""
+    n, k = 1 << 24, 1 << 15
+    v = data.generate("uniform", n, seed=12, device=cuda)
+    cfg = dtopk.validate_config(dtopk.PipelineConfig(k=k, alpha=6, auto_alpha=False), n)
+    p = DrTopK(n, cfg, _native.DTYPE_U32, torch.uint32, cuda, timed=False)
+    s = torch.cuda.current_stream()
+    lib = p.lib
+    _native.check(lib.dtopk_select_begin(v.data_ptr(), n, _native.DTYPE_U32, k, 1, cfg.alpha, cfg.beta, 0,
+                                         p.ws.data_ptr(), p.ws_bytes, s.cuda_stream, None), "begin")
+    _native.check(lib.dtopk_select_finish(v.data_ptr(), n, _native.DTYPE_U32, k, 1, cfg.alpha, cfg.beta, 0, None,
+                                          p.values.data_ptr(), p.indices.data_ptr(), 0, p.ws.data_ptr(), p.ws_bytes,
+                                          s.cuda_stream, None), "finish")
+    torch.cuda.synchronize()
+    ek, ei = oracle_mod.topk_with_indices(v.cpu().numpy(), k)
+    np.testing.assert_array_equal(p.indices.cpu().numpy(), ei)
+    assert int(p.header().filtered) == 1

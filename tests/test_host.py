@@ -140,7 +140,7 @@ def test_library_host_only_entry_points():
     lib = _native.load(require_cuda=False)
     assert lib.dtopk_version().startswith(b"dtopk-b200")
     assert lib.dtopk_result_offset() == 0
-    assert ctypes.sizeof(_native.DtopkResult) == 104
+    assert ctypes.sizeof(_native.DtopkResult) == 112
     # workspace sizing is host arithmetic
     ws1 = lib.dtopk_workspace_bytes(1 << 30, 1024, 11, 2, 0)
     ws2 = lib.dtopk_workspace_bytes(1 << 30, 1 << 20, 6, 2, 0)

@@ -28,7 +28,9 @@ def table(path):
             order.append(lid)
         launches[lid][r[mi]] = float(r[vi].replace(",", ""))
     out = [launches[i] for i in order]
-    first = max(i for i, o in enumerate(out) if o["name"].startswith("k1_delegates"))
+    starts = [i for i, o in enumerate(out) if o["name"].startswith("k0_sample")] or \
+        [i for i, o in enumerate(out) if o["name"].startswith("k1_delegates")]
+    first = max(starts)
     return out[first:]
 
 
