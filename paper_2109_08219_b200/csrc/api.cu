@@ -127,7 +127,8 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.sup_cnt = take(std::max<u64>((u64)L.g2 * 8, 256 * K2_SEG_PER) * 4);  // padded: read as uint4 by thread
   L.sup_off = take(((u64)L.g2 * 8 + 1) * 4);
   // K3 records; in a filtered call first K1's per-warp record streams (K1 grid x 8 warps x fcap)
-  L.fcap = filt ? (L.nch + (u64)k1_grid(L.nch) * 8 - 1) / ((u64)k1_grid(L.nch) * 8) * (2048ull >> alpha) : 0;
+  // (a CTA reduces <= ceil(nch / grid) chunks, a warp <= ceil(that / 8))
+  L.fcap = filt ? ((L.nch + k1_grid(L.nch) - 1) / k1_grid(L.nch) + 7) / 8 * (2048ull >> alpha) : 0;
   L.rec = take(std::max<u64>(L.S, (u64)k1_grid(L.nch) * 8 * L.fcap) * 16);
   L.k5_tg = take(L.k5_tiles * 8);
   L.k5_te = take(L.k5_tiles * 8);
@@ -389,11 +390,12 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
   const bool filt = filt_possible(L.S, alpha, beta, 0);
   if (filt) {
-    const int g0 = grid_for(((L.S - 1) / K0_GROUP + 255) / 256, nsm * 8);
+    const u64 nch_full = n >> K1_LOG_CHUNK;
+    const int g0 = grid_for((K0_REGIONS * k0_run(nch_full) + 7) / 8, nsm * 4);
     if (beta == 2)
-      k0_sample<MODE, 2><<<g0, 256, 0, s>>>(keys, alpha, L.S, k, L.D_len, ctrl);
+      k0_sample<MODE, 2><<<g0, 256, 0, s>>>(keys, alpha, L.S, k, L.D_len, ctrl, nch_full);
     else
-      k0_sample<MODE, 1><<<g0, 256, 0, s>>>(keys, alpha, L.S, k, L.D_len, ctrl);
+      k0_sample<MODE, 1><<<g0, 256, 0, s>>>(keys, alpha, L.S, k, L.D_len, ctrl, nch_full);
     counted();
   }
   stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm, filt ? 1 : 0);

@@ -458,6 +458,21 @@ __device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stag
 #ifndef DTOPK_K1_EVICT_FIRST
 #define DTOPK_K1_EVICT_FIRST 1  // K1's input stream is marked L2 evict_first
 #endif
+#ifndef DTOPK_K1_CONTIG
+#define DTOPK_K1_CONTIG 0  // 1: CTA b reduces the contiguous chunk range [b R, (b+1) R), R = ceil(nch / grid)
+#endif
+
+// Chunk of iteration i of this CTA (iteration i uses ring stage i % K1_STAGES
+// and consumer warp i % K1_CWARPS), or ~0 past the CTA's last chunk.
+__device__ __forceinline__ u64 k1_chunk_of(u64 i, u64 nch) {
+  if (DTOPK_K1_CONTIG) {
+    const u64 R = (nch + gridDim.x - 1) / gridDim.x;
+    const u64 c = (u64)blockIdx.x * R + i;
+    return (i < R && c < nch) ? c : ~0ull;
+  }
+  const u64 c = blockIdx.x + i * gridDim.x;
+  return c < nch ? c : ~0ull;
+}
 
 template <int MODE, int B>
 __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
@@ -494,7 +509,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
     if (lane == 0) {
       u64 i = 0;
       const u64 pol = l2_policy_evict_first();
-      for (u64 c = blockIdx.x; c < nch; c += gridDim.x, i++) {
+      for (u64 c = k1_chunk_of(0, nch); c != ~0ull; c = k1_chunk_of(++i, nch)) {
         const u32 s = (u32)(i % K1_STAGES);
         const u32 ph = (u32)(i / K1_STAGES) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
@@ -519,7 +534,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   } else {
     u64 i = warp;
     u32 wrun = 0;  // records in this warp's stream (filtered mode)
-    for (u64 c = blockIdx.x + (u64)warp * gridDim.x; c < nch; c += (u64)K1_CWARPS * gridDim.x, i += K1_CWARPS) {
+    for (u64 c = k1_chunk_of(i, nch); c != ~0ull; i += K1_CWARPS, c = k1_chunk_of(i, nch)) {
       const u32 s = (u32)(i % K1_STAGES);
       const u32 ph = (u32)(i / K1_STAGES) & 1u;
       mbar_wait(&full[s], ph);
@@ -551,51 +566,86 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   }
 }
 
-// K0: sample for the filtered delegate pass.  One subrange per group of
-// K0_GROUP (position hashed inside the group) is reduced to its top-B
-// delegates (16 loads in flight per thread) and histogrammed on the first radix
-// digit; the last CTA picks the
-// floor of the bucket holding sample rank r_s ~ (1.25 k + 64) * f (+4 sigma),
-// f = sampled share of D.  With probability ~1 that floor lies at or below
-// theta's bucket floor (K2 verifies it exactly and falls back to the full
-// pass otherwise), so K1 need only store subranges whose max delegate reaches
-// it.  The filter stays off when the chosen buckets hold more than a quarter
-// of the sample (tie-heavy / narrow-range input: the floor would keep most
-// subranges).  Reads 1/K0_GROUP of the input.
-constexpr int K0_GROUP = 128;
+// K0: sample for the filtered delegate pass.  1/K0_GROUP of the K1 chunks
+// (2048 keys), as K0_REGIONS runs of consecutive chunks at hashed offsets (one
+// run per 1/K0_REGIONS of the input: a few hundred TLB entries instead of one
+// per sampled chunk, which made a scattered sample latency-bound), each chunk
+// read by one warp with coalesced 16-byte loads (uint4 j*32 + lane, all 16 in flight), its
+// subranges (alpha 6..8) are reduced to their top-B delegates with shuffles and
+// histogrammed on the first radix digit; the last CTA picks the floor of the
+// bucket holding sample rank r_s ~ (1.25 k + 64) * f (+4 sigma), f = sampled
+// share of D.  With probability ~1 that floor lies at or below theta's bucket
+// floor (K2 verifies it exactly and falls back to the full pass otherwise), so
+// K1 need only store subranges whose max delegate reaches it.  The filter
+// stays off when the chosen buckets hold more than a quarter of the sample
+// (tie-heavy / narrow-range input: the floor would keep most subranges).
+// Reads 1/K0_GROUP of the input.
+constexpr int K0_GROUP = 512;
+constexpr int K0_REGIONS = 64;
+__host__ __device__ __forceinline__ u64 k0_run(u64 nch_full) {
+  const u64 L = nch_full / (K0_REGIONS * K0_GROUP);
+  return L ? L : 1;
+}
+
+// top-2 (or top-1) merge of two ladders
+template <int B>
+__device__ __forceinline__ void k0_merge(u32& a0, u32& a1, u32 b0, u32 b1) {
+  if (B >= 2) a1 = max(min(a0, b0), max(a1, b1));
+  a0 = max(a0, b0);
+}
 
 template <int MODE, int B>
 __global__ void __launch_bounds__(256) k0_sample(const u32* __restrict__ keys, int alpha, u64 S, u64 k, u64 nD,
-                                                 Ctrl* ctrl) {
+                                                 Ctrl* ctrl, u64 nch_full) {
   __shared__ u32 sh[NBD1];
   __shared__ ull scratch[8];
   __shared__ DigitResult res;
   __shared__ int am_last;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < NBD1; i += 256) sh[i] = 0;
   __syncthreads();
-  const u64 ng = (S - 1) / K0_GROUP;  // whole groups, the (possibly ragged) last subrange excluded
-  const u32 nq = 1u << (alpha - 2);   // uint4 per subrange (a multiple of 16 for alpha >= 6)
-  for (u64 g = (u64)blockIdx.x * 256 + tid; g < ng; g += (u64)gridDim.x * 256) {
-    const u64 sid = g * K0_GROUP + (((u32)g * 0x9E3779B1u) >> 25);
-    const uint4* p = reinterpret_cast<const uint4*>(keys + (sid << alpha));
-    u32 L0 = 0, L1 = 0;
-    for (u32 q = 0; q < nq; q += 16) {  // 16 independent 16-byte loads in flight per thread
-      uint4 v[16];
+  // K0_REGIONS runs of L consecutive chunks, one per 1/K0_REGIONS of the input at
+  // a hashed offset: few pages (TLB entries) touched, 1/K0_GROUP of the chunks
+  const u64 slot = nch_full / K0_REGIONS, L = k0_run(nch_full);
+  const u64 ng = K0_REGIONS * L;
+  const u64 gw = ((u64)blockIdx.x * 256 + tid) >> 5, nw = ((u64)gridDim.x * 256) >> 5;
+  for (u64 g = gw; g < ng; g += nw) {
+    const u64 r = g / L;
+    const u64 c = r * slot + (((u32)r * 0x9E3779B1u) >> 16) % (slot - L + 1) + g % L;
+    const uint4* p = reinterpret_cast<const uint4*>(keys + (c << K1_LOG_CHUNK));
+    uint4 v[16];
 #pragma unroll
-      for (int j = 0; j < 16; j++) v[j] = ld_nc_v4(p + q + j);
+    for (int j = 0; j < 16; j++) v[j] = ld_nc_v4(p + j * 32 + lane);
+    u32 t0[16], t1[16];  // this lane's top-B of uint4 j*32 + lane
 #pragma unroll
-      for (int j = 0; j < 16; j++) {
-        const u32 x[4] = {to_key<MODE>(v[j].x), to_key<MODE>(v[j].y), to_key<MODE>(v[j].z), to_key<MODE>(v[j].w)};
+    for (int j = 0; j < 16; j++) {
+      const u32 x[4] = {to_key<MODE>(v[j].x), to_key<MODE>(v[j].y), to_key<MODE>(v[j].z), to_key<MODE>(v[j].w)};
+      const u32 h1 = max(x[0], x[1]), l1 = min(x[0], x[1]), h2 = max(x[2], x[3]), l2 = min(x[2], x[3]);
+      t0[j] = max(h1, h2);
+      t1[j] = max(min(h1, h2), max(l1, l2));
+    }
+    // alpha 6: 16 lanes per subrange and instruction; 7: 32; 8: 32 lanes x 2 instructions
+    const int G = alpha == 6 ? 16 : 32;
+    const int per = alpha >= 8 ? 2 : 1;
 #pragma unroll
-        for (int c = 0; c < 4; c++) {
-          if (B >= 2) L1 = max(L1, min(L0, x[c]));
-          L0 = max(L0, x[c]);
+    for (int j = 0; j < 16; j += 2) {
+      u32 a0 = t0[j], a1 = t1[j], b0 = t0[j + 1], b1 = t1[j + 1];
+      if (per == 2) {
+        k0_merge<B>(a0, a1, b0, b1);
+      }
+      for (int o = 1; o < G; o <<= 1) {
+        k0_merge<B>(a0, a1, __shfl_xor_sync(FULL, a0, o), __shfl_xor_sync(FULL, a1, o));
+        if (per == 1) k0_merge<B>(b0, b1, __shfl_xor_sync(FULL, b0, o), __shfl_xor_sync(FULL, b1, o));
+      }
+      if ((lane & (G - 1)) == 0) {
+        atomicAdd(&sh[ddig1(a0)], 1u);
+        if (B >= 2) atomicAdd(&sh[ddig1(a1)], 1u);
+        if (per == 1) {
+          atomicAdd(&sh[ddig1(b0)], 1u);
+          if (B >= 2) atomicAdd(&sh[ddig1(b1)], 1u);
         }
       }
     }
-    atomicAdd(&sh[ddig1(L0)], 1u);
-    if (B >= 2) atomicAdd(&sh[ddig1(L1)], 1u);
   }
   __syncthreads();
   for (int i = tid; i < NBD1; i += 256)
@@ -606,7 +656,7 @@ __global__ void __launch_bounds__(256) k0_sample(const u32* __restrict__ keys, i
   __syncthreads();
   if (!am_last) return;
   __threadfence();
-  const ull ns = ng * (u64)B;
+  const ull ns = K0_REGIONS * k0_run(nch_full) * (2048ull >> alpha) * (u64)B;  // sampled delegates
   const double f = (double)ns / (double)nD;
   const double R = (double)k * 1.25 + 64.0;
   const ull rs = (ull)ceil(R * f + 4.0 * sqrt(R * f) + 8.0);

@@ -14,9 +14,17 @@
 
 #include "common.cuh"
 
+#ifndef DTOPK_K1_CONTIG
+#define DTOPK_K1_CONTIG 0
+#endif
+
 namespace dtopk {
 
-constexpr int K1_LOG_CHUNK_ = 11;  // keys per K1 chunk = 2^11 (delegate.cuh K1_LOG_CHUNK)
+constexpr int K1_LOG_CHUNK_ = 11;
+#ifndef DTOPK_K2R_U
+#define DTOPK_K2R_U 4
+#endif
+constexpr int K2R_U = DTOPK_K2R_U;  // record loads in flight per lane (K2 over records)  // keys per K1 chunk = 2^11 (delegate.cuh K1_LOG_CHUNK)
 
 struct K2Args {
   const u32* D;
@@ -133,48 +141,66 @@ __device__ __noinline__ void k2_records(const K2Args& a, u32 kmin, u32 span, u32
   const u64 out0 = c0 << lspc;
   const u32 lt = lanemask_lt();
   u32 run = 0;
+  u32 word = (c0 + lane < c1) ? __ldcg(a.chunk_cnt + c0 + lane) : 0u;
   for (u64 cb = c0; cb < c1; cb += 32) {
     const u64 c = cb + lane;
-    const u32 word = c < c1 ? __ldcg(a.chunk_cnt + c) : 0u;
+    // the next 32 chunks' words are in flight while this batch is processed
+    const u32 next = (c + 32 < c1) ? __ldcg(a.chunk_cnt + c + 32) : 0u;
     const u32 cnt = word & 63u;
     // start of chunk c's records: its K1 warp's stream + the offset in it
-    const u64 src = ((u64)((c % a.g1) * 8 + (c / a.g1) % 8)) * a.fcap + (word >> 6);
+    // (K1 CTA b reduces chunks b + i g1, or [b R, (b+1) R) with DTOPK_K1_CONTIG; warp i % 8)
+#if DTOPK_K1_CONTIG
+    const u64 R1 = (a.nch + a.g1 - 1) / a.g1;
+    const u64 kw = (c / R1) * 8 + (c % R1) % 8;
+#else
+    const u64 kw = (c % a.g1) * 8 + (c / a.g1) % 8;
+#endif
+    const u64 src = kw * a.fcap + (word >> 6);
+    word = next;
     const u32 incl = warp_incl_scan<u32>(cnt);
     const u32 excl = incl - cnt;
     const u32 tot = __shfl_sync(FULL, incl, 31);
-    for (u32 r0 = 0; r0 < tot; r0 += 32) {
-      const u32 r = r0 + lane;
-      int j = 0;
+    for (u32 r0 = 0; r0 < tot; r0 += 32 * K2R_U) {
+      // up to K2R_U x 32 record loads in flight before any is used
+      uint4 e[K2R_U];
 #pragma unroll
-      for (int st = 16; st; st >>= 1) {
-        const u32 e = __shfl_sync(FULL, excl, j + st);
-        if (e <= r) j += st;
+      for (int u = 0; u < K2R_U; u++) {
+        const u32 r = r0 + u * 32 + lane;
+        int j = 0;
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+          const u32 ex = __shfl_sync(FULL, excl, j + st);
+          if (ex <= r) j += st;
+        }
+        const u32 ej = __shfl_sync(FULL, excl, j);
+        const u64 sj = __shfl_sync(FULL, src, j);
+        e[u] = r < tot ? __ldcg(&a.frec[sj + (r - ej)]) : make_uint4(0u, 0u, 0u, 0u);
       }
-      const u32 ej = __shfl_sync(FULL, excl, j);
-      const u64 sj = __shfl_sync(FULL, src, j);
-      const bool v = r < tot;
-      uint4 e = make_uint4(0u, 0u, 0u, 0u);
-      if (v) e = __ldcg(&a.frec[sj + (r - ej)]);
-      const bool keep = v && e.y >= kmin;
-      const u32 qk = __ballot_sync(FULL, keep);
-      if (keep) a.sup_sid[out0 + run + __popc(qk & lt)] = e;
-      run += __popc(qk);
-      const bool m1 = v && e.y - kmin <= span;
-      const bool m2 = BETA2 && v && e.z - kmin <= span;
-      const u32 nb = (m1 ? 1u : 0u) + (m2 ? 1u : 0u);
-      const u32 wnb = __reduce_add_sync(FULL, nb);
-      if (wnb == 0) continue;
-      const u32 inb = warp_incl_scan<u32>(nb);
-      u32 o = 0;
-      if (lane == 31) o = atomicAdd(s_cnt, inb);
-      o = __shfl_sync(FULL, o, 31) + inb - nb;
-      if (m1) {
-        atomicAdd(&shist[(e.y - kmin) >> DSH3], 1u);
-        region[o++] = e.y;
-      }
-      if (m2) {
-        atomicAdd(&shist[(e.z - kmin) >> DSH3], 1u);
-        region[o] = e.z;
+#pragma unroll
+      for (int u = 0; u < K2R_U; u++) {
+        if (r0 + u * 32 >= tot) break;  // warp-uniform
+        const bool v = r0 + u * 32 + lane < tot;
+        const bool keep = v && e[u].y >= kmin;
+        const u32 qk = __ballot_sync(FULL, keep);
+        if (keep) a.sup_sid[out0 + run + __popc(qk & lt)] = e[u];
+        run += __popc(qk);
+        const bool m1 = v && e[u].y - kmin <= span;
+        const bool m2 = BETA2 && v && e[u].z - kmin <= span;
+        const u32 nb = (m1 ? 1u : 0u) + (m2 ? 1u : 0u);
+        const u32 wnb = __reduce_add_sync(FULL, nb);
+        if (wnb == 0) continue;
+        const u32 inb = warp_incl_scan<u32>(nb);
+        u32 o = 0;
+        if (lane == 31) o = atomicAdd(s_cnt, inb);
+        o = __shfl_sync(FULL, o, 31) + inb - nb;
+        if (m1) {
+          atomicAdd(&shist[(e[u].y - kmin) >> DSH3], 1u);
+          region[o++] = e[u].y;
+        }
+        if (m2) {
+          atomicAdd(&shist[(e[u].z - kmin) >> DSH3], 1u);
+          region[o] = e[u].z;
+        }
       }
     }
   }

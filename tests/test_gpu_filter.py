@@ -2,11 +2,11 @@
 records, csrc/delegate.cuh / select.cuh) and of its fallback.
 
 For alpha 6..8 and beta <= 2, K1 stores only the subranges whose max delegate
-reaches a floor sampled from 1/128 of the subranges; K2 checks that the floor
+reaches a floor sampled from 1/128 of the K1 chunks; K2 checks that the floor
 lies at or below theta's first-digit bucket and otherwise re-runs the full K1 +
 K2.  Either way the answer must equal the oracle's bit for bit (values,
 indices, the reference counters of pipeline.py:87-159).  The fallback is forced
-with inputs whose sampled subranges hold the largest keys, so the sample
+with inputs whose sampled chunks hold the largest keys, so the sample
 overestimates theta.
 """
 
@@ -24,25 +24,30 @@ from test_gpu_parity import check_topk
 
 pytestmark = pytest.mark.gpu
 
-K0_GROUP = 128
+K0_GROUP = 512
+K0_REGIONS = 64
+CHUNK = 2048
 
 
-def sampled_sids(S: int) -> np.ndarray:
-    """Subranges K0 samples (k0_sample: one per group of 128, hashed position)."""
-    g = np.arange((S - 1) // K0_GROUP, dtype=np.uint64)
-    off = ((g.astype(np.uint32) * np.uint32(0x9E3779B1)) >> np.uint32(25)).astype(np.uint64)
-    return (g * K0_GROUP + off).astype(np.int64)
+def sampled_chunks(n: int) -> np.ndarray:
+    """K1 chunks K0 samples (k0_sample: 64 runs of L = max(1, nch / 32768) consecutive
+    full chunks, run r at r * (nch / 64) + a hashed offset)."""
+    nch = n // CHUNK
+    slot, L = nch // K0_REGIONS, max(1, nch // (K0_REGIONS * K0_GROUP))
+    r = np.arange(K0_REGIONS, dtype=np.uint64)
+    h = ((r.astype(np.uint32) * np.uint32(0x9E3779B1)) >> np.uint32(16)).astype(np.uint64) % np.uint64(slot - L + 1)
+    start = r * np.uint64(slot) + h
+    return (start[:, None] + np.arange(L, dtype=np.uint64)[None, :]).ravel().astype(np.int64)
 
 
 def adversarial_for_sample(n: int, alpha: int, cuda, dtype=torch.uint32):
-    """Uniform keys below 2^31, except the sampled subranges, lifted above 2^31."""
+    """Uniform keys below 2^31, except the sampled chunks, lifted above 2^31."""
     v = data.generate("uniform", n, seed=3, device=cuda)
     vi = v.view(torch.int32)
     vi &= 0x7FFFFFFF
-    sids = torch.from_numpy(sampled_sids(-(-n >> alpha))).to(cuda)
-    W = 1 << alpha
-    rows = vi[: (n >> alpha) << alpha].view(-1, W)
-    rows[sids] |= torch.tensor(-0x80000000, dtype=torch.int32, device=cuda)
+    cs = torch.from_numpy(sampled_chunks(n)).to(cuda)
+    rows = vi[: (n // CHUNK) * CHUNK].view(-1, CHUNK)
+    rows[cs] |= torch.tensor(-0x80000000, dtype=torch.int32, device=cuda)
     return v
 
 
