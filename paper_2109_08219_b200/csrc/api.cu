@@ -51,7 +51,7 @@ struct Layout {
   size_t ctrl, lb_emg, lb_eme, zero_bytes, k5_tg, k5_te;
   size_t D, meta, partial, pmeta, selbuf, region_cnt, sup_sid, sup_in, sup_cnt, sup_off, rec, e_sid, t_sid, t_cnt,
       stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, e_gpos, e_epos, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
-      digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, chunk_cnt, total;
+      digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, chunk_cnt, tseg, total;
   u64 fcap, S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
       sort_cap;
   u32 g2;
@@ -160,6 +160,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.bk_info = take(4 * 4);
   L.bk_comp = take(bk ? L.sort_cap * 8 : 0);
   L.chunk_cnt = take(filt ? L.nch * 4 : 0);
+  L.tseg = take(direct ? 0 : (u64)L.g2 * 8 * 8);
   L.total = off;
   return L;
 }
@@ -301,6 +302,7 @@ K2Args k2_args(char* ws, const Layout& L, u64 k, int beta, int alpha = 0, int fm
                 reinterpret_cast<u32*>(ws + L.sup_cnt),
                 reinterpret_cast<u32*>(ws + L.sup_off),
                 reinterpret_cast<const u32*>(ws + L.meta),
+                reinterpret_cast<const uint2*>(ws + L.tseg),
                 fmode,
                 reinterpret_cast<const u32*>(ws + L.chunk_cnt),
                 reinterpret_cast<const uint4*>(ws + L.rec),
@@ -365,11 +367,16 @@ bool cond_end(cudaStream_t inner) {
 
 // K2 pass 3 (theta from the bucket members) and K2b (the exact superset of a
 // large-bucket call).
-void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, int nsm) {
+void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, int nsm, bool trunc_ok = false) {
   const K2Args k2 = k2_args(ws, L, k, beta);
   launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2,
              k2.sup_cnt, k2.sup_off, k2.D, L.D_len);
   counted();
+  if (trunc_ok && beta <= 2) {
+    launch_pdl(k2c_tie_bounds, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.D, L.D_len, L.R2, L.g2, beta,
+               k, reinterpret_cast<uint2*>(ws + L.tseg));
+    counted();
+  }
   if (beta == 2)
     launch_pdl(k2b_superset<1>, dim3(L.g2), dim3(256), 0, s, k2);
   else
@@ -596,8 +603,10 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   }
   cudaStream_t s_outer = s;
   if (g && fast) s = gc->s4;  // the general chain is the body of the conditional node
-  // fused call: theta was left to fast_tail; the general chain resolves it itself
-  if (fused) theta_resolve(ws, L, k, beta, s, nsm);
+  // fused call: theta was left to fast_tail; the general chain resolves it itself.
+  // No external theta here, so a tie-heavy call may drop tie-only superset
+  // entries past the first k ties (not with exact stats: |C| counts every one)
+  if (fused) theta_resolve(ws, L, k, beta, s, nsm, (flags & DTOPK_FLAG_EXACT_STATS) == 0);
   Records rc{reinterpret_cast<uint4*>(ws + L.rec)};
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
   u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);

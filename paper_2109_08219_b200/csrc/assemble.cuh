@@ -252,9 +252,11 @@ __global__ void __launch_bounds__(256) k3_classify(K3Args a) {
     ull t[4] = {0, 0, 0, 0};
     for (int w = 0; w < 8; w++)
       for (int i = 0; i < 4; i++) t[i] += s_stat[i][w];
-    if (t[0]) atomicAdd((ull*)&ctrl->res.candidate_subranges, t[0]);
-    if (t[1]) atomicAdd((ull*)&ctrl->res.fully_qualified, t[1]);
-    if (t[2]) atomicAdd((ull*)&ctrl->res.partially_qualified, t[2]);
+    // truncated superset (tie-heavy call): pass 3 counted these over all of D
+    const bool counted = ld_volatile_u32(&ctrl->trunc) != 0;
+    if (t[0] && !counted) atomicAdd((ull*)&ctrl->res.candidate_subranges, t[0]);
+    if (t[1] && !counted) atomicAdd((ull*)&ctrl->res.fully_qualified, t[1]);
+    if (t[2] && !counted) atomicAdd((ull*)&ctrl->res.partially_qualified, t[2]);
     if (t[3]) atomicAdd(&ctrl->nA, t[3]);
   }
 }
@@ -486,6 +488,34 @@ __device__ __forceinline__ u32 count_ties_warp(const u32* __restrict__ keys, u64
   return __reduce_add_sync(FULL, c);
 }
 
+// Ties of one subrange counted by one lane (16-byte loads, 8 in flight): the
+// ticketed K4T path runs 32 T records of a chunk in parallel this way instead
+// of one warp-wide count after another (which left a ticket ~32 load
+// latencies long).
+template <int MODE>
+__device__ __forceinline__ u32 count_ties_lane(const u32* __restrict__ keys, u64 n, int alpha, u64 sid, u32 theta) {
+  const u64 b = sid << alpha;
+  const u64 len = min((u64)(1ull << alpha), (u64)(n - b));
+  u32 c = 0;
+  if (len == (1ull << alpha)) {  // whole subrange: 16-byte aligned (keys is, and alpha >= 2 here)
+    const uint4* p = reinterpret_cast<const uint4*>(keys + b);
+    const u32 nq = (u32)(len >> 2);
+    for (u32 q = 0; q < nq; q += 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) v[j] = q + j < nq ? __ldg(p + q + j) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        if (q + j < nq)
+          c += (to_key<MODE>(v[j].x) == theta) + (to_key<MODE>(v[j].y) == theta) + (to_key<MODE>(v[j].z) == theta) +
+               (to_key<MODE>(v[j].w) == theta);
+    }
+  } else {
+    for (u64 e = 0; e < len; e++) c += to_key<MODE>(keys[b + e]) == theta;
+  }
+  return c;
+}
+
 struct K4TArgs {
   const u32* keys;
   u64 n;
@@ -528,17 +558,47 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
   const u64 nchunks = (total + 31) / 32;  // 32-record chunks, subrange order
   const int lseg = a.alpha < 13 ? a.alpha : 13;
   const u64 ppc = (1ull << a.alpha) >> lseg;
+  // Tickets are handed out at most `window` ahead of the completed ones (about
+  // 8 MB of T subranges in flight): with the whole grid grabbing tickets at
+  // once, the first wave alone re-read ~37x the subranges the first k ties
+  // needed on few-distinct input (161 MB instead of ~4 MB at alpha 8).
+  const u32 window = max(4u, 1u << max(0, 13 - a.alpha));
   for (;;) {
-    if (threadIdx.x == 0)
-      s_chunk = ld_volatile_u32((const u32*)&ctrl->k4t_eq_done) >= a.k ? ~0ull
-                                                                          : (u64)atomicAdd(&ctrl->k4t_ticket, 1u);
+    if (threadIdx.x == 0) {
+      u64 t = ~0ull;
+      for (;;) {
+        if (*(volatile ull*)&ctrl->k4t_eq_done >= a.k) break;
+        const u32 next = ld_volatile_u32(&ctrl->k4t_ticket);
+        if ((u64)next * K4T_CHUNKS_PER_TICKET >= nchunks) {
+          t = ~1ull;  // every chunk handed out
+          break;
+        }
+        if (next < ld_volatile_u32(&ctrl->k4t_completed) + window) {
+          // claim exactly ticket `next` (a plain atomicAdd let every spinning CTA
+          // pass the window test at once)
+          if (atomicCAS(&ctrl->k4t_ticket, next, next + 1u) == next) {
+            t = next;
+            break;
+          }
+          continue;
+        }
+        __nanosleep(200);
+      }
+      s_chunk = t;
+    }
     __syncthreads();
     const u64 chunk = s_chunk;
-    if (chunk == ~0ull) {
+    if (chunk == ~0ull) {  // the first k ties are counted: the rest of the T work is skipped
       if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, 1ull);
       break;
     }
-    if (chunk * K4T_CHUNKS_PER_TICKET >= nchunks) break;
+    if (chunk == ~1ull || chunk * K4T_CHUNKS_PER_TICKET >= nchunks) break;
+#ifdef DTOPK_K4T_DEBUG
+    if (threadIdx.x == 0 && chunk % 64 == 0)
+      printf("k4t blk %d chunk %llu completed %u eq_done %llu k %llu nchunks %llu window %u\n", blockIdx.x,
+             (unsigned long long)chunk, ctrl->k4t_completed, (unsigned long long)ctrl->k4t_eq_done,
+             (unsigned long long)a.k, (unsigned long long)nchunks, window);
+#endif
     // one 32-record chunk per warp, lane per record: ties of its B/C/E/T records
     u32 eq = 0;
     const u64 c = chunk * K4T_CHUNKS_PER_TICKET + warp;
@@ -556,6 +616,14 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
         for (u64 p = 0; p < ppc; p++) e += a.seg_eq[ei * ppc + p];
       }
       u32 bt = __ballot_sync(FULL, cls == CLS_T);
+      if (a.alpha >= 2 && a.alpha <= 9) {  // lane-parallel: every T record of the chunk at once
+        if (cls == CLS_T) {
+          const u32 cn = count_ties_lane<MODE>(a.keys, a.n, a.alpha, rc.x, theta);
+          a.t_cnt[rc.w >> 4] = cn;
+          e += cn;
+        }
+        bt = 0;
+      }
       while (bt) {
         const int q = __ffs(bt) - 1;
         bt &= bt - 1;
@@ -575,6 +643,8 @@ __global__ void __launch_bounds__(256) k4t_count(K4TArgs a) {
       u64 tot = 0;
       for (int i = 0; i < 8; i++) tot += s_eq[i];
       if (tot) atomicAdd(&ctrl->k4t_eq_done, (ull)min(tot, (u64)0xffffffffull));
+      __threadfence();
+      atomicAdd(&ctrl->k4t_completed, 1u);
     }
     __syncthreads();
   }

@@ -141,6 +141,7 @@ struct Ctrl {
   u32 nT;          // class-T records (tie-only, counted by K4T)
   u32 nTslots;     // T-list slots handed out by K3 (>= nT for beta 2: C entries leave holes)
   u32 k4t_ticket;
+  u32 k4t_completed;  // tickets K4T has finished (bounds how far ahead tickets are handed out)
   ull k4t_eq_done; // ties of the word chunks K4T has completed
   // emit and sort of the answer
   u32 em_ticket;
@@ -157,6 +158,11 @@ struct Ctrl {
   u32 filt_t;     // K0: floor of the sample bucket at ~1.25 k delegates (a lower bound of theta's bucket floor)
   u32 filt_fail;  // K2: the floor was above theta's bucket (or the bucket is huge): full K1 + K2 rerun
   u32 samp_done;  // K0 last-CTA counter
+  // theta's first-digit bucket holding a large share of D (tie-heavy input)
+  u32 bk_nmin, bk_max;  // K2: ~min and max of the bucket's members (one value: theta without a digit-3 pass)
+  u32 trunc;            // pass 3: tie-only superset entries past tie_cut are dropped (enough ties before it)
+  u32 tie_cut;          // last K2b segment whose tie-only entries are kept
+  u32 tb_done;          // K2c last-CTA counter
   alignas(16) ull samp_hist[NBD1];  // K0: first-digit histogram of the sampled subranges' delegates
 };
 

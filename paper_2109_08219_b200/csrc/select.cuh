@@ -42,6 +42,7 @@ struct K2Args {
   u32* sup_cnt;  // [g2 * 8] entries of each segment
   u32* sup_off;  // [g2 * 8 + 1] exclusive prefix of sup_cnt (theta resolver)
   const u32* meta;  // [S] K1 meta words, copied into the superset entries
+  const uint2* tseg;  // [g2 * 8] (tie lower bound, entries above theta) per segment (pass 3, truncation)
   // filtered delegate pass (K1 fmode): 1 = scan K1's records when ctrl->filt_on,
   // 2 = fallback full scan, only when ctrl->filt_fail
   int fmode;
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
   // not copy it into the regions; pass 3 scans D itself (same bytes, no writes)
   const bool compact = r1.cnt * 4 <= a.nD;
   u32 run = 0;
+  u32 bmn = 0xffffffffu, bmx = 0u;  // large bucket: value range of its members
   if (records) k2_records<BETA2>(a, kmin, span, shist, &s_cnt, region, out0, run);
   for (u64 base = records ? whi : wlo; base < whi; base += 512) {
     const u64 i0 = base + (u64)lane * 16;
@@ -324,6 +326,14 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
     }
     const u32 wnb = __reduce_add_sync(FULL, nb);
     if (wnb == 0) continue;
+    if (!compact) {
+#pragma unroll
+      for (int j = 0; j < 16; j++)
+        if ((mb >> j) & 1u) {
+          bmn = min(bmn, v[j]);
+          bmx = max(bmx, v[j]);
+        }
+    }
     const u32 incl = warp_incl_scan<u32>(nb);
     u32 o = 0;
     if (lane == 31) o = atomicAdd(&s_cnt, incl);
@@ -346,6 +356,14 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
     a.sup_in[blockIdx.x * 8 + warp] = (u32)out0;
     a.sup_cnt[blockIdx.x * 8 + warp] = run;
   }
+  if (!compact) {
+    bmn = __reduce_min_sync(FULL, bmn);
+    bmx = __reduce_max_sync(FULL, bmx);
+    if (lane == 0 && bmx >= bmn) {
+      atomicMax(&a.ctrl->bk_nmin, ~bmn);
+      atomicMax(&a.ctrl->bk_max, bmx);
+    }
+  }
   __syncthreads();
   Ctrl* ctrl = a.ctrl;
   if (tid == 0) a.region_cnt[blockIdx.x] = compact ? s_cnt : 0u;
@@ -361,6 +379,117 @@ constexpr int P3_REGIONS = 256 * P3_RPT;
 
 // Pass 3 of kth(D) over the compacted bucket regions;
 // the last CTA resolves theta and the superset record offsets.
+// Large single-valued bucket (tie-heavy input), truncation allowed: one pass
+// over D with theta known gives, per K2b segment (CTA region g, warp w), a lower
+// bound of its ties (d_1 == theta: >= 1, >= 2 when d_2 == theta too) and its
+// entries above theta, plus the exact FQ / PQ / candidate counts of the whole
+// vector (pipeline.py:104-109: d_beta >= theta / d_1 >= theta > d_beta).  The last
+// CTA finds the first segment by which the tie lower bounds reach k: K2b drops
+// tie-only entries after it, since the first k ties in index order lie before.
+__device__ __noinline__ void p3_tie_bounds(Ctrl* ctrl, const u32* __restrict__ D, u64 nD, u64 R, u32 nregions,
+                                           int beta, u64 k, u32 theta, uint2* tseg, ull* scratch, int* am_last) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ull fq = 0, pq = 0;
+  for (u32 g = blockIdx.x; g < nregions; g += gridDim.x) {
+    const u64 lo = (u64)g * R, hi = min(nD, lo + R), wlen = R / 8;
+    const u64 wlo = min(hi, lo + (u64)warp * wlen), whi = min(hi, wlo + wlen);
+    ull lb = 0;
+    u32 ngt = 0;
+    for (u64 base = wlo; base < whi; base += 512) {
+      const u64 i0 = base + (u64)lane * 16;
+      u32 v[16];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const u64 i = i0 + 4 * j;
+        if (i + 4 <= whi) {
+          const uint4 q = ld_nc_v4(D + i);
+          v[4 * j] = q.x;
+          v[4 * j + 1] = q.y;
+          v[4 * j + 2] = q.z;
+          v[4 * j + 3] = q.w;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; c++) v[4 * j + c] = i + c < whi ? D[i + c] : 0u;
+        }
+      }
+      const u32 rem = i0 < whi ? (u32)min((u64)16, whi - i0) : 0u;
+      if (beta == 2) {  // (d_1, d_2) pairs; i0 is even
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          if ((u32)j >= rem) break;
+          const u32 d1 = v[j], d2 = v[j + 1];
+          ngt += d1 > theta;
+          lb += d1 == theta ? (d2 == theta ? 2u : 1u) : 0u;
+          fq += d2 >= theta;
+          pq += d1 >= theta && d2 < theta;
+        }
+      } else {  // beta 1: d_beta = d_1
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          if ((u32)j >= rem) break;
+          ngt += v[j] > theta;
+          lb += v[j] == theta;
+          fq += v[j] >= theta;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      lb += __shfl_xor_sync(FULL, lb, o);
+      ngt += __shfl_xor_sync(FULL, ngt, o);
+    }
+    if (lane == 0) tseg[g * 8 + warp] = make_uint2((u32)min(lb, (ull)0xffffffffu), ngt);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    fq += __shfl_xor_sync(FULL, fq, o);
+    pq += __shfl_xor_sync(FULL, pq, o);
+  }
+  if (lane == 0) {
+    if (fq) atomicAdd((ull*)&ctrl->res.fully_qualified, fq);
+    if (pq) atomicAdd((ull*)&ctrl->res.partially_qualified, pq);
+    if (fq + pq) atomicAdd((ull*)&ctrl->res.candidate_subranges, fq + pq);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) *am_last = atomicAdd(&ctrl->tb_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!*am_last) return;
+  __threadfence();
+  // first segment whose inclusive tie lower bound reaches k (thread t: segments t*24 ..)
+  const u32 nseg = nregions * 8;
+  ull c[K2_SEG_PER];
+  ull sum = 0;
+#pragma unroll
+  for (int q = 0; q < K2_SEG_PER; q++) {
+    const u32 i = (u32)tid * K2_SEG_PER + q;
+    c[q] = i < nseg ? (ull)__ldcg(&tseg[i].x) : 0ull;
+    sum += c[q];
+  }
+  __shared__ u32 s_cut;
+  if (tid == 0) s_cut = nseg;
+  const ull incl = block_incl_scan_256<ull>(sum, scratch);
+  ull run = incl - sum;
+#pragma unroll
+  for (int q = 0; q < K2_SEG_PER; q++) {
+    if (run < k && run + c[q] >= k) s_cut = (u32)tid * K2_SEG_PER + q;
+    run += c[q];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ctrl->tie_cut = s_cut;
+    ctrl->trunc = 1u;
+    if (s_cut + 1 < nseg) atomicAdd((ull*)&ctrl->res.concat_skipped_fq, 1ull);  // |C| not counted past the cut
+  }
+}
+
+__device__ __forceinline__ void p3_set_theta(Ctrl* ctrl, u32 kth, const DigitResult& r1) {
+  ctrl->selD.kth = kth;
+  ctrl->res.theta_local = kth;
+  ctrl->res.theta_slot = (int64_t)kth;
+  ctrl->res.delegate_bucket = r1.cnt;
+}
+
 __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
                                                 const u32* __restrict__ region_cnt, u32 nregions, u64 R,
                                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off,
@@ -432,6 +561,14 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
     return;
   }
   if (r1.cnt * 4 > nD) {
+    // a large bucket holding one value (all-equal / few-distinct input): theta
+    // is that value, no digit-3 pass; with truncation allowed, the pass over D
+    // counts ties per K2b segment instead (p3_tie_bounds)
+    const u32 bmn = ~ld_volatile_u32(&ctrl->bk_nmin), bmx = ld_volatile_u32(&ctrl->bk_max);
+    if (bmn == bmx) {
+      if (blockIdx.x == 0 && tid == 0) p3_set_theta(ctrl, bmn, r1);
+      return;
+    }
     // K2 did not compact this (large) bucket: scan D, four uint4 per thread and step
     const u32 span = kmax - kmin;
     const u64 nq = nD / 4;
@@ -485,6 +622,20 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   }
 }
 
+// K2c: tie bounds for a large-bucket call (tie-heavy input) once theta is
+// known; exits at once otherwise (see p3_tie_bounds).
+__global__ void __launch_bounds__(256) k2c_tie_bounds(Ctrl* ctrl, const u32* __restrict__ D, u64 nD, u64 R,
+                                                      u32 nregions, int beta, u64 k, uint2* tseg) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ ull scratch[8];
+  __shared__ int am_last;
+  if (ld_volatile_u32(&ctrl->small_done)) return;
+  const DigitResult r1 = ctrl->selD.r1;
+  if (r1.cnt * 4 <= nD) return;
+  p3_tie_bounds(ctrl, D, nD, R, nregions, beta, k, ctrl->selD.kth, tseg, scratch, &am_last);
+}
+
 // K2b: exact candidate superset for calls whose theta bucket held a large share
 // of D (K2 deferred it): one more read of D with the exact theta, ordered
 // compaction per (CTA, warp) segment as in K2, then the last CTA offsets the
@@ -509,7 +660,14 @@ __global__ void __launch_bounds__(256) k2b_superset(K2Args a) {
   const u64 beta = BETA2 ? 2u : (u64)a.beta;
   const u64 out0 = (wlo + beta - 1) / beta;
   u32 run = 0;
-  for (u64 base = wlo; base < whi; base += 512) {
+  // truncated (pass 3, p3_tie_bounds): past the cut only entries above theta are
+  // kept, and segments without any are not read at all
+  const u32 seg = blockIdx.x * 8 + warp;
+  const bool trunc = ld_volatile_u32(&ctrl->trunc) != 0;
+  const bool ties = !trunc || seg <= ld_volatile_u32(&ctrl->tie_cut);
+  const bool skip = !ties && __ldcg(&a.tseg[seg].y) == 0;
+  const u32 floor_key = ties ? theta : theta + 1u;  // theta < max key whenever an entry lies above it
+  for (u64 base = skip ? whi : wlo; base < whi; base += 512) {
     const u64 i0 = base + (u64)lane * 16;
     u32 v[16];
 #pragma unroll
@@ -530,7 +688,7 @@ __global__ void __launch_bounds__(256) k2b_superset(K2Args a) {
     u32 mc = 0, r = BETA2 ? 0u : (u32)(i0 % beta);
 #pragma unroll
     for (int j = 0; j < 16; j++) {
-      mc |= ((u32)j < rem && r == 0 && v[j] >= theta) ? (1u << j) : 0u;
+      mc |= ((u32)j < rem && r == 0 && v[j] >= floor_key) ? (1u << j) : 0u;
       r = BETA2 ? (r ^ 1u) : ((r + 1 == (u32)beta) ? 0u : r + 1);
     }
     const u32 nc = __popc(mc);
