@@ -19,6 +19,11 @@
  *                              and extract_delegates_blocked   (delegate.py:158-191)
  *   dtopk_kth_largest       <- kernels.radix_topk threshold    (kernels.py:109-165),
  *                              used by pipeline.first_topk     (pipeline.py:87-116)
+ *   dtopk_qualify           <- pipeline.first_topk qualification (pipeline.py:87-116)
+ *   dtopk_concat            <- pipeline.concatenate_filtered    (pipeline.py:119-159)
+ *   dtopk_min_at_least      <- radix_topk skip_last relaxation  (kernels.py:161-164)
+ *   dtopk_merge_lists,      <- the coordinator's merge of worker lists
+ *   dtopk_dsel_*               (distributed.py:191-251)
  *   dtopk_workspace_bytes   <- (no reference counterpart: numpy allocates implicitly)
  *
  * Key spaces: every kernel works on 32-bit *keys* where "larger key" means
@@ -46,7 +51,7 @@ typedef enum {
   DTOPK_INVALID_ARG = 4,        /* ValueError (bad alpha / dtype / alignment) */
   DTOPK_WORKSPACE_TOO_SMALL = 5,
   DTOPK_CUDA_ERROR = 6,
-  DTOPK_UNSUPPORTED = 7         /* beta > 32 on the delegate path */
+  DTOPK_UNSUPPORTED = 7         /* beta > 32 with subranges of more than 8192 keys */
 } dtopk_status;
 
 typedef enum { DTOPK_U32 = 0, DTOPK_F32 = 1 } dtopk_dtype;
@@ -148,6 +153,31 @@ dtopk_status dtopk_extract_delegates(const void* keys, uint64_t n, int dtype, in
  * dtopk_workspace_bytes(n, k, 0, 1, 1). */
 dtopk_status dtopk_kth_largest(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t* out_kth,
                                void* ws, size_t ws_bytes, void* stream);
+
+/* ---- Stage operators (stage-level API and its parity tests) ----
+ * dtopk_qualify        <- pipeline.first_topk qualification (pipeline.py:87-116):
+ *   given the delegate vector (key space, beta per subrange) and theta, writes
+ *   in D order the selected delegates (>= theta) and their subrange tags, the
+ *   partial ones (selected, subrange not fully qualified) and the fully
+ *   qualified subrange ids (d_beta >= theta, ascending); out_counts[3] =
+ *   (selected, partial, fully qualified).  Output buffers hold up to
+ *   n_delegates (selected / partial) and n_delegates / beta (ids) entries.
+ * dtopk_concat         <- pipeline.concatenate_filtered (pipeline.py:119-159):
+ *   elements whose key is >= theta of the listed subranges (ascending ids),
+ *   subrange-ascending then scan order, in the input dtype; *out_count on the
+ *   device.  out_values holds up to n_fq * 2^alpha elements.
+ * dtopk_min_at_least   <- the skip_last relaxation of kernels.radix_topk
+ *   (kernels.py:161-164): *out_min = min{ key >= edge } (0xffffffff if none).
+ * Workspace: dtopk_stage_workspace_bytes(n_delegates) for qualify,
+ * dtopk_stage_workspace_bytes(n_fq << alpha) for concat. */
+size_t dtopk_stage_workspace_bytes(uint64_t n_elements);
+dtopk_status dtopk_qualify(const uint32_t* delegates, uint64_t n_delegates, int beta, uint32_t theta,
+                           uint32_t* sel_values, uint32_t* sel_tags, uint32_t* part_values, uint32_t* part_tags,
+                           uint32_t* fq_sids, int64_t* out_counts, void* ws, size_t ws_bytes, void* stream);
+dtopk_status dtopk_concat(const void* keys, uint64_t n, int dtype, int largest, int alpha, const uint32_t* fq_sids,
+                          uint64_t n_fq, uint32_t theta, void* out_values, int64_t* out_count, void* ws,
+                          size_t ws_bytes, void* stream);
+dtopk_status dtopk_min_at_least(const uint32_t* keys, uint64_t n, uint32_t edge, uint32_t* out_min, void* stream);
 
 /* ---- Multi-GPU candidate merge (distributed.py:191-251 coordinator merge) ----
  * Every rank's candidates are (value bits, global index) lists ordered

@@ -25,6 +25,7 @@
 #include "merge.cuh"
 #include "scan.cuh"
 #include "select.cuh"
+#include "stage.cuh"
 
 #ifndef DTOPK_K2_CPS
 #define DTOPK_K2_CPS 4  // K2 CTAs (regions) per SM
@@ -281,8 +282,13 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
     case 7: launch_k1<MODE, 7>(a, s, nsm, L.nch); break;
     case 8: launch_k1<MODE, 8>(a, s, nsm, L.nch); break;
     default:
-      k1_generic<MODE><<<grid_for((L.S + 7) / 8, nsm * 8), 256, 0, s>>>(
-          keys, n, alpha, beta, L.S, D, reinterpret_cast<u32*>(ws + L.meta), ctrl->selD.hist1);
+      if (beta <= 32) {
+        k1_generic<MODE><<<grid_for((L.S + 7) / 8, nsm * 8), 256, 0, s>>>(
+            keys, n, alpha, beta, L.S, D, reinterpret_cast<u32*>(ws + L.meta), ctrl->selD.hist1);
+      } else {  // any beta < 2^alpha for subranges of <= 8192 keys: block sort per subrange
+        k1_bigbeta<MODE><<<grid_for(L.S, nsm * 4), K1B_THREADS, 0, s>>>(
+            keys, n, alpha, beta, L.S, D, reinterpret_cast<u32*>(ws + L.meta), ctrl->selD.hist1);
+      }
       counted();
   }
 }
@@ -722,7 +728,7 @@ dtopk_status check_common(const void* keys, u64 n, int dtype, u64 k) {
 dtopk_status check_delegate(u64 n, int alpha, int beta) {
   if (alpha < 1 || alpha > 40 || (1ull << alpha) > n) return DTOPK_INVALID_ARG;
   if (beta < 1 || (u64)beta >= (1ull << alpha)) return DTOPK_INVALID_BETA;
-  if (beta > 32) return DTOPK_UNSUPPORTED;
+  if (beta > 32 && alpha > 13) return DTOPK_UNSUPPORTED;  // beta > 32: subranges of <= 8192 keys (k1_bigbeta)
   if (((n + (1ull << alpha) - 1) >> alpha) > 0xffffffffull) return DTOPK_INVALID_ARG;
   return DTOPK_OK;
 }
@@ -793,6 +799,19 @@ void run_dsel_digit(int64_t* state, int64_t* hist, int pass, const uint32_t* bit
 }
 
 
+template <int MODE>
+void run_concat(const u32* raw, u64 n, int alpha, const u32* fq, u64 nfq, u32 theta, u32* out, int64_t* out_count,
+                u32* tc, cudaStream_t s) {
+  const u64 nv = nfq << alpha;
+  const u64 tiles = std::max<u64>(1, (nv + STG_TILE - 1) / STG_TILE);
+  concat_count<MODE><<<(unsigned)tiles, STG_THREADS, 0, s>>>(raw, n, alpha, fq, nv, theta, tc);
+  stg_scan<<<1, STG_THREADS, 0, s>>>(tc, tiles, 1, out_count);
+  concat_emit<MODE><<<(unsigned)tiles, STG_THREADS, 0, s>>>(raw, n, alpha, fq, nv, theta, tc, out);
+  counted(3);
+}
+
+
+
 #define DISPATCH_MODE(mode, FN, ...)  \
   switch (mode) {                     \
     case 0: FN<0>(__VA_ARGS__); break; \
@@ -804,6 +823,8 @@ void run_dsel_digit(int64_t* state, int64_t* hist, int pass, const uint32_t* bit
 }  // namespace
 
 extern "C" {
+
+size_t dtopk_stage_workspace_bytes(uint64_t n_elements);
 
 size_t dtopk_workspace_bytes(uint64_t n, uint64_t k, int alpha, int beta, int direct) {
   if (k < 1) k = 1;
@@ -1112,6 +1133,53 @@ dtopk_status dtopk_dsel_place(const int64_t* gathered, const int64_t* state, int
              (long long)k, bits, reinterpret_cast<const long long*>(idx), reinterpret_cast<long long*>(slots),
              reinterpret_cast<long long*>(seg_off), reinterpret_cast<long long*>(seg_len));
   counted();
+  return cuda_status();
+}
+
+dtopk_status dtopk_qualify(const uint32_t* delegates, uint64_t n_delegates, int beta, uint32_t theta,
+                           uint32_t* sel_values, uint32_t* sel_tags, uint32_t* part_values, uint32_t* part_tags,
+                           uint32_t* fq_sids, int64_t* out_counts, void* ws, size_t ws_bytes, void* stream) {
+  if (!delegates || !out_counts || beta < 1 || n_delegates == 0 || n_delegates % (uint64_t)beta) return DTOPK_INVALID_ARG;
+  if (!sel_values || !sel_tags || !part_values || !part_tags || !fq_sids) return DTOPK_INVALID_ARG;
+  const u64 tiles = (n_delegates + STG_TILE - 1) / STG_TILE;
+  if (ws == nullptr || ws_bytes < dtopk_stage_workspace_bytes(n_delegates)) return DTOPK_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  u32* tc = reinterpret_cast<u32*>(ws);
+  qual_count<<<(unsigned)tiles, STG_THREADS, 0, s>>>(delegates, n_delegates, beta, theta, tc);
+  stg_scan<<<1, STG_THREADS, 0, s>>>(tc, tiles, STG_STREAMS, reinterpret_cast<int64_t*>(out_counts));
+  qual_emit<<<(unsigned)tiles, STG_THREADS, 0, s>>>(delegates, n_delegates, beta, theta, tc, sel_values, sel_tags,
+                                                    part_values, part_tags, fq_sids);
+  counted(3);
+  return cuda_status();
+}
+
+size_t dtopk_stage_workspace_bytes(uint64_t n_elements) {
+  return (size_t)((n_elements + STG_TILE - 1) / STG_TILE) * STG_STREAMS * 4 + 256;
+}
+
+dtopk_status dtopk_concat(const void* keys, uint64_t n, int dtype, int largest, int alpha, const uint32_t* fq_sids,
+                          uint64_t n_fq, uint32_t theta, void* out_values, int64_t* out_count, void* ws,
+                          size_t ws_bytes, void* stream) {
+  dtopk_status st = check_common(keys, n, dtype, 1);
+  if (st != DTOPK_OK) return st;
+  if (alpha < 0 || alpha > 40 || !out_values || !out_count || (n_fq && !fq_sids)) return DTOPK_INVALID_ARG;
+  if (ws == nullptr || ws_bytes < dtopk_stage_workspace_bytes(std::max<u64>(1, n_fq << alpha)))
+    return DTOPK_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DISPATCH_MODE(key_mode(dtype, largest), run_concat, reinterpret_cast<const u32*>(keys), n, alpha, fq_sids, n_fq,
+                theta, reinterpret_cast<u32*>(out_values), out_count, reinterpret_cast<u32*>(ws), s);
+  return cuda_status();
+}
+
+dtopk_status dtopk_min_at_least(const uint32_t* keys, uint64_t n, uint32_t edge, uint32_t* out_min, void* stream) {
+  if (!keys || !out_min) return DTOPK_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(out_min, 0xff, 4, s);
+  if (n) {
+    min_at_least<<<grid_for((n + STG_THREADS - 1) / STG_THREADS, num_sms() * 8), STG_THREADS, 0, s>>>(keys, n, edge,
+                                                                                                  out_min);
+    counted();
+  }
   return cuda_status();
 }
 

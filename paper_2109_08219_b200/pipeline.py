@@ -223,55 +223,81 @@ class QualificationReport:
 
 def first_topk(d, k: int, backend: str = "radix", skip_last: bool = True, *,
                stats: WorkloadStats | None = None) -> QualificationReport:
-    """Delegate top-k + qualification (pipeline.py:87-116).
+    """Delegate top-k + qualification (pipeline.py:87-116), on the device.
 
-    theta comes from the device radix select (``dtopk_kth_largest``); with
-    ``skip_last`` it is relaxed exactly as kernels.radix_topk does
-    (min of delegates >= kth & ~0xFF, kernels.py:161-164).
+    theta = kth(D) by the radix select ``dtopk_kth_largest``; with ``skip_last``
+    it is relaxed as kernels.radix_topk does (kernels.py:161-164: the minimum
+    delegate >= kth & ~0xff, ``dtopk_min_at_least``).  The qualification --
+    selected delegates and tags, fully qualified subranges, partial delegates
+    -- is one ordered compaction (``dtopk_qualify``).  Values are the delegate
+    keys (int64 view), tags / ids int64, all on the delegates' device.
     """
     from .kernels import kth_largest
 
-    vals = d.values if isinstance(d.values, torch.Tensor) else torch.from_numpy(np.asarray(d.values)).cuda()
+    lib = _native.load()
+    vals = d.values if isinstance(d.values, torch.Tensor) else torch.from_numpy(np.asarray(d.values))
+    vals = _device._aligned(_device._torch_u32(vals.cuda() if not vals.is_cuda else vals))
     if k > vals.numel():
         raise InvalidK(f"k={k} exceeds delegate vector length {vals.numel()}")
-    kth = kth_largest(vals, k)
-    theta = kth
-    v64 = vals.to(torch.int64)
+    dev = vals.device
+    s = torch.cuda.current_stream(dev).cuda_stream
+    theta = kth_largest(vals, k)
     if skip_last and backend != "bitonic":
-        edge = kth & 0xFFFFFF00
-        theta = int(v64[v64 >= edge].min().item())
-    in_t = v64 >= theta
-    rows = in_t.view(-1, d.beta).sum(dim=1)
-    full = rows == d.beta
-    full_rep = full.repeat_interleave(d.beta)
-    tags = torch.arange(d.subrange_count, device=vals.device, dtype=torch.int64).repeat_interleave(d.beta)
-    partial = in_t & ~full_rep
-    # torch has no uint32 gather kernels: masks are applied to the int64 view
+        out = torch.empty(1, dtype=torch.int32, device=dev)
+        _native.check(lib.dtopk_min_at_least(vals.data_ptr(), vals.numel(), theta & 0xFFFFFF00, out.data_ptr(), s),
+                      "dtopk_min_at_least")
+        theta = int(out.item()) & 0xFFFFFFFF
+    nd, beta = vals.numel(), d.beta
+    bufs = [torch.empty(n_, dtype=torch.int32, device=dev) for n_ in (nd, nd, nd, nd, nd // beta)]
+    counts = torch.empty(3, dtype=torch.int64, device=dev)
+    wsb = int(lib.dtopk_stage_workspace_bytes(nd))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    _native.check(lib.dtopk_qualify(vals.data_ptr(), nd, beta, theta, *(b.data_ptr() for b in bufs),
+                                    counts.data_ptr(), ws.data_ptr(), wsb, s), "dtopk_qualify")
+    n_sel, n_part, n_fq = (int(x) for x in counts.tolist())
+
+    def u64(t, m):
+        return t[:m].to(torch.int64) & 0xFFFFFFFF
+
+    if stats is not None:
+        stats.add_read(2 * nd)
+        stats.add_written(n_sel)
     return QualificationReport(
-        selected_values=v64[in_t],
-        selected_tags=tags[in_t],
+        selected_values=u64(bufs[0], n_sel),
+        selected_tags=u64(bufs[1], n_sel),
         theta=int(theta),
-        fully_qualified=torch.nonzero(full).flatten(),
-        partial_values=v64[partial],
-        partial_tags=tags[partial],
+        fully_qualified=u64(bufs[4], n_fq),
+        partial_values=u64(bufs[2], n_part),
+        partial_tags=u64(bufs[3], n_part),
     )
 
 
 def concatenate_filtered(v, report: QualificationReport, alpha: int, *,
                          stats: WorkloadStats | None = None) -> torch.Tensor:
     """Elements >= theta of fully qualified subranges, subrange-ascending then
-    scan order (pipeline.py:119-159)."""
+    scan order (pipeline.py:119-159), by one ordered device compaction
+    (``dtopk_concat``).  Returned in the input's dtype on its device."""
+    lib = _native.load()
     dv = _device.to_device(v)
-    keys = dv.keys.to(torch.int64)
-    w = 1 << alpha
-    nsub = -(-dv.n // w)
-    fq = torch.zeros(nsub, dtype=torch.bool, device=keys.device)
-    if report.fully_qualified.numel():
-        fq[report.fully_qualified.to(keys.device)] = True
-    member = fq.repeat_interleave(w)[: dv.n]
+    dev = dv.keys.device
+    fq = report.fully_qualified
+    fq = (fq if isinstance(fq, torch.Tensor) else torch.as_tensor(np.asarray(fq))).to(dev)
+    fq32 = fq.to(torch.int64).to(torch.int32).contiguous()
+    nfq = fq32.numel()
     if stats is not None:
-        stats.add_read(int(report.fully_qualified.numel()) * w)
-    out = keys[member & (keys >= report.theta)]
+        stats.add_read(nfq << alpha)
+    cap = max(1, min(nfq << alpha, dv.n))
+    out = torch.empty(cap, dtype=torch.int32, device=dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    wsb = int(lib.dtopk_stage_workspace_bytes(max(1, nfq << alpha)))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    theta = int(report.theta)  # a key (for uint32 largest: the value itself)
+    _native.check(lib.dtopk_concat(dv.keys.data_ptr(), dv.n, dv.code, 1, alpha, fq32.data_ptr() if nfq else None, nfq,
+                                   theta & 0xFFFFFFFF, out.data_ptr(), cnt.data_ptr(), ws.data_ptr(), wsb,
+                                   torch.cuda.current_stream(dev).cuda_stream), "dtopk_concat")
+    m = int(cnt.item())
+    res = out[:m]
+    res = res.view(torch.float32) if dv.code == _native.DTYPE_F32 else res.view(torch.uint32)
     if stats is not None:
-        stats.add_written(out.numel())
-    return out
+        stats.add_written(m)
+    return res
