@@ -58,6 +58,7 @@ typedef enum { DTOPK_U32 = 0, DTOPK_F32 = 1 } dtopk_dtype;
 
 /* flags for dtopk_select / dtopk_select_begin */
 #define DTOPK_FLAG_EXACT_STATS 1u  /* re-read tie-only subranges so concatenated_len is exact */
+#define DTOPK_FLAG_DELEGATES_DONE 2u  /* dtopk_select: K1 already ran via dtopk_delegates_range */
 
 /* Device-resident result header, written by the kernels of one call.
  * Field names follow core.WorkloadStats (core.py:59-93) where they overlap. */
@@ -125,6 +126,16 @@ dtopk_status dtopk_plan_launch(dtopk_plan plan, void* stream);
 /* kernels in the always-executed part and in the conditional tail */
 void dtopk_plan_kernels(dtopk_plan plan, unsigned long long* main_kernels, unsigned long long* tail_kernels);
 void dtopk_plan_destroy(dtopk_plan plan);
+
+/* Streamed host input (distributed.py:97-137 residency / reload plan,
+ * PAPER.md:928-932): K1 over K1 chunks [chunk_begin, chunk_end) (2048 keys
+ * each, ceil(n / 2048) in all) of the device buffer `keys`, as soon as that
+ * range has arrived (chunk_begin == 0 also clears the workspace).  After the
+ * last range, dtopk_select with DTOPK_FLAG_DELEGATES_DONE finishes the call.
+ * beta <= 8.  The ranges must cover every chunk exactly once. */
+dtopk_status dtopk_delegates_range(const void* keys, uint64_t n, int dtype, uint64_t k, int largest,
+                                   int alpha, int beta, uint64_t chunk_begin, uint64_t chunk_end,
+                                   void* ws, size_t ws_bytes, void* stream);
 
 /* First half of dtopk_select (delegate path only): delegates, theta = kth(D).
  * Afterwards dtopk_result.theta_slot holds theta (int64) in device memory. */

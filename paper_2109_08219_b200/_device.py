@@ -90,6 +90,59 @@ def to_device(v, device: torch.device | None = None) -> DeviceVector:
     return DeviceVector(_aligned(d), code, odt, "numpy", h2d_bytes=host.size * 4)
 
 
+@dataclass
+class HostVector:
+    host: torch.Tensor  # 1-D contiguous CPU tensor (uint32 or float32 bits as stored)
+    code: int
+    out_dtype: torch.dtype
+    kind: str  # "numpy" | "torch_cpu"
+
+    @property
+    def n(self) -> int:
+        return int(self.host.numel())
+
+
+def host_view(v) -> HostVector | None:
+    """A host input as a flat CPU tensor without copying (None for CUDA tensors)."""
+    if isinstance(v, torch.Tensor):
+        if v.is_cuda:
+            return None
+        if v.numel() == 0:
+            raise EmptyInput("input vector must hold at least one element")
+        if v.dtype == torch.float32:
+            return HostVector(v.reshape(-1).contiguous(), _native.DTYPE_F32, torch.float32, "torch_cpu")
+        odt = torch.int32 if v.dtype == torch.int32 else torch.uint32
+        return HostVector(_torch_u32(v.reshape(-1)).contiguous(), _native.DTYPE_U32, odt, "torch_cpu")
+    arr = np.asarray(v)
+    if arr.dtype == np.float32:
+        host, code, odt = np.ascontiguousarray(arr.ravel()), _native.DTYPE_F32, torch.float32
+    else:
+        host = np.ascontiguousarray(np.asarray(v, dtype=ELEMENT_DTYPE).ravel())
+        code, odt = _native.DTYPE_U32, torch.uint32
+    if host.size == 0:
+        raise EmptyInput("input vector must hold at least one element")
+    return HostVector(torch.from_numpy(host), code, odt, "numpy")
+
+
+# Streamed host input (SURVEY 8f row f1; reference residency / reload plan,
+# distributed.py:97-137): ranges of STREAM_RANGE keys go host -> pinned staging
+# (parallel CPU copy, pageable inputs only) -> HBM on a copy stream, and K1
+# reduces each range as soon as it has landed, so the H2D stream is the only
+# serial cost.  Two staging buffers per device, allocated once.
+STREAM_MIN = 1 << 24
+STREAM_RANGE = 1 << 24  # keys per range (64 MiB), a multiple of the 2048-key K1 chunk
+_staging: dict = {}
+
+
+def staging_buffers(device: torch.device):
+    st = _staging.get(device)
+    if st is None:
+        bufs = [torch.empty(STREAM_RANGE, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        evs = [None, None]
+        st = _staging[device] = (bufs, evs, torch.cuda.Stream(device))
+    return st
+
+
 def to_caller(t: torch.Tensor, kind: str):
     """Return a result in the caller's container kind."""
     if kind == "torch_cuda":

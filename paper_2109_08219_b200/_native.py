@@ -28,6 +28,7 @@ UNSUPPORTED = 7
 DTYPE_U32 = 0
 DTYPE_F32 = 1
 FLAG_EXACT_STATS = 1
+FLAG_DELEGATES_DONE = 2
 
 PATH_SELECT = 1
 PATH_MERGE = 2
@@ -106,6 +107,11 @@ EXPORTS = {
     "dtopk_event_elapsed_ms": (ctypes.c_float, [ctypes.c_void_p, ctypes.c_void_p]),
     "dtopk_generate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_void_p]),
+    "dtopk_delegates_range": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+         ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p],
+    ),
     "dtopk_stage_workspace_bytes": (ctypes.c_size_t, [ctypes.c_uint64]),
     "dtopk_qualify": (
         ctypes.c_int,

@@ -241,20 +241,26 @@ inline int key_mode(int dtype, int largest) { return (dtype == DTOPK_F32 ? 2 : 0
 
 // ---------------------------------------------------------------------------
 template <int MODE, int B>
-void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch) {
+void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch, int merge = 1) {
   ensure_smem(k1_delegates<MODE, B>, (int)K1_SMEM);
-  k1_delegates<MODE, B><<<grid_for(nch, nsm * K1_CPS), K1_THREADS, K1_SMEM, s>>>(a);
-  counted();
-  if (a.alpha > K1_LOG_CHUNK) {
+  if (a.c_end > a.c_begin) {
+    // the full-range launch keeps the grid the record streams were sized for (k1_grid)
+    k1_delegates<MODE, B><<<grid_for(a.c_begin == 0 && a.c_end == nch ? nch : a.c_end - a.c_begin, nsm * K1_CPS),
+                            K1_THREADS, K1_SMEM, s>>>(a);
+    counted();
+  }
+  if (merge && a.alpha > K1_LOG_CHUNK) {
     k1_merge<B><<<grid_for((a.S + 255) / 256, nsm * 4), 256, 0, s>>>(a.partial, a.pmeta, nch, a.alpha, a.S, a.D,
                                                                        a.meta, a.hist1);
     counted();
   }
 }
 
+// K1 over chunks [c0, c1) (all by default); `merge` 0 skips k1_merge (alpha >
+// 11: run once after the last range), `k1` 0 runs only k1_merge.
 template <int MODE>
 void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* ws, const Layout& L, cudaStream_t s,
-                     int nsm, int fmode = 0) {
+                     int nsm, int fmode = 0, u64 c0 = 0, u64 c1 = ~0ull, int merge = 1, int k1 = 1) {
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
   K1Args a{keys,
            n,
@@ -271,16 +277,18 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
            fmode,
            reinterpret_cast<uint4*>(ws + L.rec),
            reinterpret_cast<u32*>(ws + L.chunk_cnt),
-           L.fcap};
+           L.fcap,
+           k1 ? c0 : 0,
+           k1 ? std::min<u64>(c1, L.nch) : 0};
   switch (beta) {
-    case 1: launch_k1<MODE, 1>(a, s, nsm, L.nch); break;
-    case 2: launch_k1<MODE, 2>(a, s, nsm, L.nch); break;
-    case 3: launch_k1<MODE, 3>(a, s, nsm, L.nch); break;
-    case 4: launch_k1<MODE, 4>(a, s, nsm, L.nch); break;
-    case 5: launch_k1<MODE, 5>(a, s, nsm, L.nch); break;
-    case 6: launch_k1<MODE, 6>(a, s, nsm, L.nch); break;
-    case 7: launch_k1<MODE, 7>(a, s, nsm, L.nch); break;
-    case 8: launch_k1<MODE, 8>(a, s, nsm, L.nch); break;
+    case 1: launch_k1<MODE, 1>(a, s, nsm, L.nch, merge); break;
+    case 2: launch_k1<MODE, 2>(a, s, nsm, L.nch, merge); break;
+    case 3: launch_k1<MODE, 3>(a, s, nsm, L.nch, merge); break;
+    case 4: launch_k1<MODE, 4>(a, s, nsm, L.nch, merge); break;
+    case 5: launch_k1<MODE, 5>(a, s, nsm, L.nch, merge); break;
+    case 6: launch_k1<MODE, 6>(a, s, nsm, L.nch, merge); break;
+    case 7: launch_k1<MODE, 7>(a, s, nsm, L.nch, merge); break;
+    case 8: launch_k1<MODE, 8>(a, s, nsm, L.nch, merge); break;
     default:
       if (beta <= 32) {
         k1_generic<MODE><<<grid_for((L.S + 7) / 8, nsm * 8), 256, 0, s>>>(
@@ -396,11 +404,25 @@ void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, i
 // run here, so that theta_slot holds theta when the call returns.
 template <int MODE>
 void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, const Layout& L, cudaStream_t s, int nsm,
-               void* const* ev, bool fused = false, GraphCtx* gc = nullptr) {
-  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
-  rec(ev, 0, s);
+               void* const* ev, bool fused = false, GraphCtx* gc = nullptr, bool delegates_done = false) {
   u32* D = reinterpret_cast<u32*>(ws + L.D);
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(ws + L.ctrl);
+  if (delegates_done) {  // K1 already ran range by range (dtopk_delegates_range, streamed host input)
+    rec(ev, 0, s);
+    if (alpha > K1_LOG_CHUNK) stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm, 0, 0, 0, 1, 0);
+    rec(ev, 1, s);
+    const K2Args k2 = k2_args(ws, L, k, beta, alpha, 0);
+    if (beta == 2)
+      launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
+    else
+      launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, s, k2);
+    counted();
+    if (!fused) theta_resolve(ws, L, k, beta, s, nsm);
+    rec(ev, 2, s);
+    return;
+  }
+  cudaMemsetAsync(ws, 0, L.zero_bytes, s);
+  rec(ev, 0, s);
   const bool filt = filt_possible(L.S, alpha, beta, 0);
   if (filt) {
     const u64 nch_full = n >> K1_LOG_CHUNK;
@@ -1031,9 +1053,31 @@ dtopk_status dtopk_select(const void* keys, uint64_t n, int dtype, uint64_t k, i
   const u32* kp = reinterpret_cast<const u32*>(keys);
   char* w = reinterpret_cast<char*>(ws);
   const bool fused = alpha <= FT_MAX_ALPHA;
-  DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, stage_events, fused);
+  const bool done = (flags & DTOPK_FLAG_DELEGATES_DONE) != 0;
+  if (done && beta > 8) return DTOPK_INVALID_ARG;  // streamed delegates: the K1 ladder kernels only
+  DISPATCH_MODE(key_mode(dtype, largest), run_begin, kp, n, k, alpha, beta, w, L, s, nsm, stage_events, fused, nullptr,
+                done);
   DISPATCH_MODE(key_mode(dtype, largest), run_finish, kp, n, k, alpha, beta, flags, nullptr, out_values, out_indices,
                 index_offset, w, L, s, nsm, stage_events, nullptr, fused);
+  return cuda_status();
+}
+
+dtopk_status dtopk_delegates_range(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha,
+                                   int beta, uint64_t chunk_begin, uint64_t chunk_end, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  dtopk_status st = check_common(keys, n, dtype, k);
+  if (st != DTOPK_OK) return st;
+  if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
+  if (beta > 8) return DTOPK_INVALID_ARG;
+  const Layout L = make_layout(n, k, alpha, beta, 0);
+  if (ws == nullptr || ws_bytes < L.total) return DTOPK_WORKSPACE_TOO_SMALL;
+  if (chunk_begin > chunk_end || chunk_end > L.nch) return DTOPK_INVALID_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* w = reinterpret_cast<char*>(ws);
+  if (chunk_begin == 0) cudaMemsetAsync(w, 0, L.zero_bytes, s);
+  const u32* kp = reinterpret_cast<const u32*>(keys);
+  DISPATCH_MODE(key_mode(dtype, largest), stage_delegates, kp, n, alpha, beta, reinterpret_cast<u32*>(w + L.D), w, L,
+                s, num_sms(), 0, chunk_begin, chunk_end, 0, 1);
   return cuda_status();
 }
 

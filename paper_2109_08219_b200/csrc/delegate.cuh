@@ -70,6 +70,7 @@ struct K1Args {
   uint4* frec;     // per consumer warp of the grid, a contiguous stream of fcap records
   u32* chunk_cnt;  // [nchunks] (offset of chunk c's records in its warp's stream << 6) | count
   u64 fcap;        // records per warp stream: ceil(nchunks / (grid * 8)) * (2048 >> alpha)
+  u64 c_begin, c_end;  // chunks this launch reduces (a streamed host input arrives range by range)
 };
 
 // Per-lane accumulator: top-B ladder, uint4 index p of the running maximum
@@ -464,14 +465,14 @@ __device__ __noinline__ void k1_warp_chunk_tail(const K1Args& a, const u32* stag
 
 // Chunk of iteration i of this CTA (iteration i uses ring stage i % K1_STAGES
 // and consumer warp i % K1_CWARPS), or ~0 past the CTA's last chunk.
-__device__ __forceinline__ u64 k1_chunk_of(u64 i, u64 nch) {
+__device__ __forceinline__ u64 k1_chunk_of(u64 i, u64 c0, u64 c1) {
   if (DTOPK_K1_CONTIG) {
-    const u64 R = (nch + gridDim.x - 1) / gridDim.x;
-    const u64 c = (u64)blockIdx.x * R + i;
-    return (i < R && c < nch) ? c : ~0ull;
+    const u64 R = (c1 - c0 + gridDim.x - 1) / gridDim.x;
+    const u64 c = c0 + (u64)blockIdx.x * R + i;
+    return (i < R && c < c1) ? c : ~0ull;
   }
-  const u64 c = blockIdx.x + i * gridDim.x;
-  return c < nch ? c : ~0ull;
+  const u64 c = c0 + blockIdx.x + i * gridDim.x;
+  return c < c1 ? c : ~0ull;
 }
 
 template <int MODE, int B>
@@ -509,7 +510,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
     if (lane == 0) {
       u64 i = 0;
       const u64 pol = l2_policy_evict_first();
-      for (u64 c = k1_chunk_of(0, nch); c != ~0ull; c = k1_chunk_of(++i, nch)) {
+      for (u64 c = k1_chunk_of(0, a.c_begin, a.c_end); c != ~0ull; c = k1_chunk_of(++i, a.c_begin, a.c_end)) {
         const u32 s = (u32)(i % K1_STAGES);
         const u32 ph = (u32)(i / K1_STAGES) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   } else {
     u64 i = warp;
     u32 wrun = 0;  // records in this warp's stream (filtered mode)
-    for (u64 c = k1_chunk_of(i, nch); c != ~0ull; i += K1_CWARPS, c = k1_chunk_of(i, nch)) {
+    for (u64 c = k1_chunk_of(i, a.c_begin, a.c_end); c != ~0ull; i += K1_CWARPS, c = k1_chunk_of(i, a.c_begin, a.c_end)) {
       const u32 s = (u32)(i % K1_STAGES);
       const u32 ph = (u32)(i / K1_STAGES) & 1u;
       mbar_wait(&full[s], ph);

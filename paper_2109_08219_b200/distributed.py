@@ -585,35 +585,55 @@ def _worker_lane(worker_id, source, parts, plan_, k, cfg, device, outbox):
         stream = torch.cuda.Stream(device)
         with torch.cuda.stream(stream):
             is_file = not isinstance(source, (np.ndarray, torch.Tensor))
-            stage = None
+            stage, stage_ev = None, [None, None]
+            copy = torch.cuda.Stream(device)
             if is_file:
                 cap = max(plan_.partitions[i].length for i in parts) if parts else 1
-                stage = torch.empty(cap, dtype=torch.uint32, pin_memory=True)
+                # two pinned staging buffers: the file read of one partition overlaps
+                # the H2D of the previous one (copy stream) and the top-k before it
+                stage = [torch.empty(cap, dtype=torch.uint32, pin_memory=True) for _ in range(2)]
 
-            def load(part):
+            def load(part, slot=0):
                 if not is_file:
                     chunk = source[part.offset:part.offset + part.length]
                     return to_device(chunk, device).keys if not isinstance(chunk, torch.Tensor) or not chunk.is_cuda \
                         else chunk
-                host = read_vector(source, offset=part.offset, count=part.length,
-                                   out=stage.numpy()[: part.length])
-                del host
+                if stage_ev[slot] is not None:
+                    stage_ev[slot].synchronize()  # its previous H2D has finished reading it
+                buf = stage[slot]
+                read_vector(source, offset=part.offset, count=part.length, out=buf.numpy()[: part.length])
                 dev = torch.empty(part.length, dtype=torch.uint32, device=device)
-                dev.copy_(stage[: part.length], non_blocking=True)
-                stream.synchronize()
+                copy.wait_stream(stream)
+                with torch.cuda.stream(copy):
+                    dev.copy_(buf[: part.length], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                stage_ev[slot] = ev
+                stream.wait_event(ev)  # the top-k of this partition runs after its copy
+                dev.record_stream(stream)
                 return dev
 
             resident = {i: load(plan_.partitions[i]) for i in parts if plan_.partitions[i].resident}
             reload_nanos, vals, idxs = 0, [], []
             t_compute = time.perf_counter_ns()
+            streamed = [i for i in parts if i not in resident]
+            prefetched = {}
+            if streamed:  # the first reload starts before any compute
+                t0 = time.perf_counter_ns()
+                prefetched[streamed[0]] = load(plan_.partitions[streamed[0]], 0)
+                reload_nanos += time.perf_counter_ns() - t0
             for i in parts:
                 part = plan_.partitions[i]
                 if i in resident:
                     chunk = resident.pop(i)
                 else:  # a partition beyond the residency cap: streamed from the file (reload overhead)
-                    t0 = time.perf_counter_ns()
-                    chunk = load(part)
-                    reload_nanos += time.perf_counter_ns() - t0
+                    chunk = prefetched.pop(i)
+                    pos = streamed.index(i)
+                    if pos + 1 < len(streamed):  # read the next one while this one is on the GPU
+                        t0 = time.perf_counter_ns()
+                        nxt = streamed[pos + 1]
+                        prefetched[nxt] = load(plan_.partitions[nxt], (pos + 1) % 2)
+                        reload_nanos += time.perf_counter_ns() - t0
                 r = dr_topk(chunk, replace(cfg, k=min(k, part.length)))
                 vals.append(r.values)
                 idxs.append(r.indices + part.offset)

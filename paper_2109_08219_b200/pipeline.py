@@ -132,6 +132,48 @@ class DrTopK:
         )
         _native.check(st, "dtopk_select")
 
+    def stream_from_host(self, hv: "_device.HostVector", dev_keys: torch.Tensor) -> None:
+        """Copy a host vector into ``dev_keys`` range by range and run K1 on each
+        range as it lands (dtopk_delegates_range), then finish the call
+        (dtopk_select with DTOPK_FLAG_DELEGATES_DONE).  Stream-ordered on the
+        current stream; pageable inputs pass through pinned staging."""
+        c = self.cfg
+        lib = self.lib
+        comp = torch.cuda.current_stream(self.device)
+        bufs, evs, copy = _device.staging_buffers(self.device)
+        copy.wait_stream(comp)  # the destination / workspace are free once earlier work on comp is done
+        src = hv.host.view(torch.int32) if hv.host.dtype != torch.float32 else hv.host.view(torch.int32)
+        dst = dev_keys.view(torch.int32)
+        pinned = src.is_pinned()
+        n, R = self.n, _device.STREAM_RANGE
+        nch = -(-n // 2048)
+        for r, a in enumerate(range(0, n, R)):
+            b = min(n, a + R)
+            if pinned:
+                part = src[a:b]
+            else:
+                j = r % 2
+                if evs[j] is not None:
+                    evs[j].synchronize()  # the H2D that last read this staging buffer is done
+                part = bufs[j][: b - a]
+                part.copy_(src[a:b])
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(copy):
+                dst[a:b].copy_(part, non_blocking=True)
+                ev.record(copy)
+            if not pinned:
+                evs[r % 2] = ev
+            comp.wait_event(ev)
+            c0, c1 = a // 2048, (nch if b == n else b // 2048)
+            _native.check(lib.dtopk_delegates_range(dev_keys.data_ptr(), n, self.code, c.k, int(c.largest), c.alpha,
+                                                    c.beta, c0, c1, self.ws.data_ptr(), self.ws_bytes,
+                                                    comp.cuda_stream), "dtopk_delegates_range")
+        st = lib.dtopk_select(
+            dev_keys.data_ptr(), n, self.code, c.k, int(c.largest), c.alpha, c.beta, 0,
+            self.flags | _native.FLAG_DELEGATES_DONE, self.values.data_ptr(), self.indices.data_ptr(), 0,
+            self.ws.data_ptr(), self.ws_bytes, comp.cuda_stream, self.events)
+        _native.check(st, "dtopk_select")
+
     def header(self) -> _native.DtopkResult:
         return read_header(self.ws)
 
@@ -187,22 +229,38 @@ def dr_topk(v, cfg: PipelineConfig, *, stats: WorkloadStats | None = None, exact
     ``threshold == values[-1]`` and the work counters.
     """
     _native.load()  # fails loudly (NativeUnavailable) without libdtopk.so or a CUDA device
-    dv = _device.to_device(v)
     stats = stats if stats is not None else WorkloadStats()
+    hv = _device.host_view(v)
+    if hv is not None and hv.n >= _device.STREAM_MIN:
+        vc = validate_config(cfg, hv.n)
+        if not vc.direct_fallback and vc.beta <= 8:
+            # large host input: H2D range by range, K1 overlapped with the copy
+            dev = torch.device("cuda", torch.cuda.current_device())
+            plan = DrTopK(hv.n, cfg, hv.code, hv.out_dtype, dev, exact_stats=exact_stats)
+            keys = torch.empty(hv.n, dtype=torch.int32, device=dev)
+            with torch.cuda.device(dev):
+                plan.stream_from_host(hv, keys)
+                hdr = plan.header()
+            return _result(plan, hdr, stats, hv.code, hv.kind)
+    dv = _device.to_device(v)
     plan = DrTopK(dv.n, cfg, dv.code, dv.out_dtype, dv.device, exact_stats=exact_stats)
     with torch.cuda.device(dv.device):
         plan.launch(dv.keys)
         hdr = plan.header()
+    return _result(plan, hdr, stats, dv.code, dv.kind)
+
+
+def _result(plan: "DrTopK", hdr, stats: WorkloadStats, code: int, kind: str) -> TopKResult:
     plan.fill_stats(stats, hdr)
     k_out = int(hdr.k_out)
     values = plan.values[:k_out]
     indices = plan.indices[:k_out]
-    threshold = _device.key_to_value(int(hdr.kth_key), dv.code, plan.cfg.largest)
+    threshold = _device.key_to_value(int(hdr.kth_key), code, plan.cfg.largest)
     return TopKResult(
-        values=_device.to_caller(values, dv.kind),
+        values=_device.to_caller(values, kind),
         threshold=threshold,
         stats=stats,
-        indices=_device.to_caller(indices, dv.kind),
+        indices=_device.to_caller(indices, kind),
     )
 
 

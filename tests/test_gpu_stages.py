@@ -88,3 +88,32 @@ def test_dr_topk_beta_40(dist, oracle_mod, cuda):
 
     v = data.generate(dist, (1 << 21) + 5, seed=40, device=cuda)
     check_topk(v, 3000, oracle_mod, alpha=9, auto_alpha=False, beta=40)
+
+
+# ---------------------------------------------------------------- streamed host input (row f1)
+@pytest.mark.parametrize("kind,n,k,largest,dtype", [
+    ("numpy", (1 << 25) + 4099, 1000, True, "u32"),      # pageable: pinned staging, 3 ranges, ragged tail
+    ("numpy", 1 << 25, 1, True, "u32"),                  # alpha > 11: k1_merge after the last range
+    ("pinned", (1 << 24) + 2048, 70000, False, "u32"),   # pinned: direct DMA per range
+    ("torch_cpu", (1 << 24) + 5, 3000, True, "f32"),
+])
+def test_streamed_host_input(kind, n, k, largest, dtype, oracle_mod, cuda):
+    from paper_2109_08219_b200 import _device
+
+    g = data.generate("normal_f32" if dtype == "f32" else "uniform", n, seed=n % 97, device=cuda)
+    host = g.cpu()
+    if kind == "pinned":
+        host = host.pin_memory()
+    v = host.numpy() if kind == "numpy" else host
+    assert n >= _device.STREAM_MIN
+    r = dtopk.dr_topk(v, dtopk.PipelineConfig(k=k, largest=largest))
+    keys = oracle_mod.to_keys(host.numpy(), largest)
+    ek, ei = oracle_mod.topk_with_indices(keys, k)
+    gi = np.asarray(r.indices.numpy() if isinstance(r.indices, torch.Tensor) else r.indices)
+    gv = np.asarray(r.values.numpy() if isinstance(r.values, torch.Tensor) else r.values)
+    np.testing.assert_array_equal(gi, ei)
+    np.testing.assert_array_equal(oracle_mod.to_keys(gv, largest), ek)
+    # counters equal the resident-input call's
+    r2 = dtopk.dr_topk(g, dtopk.PipelineConfig(k=k, largest=largest))
+    for f in ("delegate_vector_len", "fully_qualified_subranges", "partially_qualified_subranges"):
+        assert getattr(r.stats, f) == getattr(r2.stats, f), f
