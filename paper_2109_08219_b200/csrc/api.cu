@@ -17,6 +17,8 @@
 #include <set>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "assemble.cuh"
 #include "delegate.cuh"
@@ -34,6 +36,18 @@
 using namespace dtopk;
 
 namespace {
+
+// NVTX ranges (header-only NVTX3; inert unless a profiler is attached): every
+// C entry point, and the reference's stages (core.STAGES) inside a call, so
+// an nsys timeline groups the kernel launches as Delegate / FirstK / Concat /
+// SecondK.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define DTOPK_RANGE(name) NvtxRange nvtx_range_(name)
 
 std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library
 thread_local unsigned long long t_launches = 0;  // kernels launched (or captured) by this thread
@@ -423,6 +437,7 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   }
   cudaMemsetAsync(ws, 0, L.zero_bytes, s);
   rec(ev, 0, s);
+  nvtxRangePushA("Delegate");
   const bool filt = filt_possible(L.S, alpha, beta, 0);
   if (filt) {
     const u64 nch_full = n >> K1_LOG_CHUNK;
@@ -434,7 +449,9 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
     counted();
   }
   stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm, filt ? 1 : 0);
+  nvtxRangePop();
   rec(ev, 1, s);
+  DTOPK_RANGE("FirstK");
   const bool g = gc != nullptr && filt;
   const K2Args k2 = k2_args(ws, L, k, beta, alpha, filt ? 1 : 0, g ? gc->fb : cudaGraphConditionalHandle{}, g ? 1 : 0);
   if (beta == 2)
@@ -635,6 +652,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   // No external theta here, so a tie-heavy call may drop tie-only superset
   // entries past the first k ties (not with exact stats: |C| counts every one)
   if (fused) theta_resolve(ws, L, k, beta, s, nsm, (flags & DTOPK_FLAG_EXACT_STATS) == 0);
+  nvtxRangePushA("Concat");
   Records rc{reinterpret_cast<uint4*>(ws + L.rec)};
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);
   u32* t_sid = reinterpret_cast<u32*>(ws + L.t_sid);
@@ -703,6 +721,8 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
                                                                       k5.d_need, k5.ties);
   counted();
   rec(ev, 3, s_outer);
+  nvtxRangePop();
+  DTOPK_RANGE("SecondK");
   ensure_smem(finish_small<MODE>, SMALL_POOL * 8);
   const bool need_tail = std::max<u64>(L.cap_gt, k) > (u64)SMALL_POOL;  // pools beyond SMALL_POOL possible
   const bool cond = g && need_tail;
@@ -865,6 +885,7 @@ struct dtopk_plan_s {
 dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha, int beta,
                                int direct, uint32_t flags, void* out_values, int64_t* out_indices,
                                int64_t index_offset, void* ws, size_t ws_bytes, dtopk_plan* out_plan) {
+  DTOPK_RANGE("dtopk_plan_create");
   if (out_plan == nullptr) return DTOPK_INVALID_ARG;
   *out_plan = nullptr;
   dtopk_status st = check_common(keys, n, dtype, k);
@@ -935,6 +956,7 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
 }
 
 dtopk_status dtopk_plan_launch(dtopk_plan plan, void* stream) {
+  DTOPK_RANGE("dtopk_plan_launch");
   if (plan == nullptr || plan->exec == nullptr) return DTOPK_INVALID_ARG;
   if (cudaGraphLaunch(plan->exec, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess) return cuda_status();
   counted((int)plan->main_kernels);
@@ -992,6 +1014,7 @@ const char* dtopk_version(void) { return "dtopk-b200 0.1.0 (sm_100a)"; }
 
 dtopk_status dtopk_select_begin(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha, int beta,
                                 uint32_t flags, void* ws, size_t ws_bytes, void* stream, void* const* stage_events) {
+  DTOPK_RANGE("dtopk_select_begin");
   (void)flags;
   dtopk_status st = check_common(keys, n, dtype, k);
   if (st != DTOPK_OK) return st;
@@ -1011,6 +1034,7 @@ dtopk_status dtopk_select_finish(const void* keys, uint64_t n, int dtype, uint64
                                  uint32_t flags, const int64_t* theta_override, void* out_values,
                                  int64_t* out_indices, int64_t index_offset, void* ws, size_t ws_bytes,
                                  void* stream, void* const* stage_events) {
+  DTOPK_RANGE("dtopk_select_finish");
   dtopk_status st = check_common(keys, n, dtype, k);
   if (st != DTOPK_OK) return st;
   if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
@@ -1030,6 +1054,7 @@ dtopk_status dtopk_select_finish(const void* keys, uint64_t n, int dtype, uint64
 dtopk_status dtopk_select(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha, int beta,
                           int direct, uint32_t flags, void* out_values, int64_t* out_indices, int64_t index_offset,
                           void* ws, size_t ws_bytes, void* stream, void* const* stage_events) {
+  DTOPK_RANGE("dtopk_select");
   dtopk_status st = check_common(keys, n, dtype, k);
   if (st != DTOPK_OK) return st;
   if (out_values == nullptr || out_indices == nullptr) return DTOPK_INVALID_ARG;
@@ -1065,6 +1090,7 @@ dtopk_status dtopk_select(const void* keys, uint64_t n, int dtype, uint64_t k, i
 dtopk_status dtopk_delegates_range(const void* keys, uint64_t n, int dtype, uint64_t k, int largest, int alpha,
                                    int beta, uint64_t chunk_begin, uint64_t chunk_end, void* ws, size_t ws_bytes,
                                    void* stream) {
+  DTOPK_RANGE("dtopk_delegates_range");
   dtopk_status st = check_common(keys, n, dtype, k);
   if (st != DTOPK_OK) return st;
   if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
@@ -1083,6 +1109,7 @@ dtopk_status dtopk_delegates_range(const void* keys, uint64_t n, int dtype, uint
 
 dtopk_status dtopk_extract_delegates(const void* keys, uint64_t n, int dtype, int largest, int alpha, int beta,
                                      uint32_t* out_delegates, void* ws, size_t ws_bytes, void* stream) {
+  DTOPK_RANGE("dtopk_extract_delegates");
   dtopk_status st = check_common(keys, n, dtype, 1);
   if (st != DTOPK_OK) return st;
   if ((st = check_delegate(n, alpha, beta)) != DTOPK_OK) return st;
@@ -1099,6 +1126,7 @@ dtopk_status dtopk_extract_delegates(const void* keys, uint64_t n, int dtype, in
 
 dtopk_status dtopk_kth_largest(const uint32_t* keys, uint64_t n, uint64_t k, uint32_t* out_kth, void* ws,
                                size_t ws_bytes, void* stream) {
+  DTOPK_RANGE("dtopk_kth_largest");
   dtopk_status st = check_common(keys, n, DTOPK_U32, k);
   if (st != DTOPK_OK) return st;
   if (out_kth == nullptr) return DTOPK_INVALID_ARG;
@@ -1129,6 +1157,7 @@ dtopk_status dtopk_merge_lists(int dtype, int largest, const uint32_t* in_val, i
                                const int64_t* in_off, int64_t in_stride, const int64_t* in_len,
                                int64_t len_stride, int n_lists, uint64_t cap, uint32_t* out_val, int64_t* out_idx, uint32_t* tmp_val, int64_t* tmp_idx,
                                int64_t* tmp_len, void* stream) {
+  DTOPK_RANGE("dtopk_merge_lists");
   if (dtype != DTOPK_U32 && dtype != DTOPK_F32) return DTOPK_INVALID_ARG;
   if (n_lists < 1 || cap < 1 || (vstride != 1 && vstride != 2) || vmul < 1) return DTOPK_INVALID_ARG;
   if (!in_val || !in_idx || !in_len || !out_val || !out_idx || !tmp_len) return DTOPK_INVALID_ARG;
@@ -1150,6 +1179,7 @@ dtopk_status dtopk_dsel_init(int64_t* state, int64_t* hist, uint64_t k, void* st
 
 dtopk_status dtopk_dsel_hist(int dtype, int largest, const uint32_t* bits, const int64_t* cnt, uint64_t cap,
                              const int64_t* state, int pass, int64_t* hist, void* stream) {
+  DTOPK_RANGE("dtopk_dsel_hist");
   if (dtype != DTOPK_U32 && dtype != DTOPK_F32) return DTOPK_INVALID_ARG;
   if (!bits || !cnt || !state || !hist || pass < 0 || pass > 2) return DTOPK_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1159,6 +1189,7 @@ dtopk_status dtopk_dsel_hist(int dtype, int largest, const uint32_t* bits, const
 
 dtopk_status dtopk_dsel_digit(int dtype, int largest, int64_t* state, int64_t* hist, int pass, const uint32_t* bits,
                               const int64_t* cnt, int64_t* gt_eq, void* stream) {
+  DTOPK_RANGE("dtopk_dsel_digit");
   if (dtype != DTOPK_U32 && dtype != DTOPK_F32) return DTOPK_INVALID_ARG;
   if (!state || !hist || !bits || !cnt || !gt_eq || pass < 0 || pass > 2) return DTOPK_INVALID_ARG;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1169,6 +1200,7 @@ dtopk_status dtopk_dsel_digit(int dtype, int largest, int64_t* state, int64_t* h
 dtopk_status dtopk_dsel_place(const int64_t* gathered, const int64_t* state, int rank, int world, uint64_t k,
                               const uint32_t* bits, const int64_t* idx, int64_t* slots, int64_t* seg_off,
                               int64_t* seg_len, void* stream) {
+  DTOPK_RANGE("dtopk_dsel_place");
   if (!gathered || !state || !bits || !idx || !slots || !seg_off || !seg_len) return DTOPK_INVALID_ARG;
   if (world < 1 || rank < 0 || rank >= world || k < 1) return DTOPK_INVALID_ARG;
   const int g = grid_for((k + 255) / 256, num_sms() * 4);
@@ -1183,6 +1215,7 @@ dtopk_status dtopk_dsel_place(const int64_t* gathered, const int64_t* state, int
 dtopk_status dtopk_qualify(const uint32_t* delegates, uint64_t n_delegates, int beta, uint32_t theta,
                            uint32_t* sel_values, uint32_t* sel_tags, uint32_t* part_values, uint32_t* part_tags,
                            uint32_t* fq_sids, int64_t* out_counts, void* ws, size_t ws_bytes, void* stream) {
+  DTOPK_RANGE("dtopk_qualify");
   if (!delegates || !out_counts || beta < 1 || n_delegates == 0 || n_delegates % (uint64_t)beta) return DTOPK_INVALID_ARG;
   if (!sel_values || !sel_tags || !part_values || !part_tags || !fq_sids) return DTOPK_INVALID_ARG;
   const u64 tiles = (n_delegates + STG_TILE - 1) / STG_TILE;
@@ -1204,6 +1237,7 @@ size_t dtopk_stage_workspace_bytes(uint64_t n_elements) {
 dtopk_status dtopk_concat(const void* keys, uint64_t n, int dtype, int largest, int alpha, const uint32_t* fq_sids,
                           uint64_t n_fq, uint32_t theta, void* out_values, int64_t* out_count, void* ws,
                           size_t ws_bytes, void* stream) {
+  DTOPK_RANGE("dtopk_concat");
   dtopk_status st = check_common(keys, n, dtype, 1);
   if (st != DTOPK_OK) return st;
   if (alpha < 0 || alpha > 40 || !out_values || !out_count || (n_fq && !fq_sids)) return DTOPK_INVALID_ARG;

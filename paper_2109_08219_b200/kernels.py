@@ -52,8 +52,10 @@ def radix_topk(values, k, *, skip_last=False, digit_bits=RADIX_BITS, tags=None, 
                largest: bool = True):
     """Exact (or skip_last-relaxed) radix top-k (kernels.py:109-165).
 
-    Returns (selected_values, selected_tags, threshold); selected values are
-    ordered best first.  ``digit_bits`` is validated like the reference but
+    Returns (selected_values, selected_tags, threshold) in the reference's order
+    and dtype: elements above the k-th in scan order, then the k-th's ties in
+    scan order (``_extract_exact``), or every element >= the relaxed edge in
+    scan order (``_extract_at_least``); values in the input dtype.  ``digit_bits`` is validated like the reference but
     the device always uses its own 11/11/10 digits; ``states`` is not
     recorded on the device.
     """
@@ -73,9 +75,21 @@ def radix_topk(values, k, *, skip_last=False, digit_bits=RADIX_BITS, tags=None, 
     with torch.cuda.device(dv.device):
         plan.launch(dv.keys)
         hdr = plan.header()
-    idx = plan.indices
-    sel = plan.values
-    threshold = _device.key_to_value(int(hdr.kth_key), dv.code, largest)
+    # _extract_exact's order (kernels.py:83-96): every element above the k-th in
+    # scan order, then the k-th's ties in scan order.  The device answer is
+    # ordered (key desc, index asc), so its ties already close it in index
+    # order; only the strictly-better head is re-sorted by index.
+    kth = int(hdr.kth_key)
+    bits = dv.keys.view(torch.int32)
+    keyv = plan.values.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    if dv.code == _native.DTYPE_F32:
+        keyv = torch.where(keyv >> 31 == 1, keyv ^ 0xFFFFFFFF, keyv | 0x80000000)
+    if not largest:
+        keyv = 0xFFFFFFFF - keyv
+    n_gt = int((keyv > kth).sum().item())
+    idx = torch.cat([torch.sort(plan.indices[:n_gt]).values, plan.indices[n_gt:]])
+    sel = bits[idx].view(plan.values.dtype) if plan.values.dtype != torch.int32 else bits[idx]
+    threshold = _device.key_to_value(kth, dv.code, largest)
     if skip_last:
         # kernels.py:161-164: every element at or above the lower edge of the
         # 256-wide bucket holding the k-th key; threshold = their minimum.
@@ -84,8 +98,8 @@ def radix_topk(values, k, *, skip_last=False, digit_bits=RADIX_BITS, tags=None, 
             raise NotImplementedError("skip_last relaxation is defined on uint32-largest keys only")
         edge = int(hdr.kth_key) & 0xFFFFFF00
         mask = keys64 >= edge
-        idx = torch.nonzero(mask).flatten()
-        sel = keys64[idx]
+        idx = torch.nonzero(mask).flatten()  # _extract_at_least: scan order
+        sel = bits[idx].view(torch.uint32) if plan.values.dtype == torch.uint32 else bits[idx]
         threshold = int((keys64[idx]).min().item())
     if stats is not None:
         stats.add_read(2 * dv.n)

@@ -255,6 +255,29 @@ def test_radix_topk_mirror(oracle_mod, cuda):
     assert dtopk.kth_largest(v, 99) == int(exp[0])
 
 
+@pytest.mark.parametrize("dist", ["uniform", "few_distinct"])
+def test_radix_topk_reference_order_and_dtype(dist, cuda):
+    """kernels._extract_exact order (kernels.py:83-96): elements above the k-th in
+    scan order, then ties in scan order; _extract_at_least (skip_last): every
+    element >= the relaxed edge in scan order; values keep the input dtype."""
+    v = data.generate(dist, 5000, seed=3, device=cuda)
+    h = v.cpu().numpy()
+    tags = torch.arange(5000, device=cuda, dtype=torch.int64)
+    sel, st, thr = dtopk.radix_topk(v, 300, tags=tags)
+    kth = np.sort(h)[-300]
+    gt = np.flatnonzero(h > kth)
+    idx = np.concatenate([gt, np.flatnonzero(h == kth)[: 300 - gt.size]])
+    assert sel.dtype == torch.uint32 and thr == int(kth)
+    np.testing.assert_array_equal(sel.cpu().numpy(), h[idx])
+    np.testing.assert_array_equal(st.cpu().numpy(), idx)
+    sel2, st2, thr2 = dtopk.radix_topk(v, 300, skip_last=True, tags=tags)
+    edge = int(kth) & 0xFFFFFF00
+    idx2 = np.flatnonzero(h >= edge)
+    assert sel2.dtype == torch.uint32 and thr2 == int(h[idx2].min())
+    np.testing.assert_array_equal(sel2.cpu().numpy(), h[idx2])
+    np.testing.assert_array_equal(st2.cpu().numpy(), idx2)
+
+
 def test_theta_override_split_path(oracle_mod, cuda):
     """begin/finish with an external theta (the multi-GPU exchange) on one GPU:
     the two halves of a vector, each filtered with max(theta_0, theta_1)."""
