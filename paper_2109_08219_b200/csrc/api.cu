@@ -66,7 +66,7 @@ struct Layout {
   size_t ctrl, lb_emg, lb_eme, zero_bytes, k5_tg, k5_te;
   size_t D, meta, partial, pmeta, selbuf, region_cnt, sup_sid, sup_in, sup_cnt, sup_off, rec, e_sid, t_sid, t_cnt,
       stg_key, stg_idx, seg_gt, seg_eq, d_sid, d_pos, d_need, e_gpos, e_epos, gt_keys, gt_idx, ties, sak, sai, sbk, sbi, counts,
-      digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, chunk_cnt, tseg, total;
+      digit_base, digit_tot, bk_total, bk_count, bk_start, bk_comp, bk_info, chunk_cnt, tseg, sel_tcnt, total;
   u64 fcap, S, nch, W, cap_gt, cap_e, cap_d, m_emit, k4_tiles, k5_tiles, em_tiles, sort_tiles, D_len, nseg, words, R2,
       sort_cap;
   u32 g2;
@@ -127,8 +127,8 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.sort_tiles = (L.sort_cap + ST_TILE - 1) / ST_TILE;
   L.ctrl = take(sizeof(Ctrl));
   L.bk_total = take(L.sort_cap > (u64)SMALL_SORT ? BK_MAX * 4 : 0);
-  L.lb_emg = take(L.em_tiles * 8);
-  L.lb_eme = take(L.em_tiles * 8);
+  L.lb_emg = take((L.em_tiles + 1) * 8);  // + 1: emit_count's total sentinel
+  L.lb_eme = take((L.em_tiles + 1) * 8);
   L.zero_bytes = off;
   L.D = take(L.D_len * 4);
   L.meta = take(L.S * 4);
@@ -176,6 +176,7 @@ Layout make_layout(u64 n, u64 k, int alpha, int beta, int direct) {
   L.bk_comp = take(bk ? L.sort_cap * 8 : 0);
   L.chunk_cnt = take(filt ? L.nch * 4 : 0);
   L.tseg = take(direct ? 0 : (u64)L.g2 * 8 * 8);
+  L.sel_tcnt = take((L.m_emit / 2048 + 1) * 4);
   L.total = off;
   return L;
 }
@@ -533,7 +534,8 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
   }
   const u64 mcap = m_dev ? L.cap_gt : m_host;
   const int gs = grid_for((mcap + 2047) / 2048, nsm * 4);
-  SelArgs sp{keys_for_emit, m_host, m_dev, ctrl, &ctrl->selP, selbuf, k, direct ? 0 : 1};
+  SelArgs sp{keys_for_emit, m_host, m_dev, ctrl, &ctrl->selP, selbuf, k, direct ? 0 : 1,
+             reinterpret_cast<u32*>(ws + L.sel_tcnt)};
   if (direct) {
     sel_pass1<MODE><<<gs, 256, 0, cs>>>(sp);
     counted();
@@ -542,7 +544,7 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
   } else {
     sel_pass1<KM_KEY><<<gs, 256, 0, cs>>>(sp);
     counted();
-    sel_pass2<KM_KEY><<<gs, 256, 0, cs>>>(sp);
+    sel_pass2<KM_KEY><<<grid_for((mcap + 2047) / 2048, nsm * 8), 256, 0, cs>>>(sp);  // latency-bound: 8 CTAs / SM
     counted();
   }
   sel_pass3<<<gs, 256, 0, cs>>>(sp);
@@ -560,11 +562,14 @@ void big_tail(u64 k, const u32* keys_for_emit, const u64* idx_for_emit, const ul
   em.lb_eq = reinterpret_cast<u64*>(ws + L.lb_eme);
   em.check_path = direct ? 0 : 1;
   em.direct = direct;
-  if (direct)
+  if (direct) {
     scan_emit<MODE><<<grid_for(L.em_tiles, nsm * 4), 256, 0, cs>>>(em);
-  else
-    scan_emit<KM_KEY><<<grid_for(L.em_tiles, nsm * 4), 256, 0, cs>>>(em);
-  counted();
+    counted();
+  } else {  // pool select: count + scan, then write only the tiles that emit
+    emit_count<KM_KEY><<<grid_for(L.em_tiles, nsm * 8), 256, 0, cs>>>(em);
+    emit_write<KM_KEY><<<grid_for(L.em_tiles, nsm * 4), 256, 0, cs>>>(em);
+    counted(2);
+  }
   if (g) {
     gc->ok = gc->ok && cond_end(gc->s2);
     cs = s;
@@ -681,7 +686,13 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
             reinterpret_cast<u64*>(ws + L.stg_idx), reinterpret_cast<u32*>(ws + L.seg_gt),
             reinterpret_cast<u32*>(ws + L.seg_eq), L.cap_e};
-  launch_pdl(k4_read<MODE>, dim3(grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4)), dim3(256), 0, s, k4);
+  launch_pdl(k4_read<MODE, 0>, dim3(grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4)), dim3(256), 0, s,
+             k4);
+  if (L.cap_e << alpha >= DTOPK_K4_BIG_KEYS) {
+    launch_pdl(k4_read<MODE, 1>, dim3(grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 3)), dim3(256),
+               0, s, k4);
+    counted();
+  }
   counted();
   const int exact = (flags & DTOPK_FLAG_EXACT_STATS) ? 1 : 0;
   K4TArgs k4t{keys, n,  L.S,   alpha, k, ctrl, t_sid, t_cnt, rc.r, reinterpret_cast<const u32*>(ws + L.seg_eq),
@@ -1138,7 +1149,8 @@ dtopk_status dtopk_kth_largest(const uint32_t* keys, uint64_t n, uint64_t k, uin
   cudaMemsetAsync(w, 0, L.zero_bytes, s);
   const int nsm = num_sms();
   const int gs = grid_for((n + 2047) / 2048, nsm * 4);
-  SelArgs sd{keys, n, nullptr, ctrl, &ctrl->selP, reinterpret_cast<u32*>(w + L.selbuf), k, 0};
+  SelArgs sd{keys, n, nullptr, ctrl, &ctrl->selP, reinterpret_cast<u32*>(w + L.selbuf), k, 0,
+             reinterpret_cast<u32*>(w + L.sel_tcnt)};
   sel_pass1<KM_KEY><<<gs, 256, 0, s>>>(sd);
   counted();
   sel_pass2<KM_KEY><<<gs, 256, 0, s>>>(sd);

@@ -278,11 +278,19 @@ struct K4Args {
 // K4: read the E candidates.  A tile is 8192 keys: 8192 / W whole candidates,
 // or one part of a candidate when W > 8192.  Ranks inside each segment come
 // from a tile-wide exclusive scan minus the scan value at the segment start.
-template <int MODE>
-__global__ void __launch_bounds__(256) k4_read(K4Args a) {
+#ifndef DTOPK_K4_BIG_KEYS
+#define DTOPK_K4_BIG_KEYS (1ull << 21)
+#endif
+// BIG: the instantiation for calls that re-read more than DTOPK_K4_BIG_KEYS keys
+// (ascending input: 8.4 M), register-capped for 3 CTAs per SM; the uncapped one
+// serves the rest (capping it slowed small k).  Both are launched; each exits
+// at once when the other one owns the call.
+template <int MODE, int BIG>
+__global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
   pdl_trigger();
   pdl_wait();
   if (ld_volatile_u32(&a.ctrl->small_done)) return;  // finished by fast_tail
+  if (((u64)min((u64)ld_volatile_u32(&a.ctrl->nE), a.cap_e) << a.alpha >= DTOPK_K4_BIG_KEYS) != (BIG != 0)) return;
   __shared__ u32 s_wg[8], s_we[8];
   __shared__ u32 s_seg_g[K4_TILE / 4], s_seg_e[K4_TILE / 4];
   __shared__ u32 s_max[8];
@@ -904,9 +912,26 @@ __global__ void __launch_bounds__(256) k5b_copy(Ctrl* ctrl, int alpha, u64 k, co
     }
     const u32 ng = seg_gt[sg], ne = seg_eq[sg];
     const u64 sb = sg << lseg;
-    for (u32 z = lane; z < ng; z += 32) {
-      gt_keys[go + z] = stg_key[sb + z];
-      gt_idx[go + z] = stg_idx[sb + z];
+    // 8 rounds of loads in flight before their stores (the plain loop kept one)
+    for (u32 z0 = 0; z0 < ng; z0 += 256) {
+      u32 kk[8];
+      u64 ii[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const u32 z = z0 + u * 32 + lane;
+        if (z < ng) {
+          kk[u] = stg_key[sb + z];
+          ii[u] = stg_idx[sb + z];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const u32 z = z0 + u * 32 + lane;
+        if (z < ng) {
+          gt_keys[go + z] = kk[u];
+          gt_idx[go + z] = ii[u];
+        }
+      }
     }
     for (u32 z = lane; z < ne && eo + z < k; z += 32) ties[eo + z] = stg_idx[sb + seglen - 1 - z];
   }

@@ -209,6 +209,220 @@ __global__ void __launch_bounds__(256, DTOPK_TAIL_MINB) scan_emit(ScanArgs a) {
   }
 }
 
+// Ordered emit for the pool select (not the direct path), in two kernels
+// instead of scan_emit's decoupled look-back: emit_count counts keys above /
+// equal to tau per SC_TILE tile and its last CTA turns the counts into
+// exclusive prefixes; emit_write re-reads only the tiles that hold something to
+// emit.  On sorted pools (ascending input: 8.4 M keys, the answer in the last
+// few tiles) scan_emit stalled ~45 us on the look-back chain.
+template <int MODE>
+__device__ __forceinline__ u32 em_tau(const Ctrl* ctrl, DigitResult* r3s, ull* scratch) {
+  const DigitResult r1 = ctrl->selP.r1, r2 = ctrl->selP.r2;
+  find_digit<NB3>(ctrl->selP.hist3, r2.rem, r3s, scratch);
+  return (r1.digit << 21) | (r2.digit << 10) | r3s->digit;
+}
+
+template <int MODE>
+__device__ __forceinline__ void em_load(const ScanArgs& a, u64 total, u64 tile, int j, u32 (&x)[4], u32& valid) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 v0 = tile * SC_TILE + (u64)warp * 1024 + (u64)j * 128 + (u64)lane * 4;
+  x[0] = x[1] = x[2] = x[3] = 0u;
+  valid = 0;
+  if (v0 + 4 <= total) {
+    const uint4 q = ld_nc_v4(a.keys + v0);
+    x[0] = to_key<MODE>(q.x);
+    x[1] = to_key<MODE>(q.y);
+    x[2] = to_key<MODE>(q.z);
+    x[3] = to_key<MODE>(q.w);
+    valid = 0xfu;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+      if (v0 + c < total) {
+        x[c] = to_key<MODE>(a.keys[v0 + c]);
+        valid |= 1u << c;
+      }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) emit_count(ScanArgs a) {
+  __shared__ DigitResult r3s;
+  __shared__ ull scratch[8];
+  __shared__ u32 s_g[8], s_e[8], s_max[8];
+  __shared__ int am_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Ctrl* ctrl = a.ctrl;
+  if (a.check_path && ld_volatile_u32(&ctrl->big_mode) != BIG_SELECT) return;
+  const u32 tau = em_tau<MODE>(ctrl, &r3s, scratch);
+  if (blockIdx.x == 0 && tid == 0) {
+    ctrl->selP.r3 = r3s;
+    ctrl->selP.kth = tau;
+    ctrl->sort_lo = tau;
+    ctrl->sort_m = a.k;
+    ctrl->sort_src = 1u;  // pool select: the answer goes to sort buffer B
+    ctrl->res.k_out = a.k;
+    atomicMax(&ctrl->maxkey, tau);
+  }
+  const u64 total = a.m_dev ? (u64)*a.m_dev : a.m_host;
+  const u64 T = (total + SC_TILE - 1) / SC_TILE;
+  u32 bmax = 0;
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    u32 cg = 0, ce = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      u32 x[4], valid;
+      em_load<MODE>(a, total, tile, j, x, valid);
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const bool v = (valid >> c) & 1u;
+        cg += v && x[c] > tau;
+        ce += v && x[c] == tau;
+        if (v && x[c] > tau) bmax = max(bmax, x[c]);
+      }
+    }
+    cg = __reduce_add_sync(FULL, cg);
+    ce = __reduce_add_sync(FULL, ce);
+    if (lane == 0) {
+      s_g[warp] = cg;
+      s_e[warp] = ce;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      u64 g = 0, e = 0;
+      for (int w = 0; w < 8; w++) {
+        g += s_g[w];
+        e += s_e[w];
+      }
+      a.lb_gt[tile] = g;
+      a.lb_eq[tile] = e;
+    }
+    __syncthreads();
+  }
+  bmax = __reduce_max_sync(FULL, bmax);
+  if (lane == 0) s_max[warp] = bmax;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    u32 m = 0;
+    for (int w = 0; w < 8; w++) m = max(m, s_max[w]);
+    if (m) atomicMax(&ctrl->maxkey, m);
+    am_last = atomicAdd(&ctrl->em_ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // exclusive prefixes of the tile counts (thread t: tiles [t * per, (t+1) * per))
+  const u64 per = (T + 255) / 256;
+  const u64 t0 = (u64)tid * per, t1 = min(T, t0 + per);
+  ull sg = 0, se = 0;
+  for (u64 t = t0; t < t1; t++) {
+    sg += __ldcg(&a.lb_gt[t]);
+    se += __ldcg(&a.lb_eq[t]);
+  }
+  const ull ig = block_incl_scan_256<ull>(sg, scratch);
+  ull rg = ig - sg;
+  const ull ie = block_incl_scan_256<ull>(se, scratch);
+  ull re = ie - se;
+  for (u64 t = t0; t < t1; t++) {
+    const ull g = __ldcg(&a.lb_gt[t]), e = __ldcg(&a.lb_eq[t]);
+    a.lb_gt[t] = rg;
+    a.lb_eq[t] = re;
+    rg += g;
+    re += e;
+  }
+  if (tid == 255) {
+    a.lb_gt[T] = ig;  // sentinels: the totals
+    a.lb_eq[T] = ie;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) emit_write(ScanArgs a) {
+  __shared__ DigitResult r3s;
+  __shared__ ull scratch[8];
+  __shared__ u32 s_g[8], s_e[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Ctrl* ctrl = a.ctrl;
+  if (a.check_path && ld_volatile_u32(&ctrl->big_mode) != BIG_SELECT) return;
+  const u32 tau = ld_volatile_u32(&ctrl->selP.kth);
+  const u64 eq_cap = ctrl->selP.r3.rem;  // ties needed
+  const u64 ngt = a.k - eq_cap;
+  u32* eqk = a.out_keys + ngt;
+  u64* eqi = a.out_idx + ngt;
+  const u64 total = a.m_dev ? (u64)*a.m_dev : a.m_host;
+  const u64 T = (total + SC_TILE - 1) / SC_TILE;
+  const u32 lt = lanemask_lt();
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    const u64 gx = a.lb_gt[tile], ex = a.lb_eq[tile];
+    const u64 ng = a.lb_gt[tile + 1] - gx, ne = a.lb_eq[tile + 1] - ex;
+    if (ng == 0 && (ne == 0 || ex >= eq_cap)) continue;  // nothing to emit here (uniform per CTA)
+    u32 kv[8][4], vm[8], cg = 0, ce = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      em_load<MODE>(a, total, tile, j, kv[j], vm[j]);
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const bool v = (vm[j] >> c) & 1u;
+        cg += v && kv[j][c] > tau;
+        ce += v && kv[j][c] == tau;
+      }
+    }
+    cg = __reduce_add_sync(FULL, cg);
+    ce = __reduce_add_sync(FULL, ce);
+    if (lane == 0) {
+      s_g[warp] = cg;
+      s_e[warp] = ce;
+    }
+    __syncthreads();
+    u64 gpos = gx, epos = ex;
+    for (int w = 0; w < warp; w++) {
+      gpos += s_g[w];
+      epos += s_e[w];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      u32 bg[4], be[4];
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const bool v = (vm[j] >> c) & 1u;
+        bg[c] = __ballot_sync(FULL, v && kv[j][c] > tau);
+        be[c] = __ballot_sync(FULL, v && kv[j][c] == tau);
+      }
+      if ((bg[0] | bg[1] | bg[2] | bg[3] | be[0] | be[1] | be[2] | be[3]) == 0) continue;
+      u64 go = gpos, eo = epos;
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        go += __popc(bg[c] & lt);
+        eo += __popc(be[c] & lt);
+      }
+      const u64 v0 = tile * SC_TILE + (u64)warp * 1024 + (u64)j * 128 + (u64)lane * 4;
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const bool g = (bg[c] >> lane) & 1u, e = (be[c] >> lane) & 1u;
+        if (g || (e && eo < eq_cap)) {
+          const u64 idx = a.idx_in ? a.idx_in[v0 + c] : v0 + c;
+          if (g) {
+            a.out_keys[go] = kv[j][c];
+            a.out_idx[go] = idx;
+          } else {
+            eqk[eo] = kv[j][c];
+            eqi[eo] = idx;
+          }
+        }
+        go += g;
+        eo += e;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        gpos += __popc(bg[c]);
+        epos += __popc(be[c]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 constexpr int SMALL_SORT = 8192;  // answers up to this size are sorted by one CTA
 
 // Decide how the pool beyond SMALL_POOL is finished (one thread).

@@ -747,6 +747,7 @@ struct SelArgs {
   u32* selbuf;
   u64 k;
   int check_path;  // run only when ctrl->res.path == PATH_SELECT
+  u32* tcnt;       // [ceil(m / 2048)] members of digit-1 bucket per sel_pass2 tile
 };
 
 __device__ __forceinline__ bool sel_skip(const SelArgs& a) {
@@ -810,14 +811,15 @@ __global__ void __launch_bounds__(256) sel_pass2(SelArgs a) {
     }
     if (lane == 0) s_wcnt[warp] = cnt;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      u32 tot = 0;
-      for (int w = 0; w < 8; w++) tot += s_wcnt[w];
-      s_base = tot ? atomicAdd(&a.sel->buf_count, (ull)tot) : 0ull;
+    // tile-private slots (the tile's own 2048 positions of selbuf): one global
+    // atomic counter per tile serialised ~1k tiles on sorted pools
+    u64 o = tile * 2048;
+    u32 tot = 0;
+    for (int w = 0; w < 8; w++) {
+      if (w < warp) o += s_wcnt[w];
+      tot += s_wcnt[w];
     }
-    __syncthreads();
-    u64 o = s_base;
-    for (int w = 0; w < warp; w++) o += s_wcnt[w];
+    if (threadIdx.x == 0) a.tcnt[tile] = tot;
 #pragma unroll
     for (int j = 0; j < 8; j++) {
       if ((bl[j] >> lane) & 1u) a.selbuf[o + __popc(bl[j] & lt)] = v[j];
@@ -841,10 +843,13 @@ __global__ void __launch_bounds__(256) sel_pass3(SelArgs a) {
   find_digit<NB2>(a.sel->hist2, r1.rem, &r2, scratch);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.sel->r2 = r2;
   const u32 b2 = r2.digit;
-  const u64 m = r1.cnt;
-  for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < m; i += (u64)gridDim.x * 256) {
-    const u32 x = a.selbuf[i];
-    if (dig2(x) == b2) atomicAdd(&shist[dig3(x)], 1u);
+  const u64 T = (sel_count(a) + 2047) / 2048;  // sel_pass2 tiles: members at tile * 2048, tcnt[tile] of them
+  for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    const u32 c = a.tcnt[tile];
+    for (u32 i = threadIdx.x; i < c; i += 256) {
+      const u32 x = a.selbuf[tile * 2048 + i];
+      if (dig2(x) == b2) atomicAdd(&shist[dig3(x)], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NB3; i += 256) {
