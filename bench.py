@@ -208,6 +208,22 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+COOLDOWN_S = 0.1  # idle before each timed batch (see cool())
+
+
+def cool():
+    """Let the board leave its power cap before a timed batch.  Under sustained
+    back-to-back 4 GiB passes a B200 reaches its 1000 W cap within ~0.5 s and
+    drops SM clocks (1965 -> 1740-1890 MHz): steps run 4-12 % slower
+    (profiles/r2/k1_drift.txt).  The headline region is 20 steps (~13 ms); the
+    sweep's and configs' batches get the same short idle gap before them so
+    every number is taken in the same (unthrottled) state."""
+    import torch
+
+    torch.cuda.synchronize()
+    time.sleep(COOLDOWN_S)
+
+
 def time_plan(p, v, stream, reps: int, batches: int = 5) -> float:
     """Median over `batches` of back-to-back plan replays (ms per step)."""
     import torch
@@ -218,6 +234,7 @@ def time_plan(p, v, stream, reps: int, batches: int = 5) -> float:
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     out = []
     for _ in range(batches):
+        cool()
         a.record(stream)
         for _ in range(reps):
             p.launch(v, stream)
@@ -398,6 +415,7 @@ def run_ours(args):
     launches0 = lib.dtopk_launch_count()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    cool()
     with ClockSampler(local) as clk:
         barrier()
         t_start.record(stream)
@@ -493,6 +511,9 @@ def run_ours(args):
                             f"auto alpha (Eq. 11, const 3) = {plan.cfg.alpha}, beta={plan.cfg.beta}",
                 "n_per_gpu": n, "k": k, "alpha": plan.cfg.alpha, "beta": plan.cfg.beta,
                 "l2": "inputs (4 GiB/GPU) larger than the 126 MB L2; no flush",
+                "cooldown": f"{COOLDOWN_S * 1e3:.0f} ms idle before each timed batch (headline, sweep, configs): "
+                            "sustained back-to-back steps hit the 1000 W power cap and run 4-12 % slower "
+                            "(profiles/r2/k1_drift.txt)",
                 "parallelism": f"shard{world}" if world > 1 else "single",
             },
             "roofline": roof,
@@ -520,6 +541,7 @@ def run_ours(args):
             reps = max(5, args.steps // 10)
             batch = []
             for _ in range(5):
+                cool()
                 a.record(stream)
                 for _ in range(reps):
                     p.launch(v, stream)

@@ -72,6 +72,10 @@ struct Layout {
   u32 g2;
 };
 
+// fast_tail holds <= FT_CAND qualifying subranges, and at least k / beta
+// subranges qualify: for larger k it could only bail out (~18 us at k = 2^20).
+inline bool ft_enabled(int alpha, int beta, u64 k) { return alpha <= FT_MAX_ALPHA && k <= (u64)beta * FT_CAND; }
+
 // Filtered delegate pass (K0 sample -> K1 records -> K2 over records): where
 // K1's D + meta writes are a measurable share of the stream (alpha 6..8: 12 B
 // per 256..1024 B read) and the records carry everything the rest of the
@@ -616,7 +620,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   // fast_tail: the whole post-theta work of a small call in one CTA (fast.cuh);
   // the general chain below runs only when it declines (graph: conditional node,
   // eager: every chain kernel returns when ctrl->small_done is set)
-  const bool fast = alpha <= FT_MAX_ALPHA;
+  const bool fast = ft_enabled(alpha, beta, k);
   const bool g = gc != nullptr;
   if (fast) {
     ensure_smem(fast_tail<MODE>, (int)FT_SMEM);
@@ -927,7 +931,8 @@ dtopk_status dtopk_plan_create(const void* keys, uint64_t n, int dtype, uint64_t
             cudaStreamCreateWithFlags(&gc.s6, cudaStreamNonBlocking) == cudaSuccess &&
             cudaGraphCreate(&p->graph, 0) == cudaSuccess &&
             cudaGraphConditionalHandleCreate(&gc.cond, p->graph, 0, cudaGraphCondAssignDefault) == cudaSuccess &&
-            cudaGraphConditionalHandleCreate(&gc.gen, p->graph, 1, cudaGraphCondAssignDefault) == cudaSuccess &&
+            (direct || !ft_enabled(alpha, beta, k) ||
+             cudaGraphConditionalHandleCreate(&gc.gen, p->graph, 1, cudaGraphCondAssignDefault) == cudaSuccess) &&
             (!filt_possible(L.S, alpha, beta, direct) ||
              cudaGraphConditionalHandleCreate(&gc.fb, p->graph, 0, cudaGraphCondAssignDefault) == cudaSuccess) &&
             cudaStreamBeginCaptureToGraph(p->cap, p->graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==

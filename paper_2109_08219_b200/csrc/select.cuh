@@ -373,7 +373,10 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
   }
 }
 
-constexpr int P3_SMALL = 8192;   // bucket members resolved by one CTA
+#ifndef DTOPK_P3_SMALL
+#define DTOPK_P3_SMALL 8192
+#endif
+constexpr int P3_SMALL = DTOPK_P3_SMALL;  // bucket members resolved by one CTA
 constexpr int P3_RPT = 3;        // regions per thread in that CTA's prefix
 constexpr int P3_REGIONS = 256 * P3_RPT;
 
