@@ -690,6 +690,10 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
             reinterpret_cast<u64*>(ws + L.stg_idx), reinterpret_cast<u32*>(ws + L.seg_gt),
             reinterpret_cast<u32*>(ws + L.seg_eq), L.cap_e};
+  if (beta <= 2 && (L.cap_e << alpha) >= DTOPK_PF_MIN_KEYS) {  // pool floor (every E record is then fully qualified)
+    launch_pdl(k4h_floor<MODE>, dim3(nsm * 4), dim3(256), 0, s, k4, static_cast<const uint4*>(rc.r), k);
+    counted();
+  }
   launch_pdl(k4_read<MODE, 0>, dim3(grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4)), dim3(256), 0, s,
              k4);
   if (L.cap_e << alpha >= DTOPK_K4_BIG_KEYS) {

@@ -298,6 +298,10 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Ctrl* ctrl = a.ctrl;
   const u32 theta = ctrl->res.theta;
+  // pool floor (K4h): keys above theta but below it cannot reach the answer;
+  // they are only counted (|C| stays exact), not staged
+  const u32 pf = ld_volatile_u32(&ctrl->pfloor);
+  ull st_lo = 0;
   const u64 nE = min((u64)ctrl->nE, a.cap_e);
   const int alpha = a.alpha;
   const u64 W = 1ull << alpha;
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
       for (u64 c = 0; c < 2 && b + c < a.n; c++) {
         const u32 key = to_key<MODE>(a.keys[b + c]);
         st_read++;
-        if (key > theta) {
+        if (key > theta && key >= pf) {
           a.stg_key[2 * e + g] = key;
           a.stg_idx[2 * e + g] = b + c;
           g++;
@@ -325,6 +329,8 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
         } else if (key == theta) {
           a.stg_idx[2 * e + 1 - q] = b + c;
           q++;
+        } else if (key > theta) {
+          st_lo++;
         }
       }
       a.seg_gt[e] = g;
@@ -366,7 +372,8 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
 #pragma unroll
       for (int c = 0; c < 4; c++) {
         const bool vv = (valid >> c) & 1u;
-        const bool g = vv && x[c] > theta;
+        const bool g = vv && x[c] > theta && x[c] >= pf;
+        st_lo += vv && x[c] > theta && x[c] < pf;
         cg += g;
         ce += vv && x[c] == theta;
         if (g) bmax = max(bmax, x[c]);
@@ -397,7 +404,7 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
 #pragma unroll
         for (int c = 0; c < 4; c++) {
           const bool vv = (vm[j] >> c) & 1u;
-          const u32 b1 = __ballot_sync(FULL, vv && kv[j][c] > theta);
+          const u32 b1 = __ballot_sync(FULL, vv && kv[j][c] > theta && kv[j][c] >= pf);
           const u32 b2 = __ballot_sync(FULL, vv && kv[j][c] == theta);
           bg += __popc(b1 & lt);
           be += __popc(b2 & lt);
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
         if (!((vm[j] >> c) & 1u)) continue;
         const u64 vc = v0 + c;
         const u32 key = kv[j][c];
-        if (key > theta) {
+        if (key > theta && key >= pf) {
           const u64 phys = ((u64)a.e_sid[vc >> alpha] << alpha) | (vc & (W - 1));
           a.stg_key[sbase + rg] = key;
           a.stg_idx[sbase + rg] = phys;
@@ -474,6 +481,8 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
     if (rd) atomicAdd((ull*)&ctrl->res.elements_reread, rd);
   }
   if (lane == 0 && st_gt) atomicAdd(&ctrl->sumEgt, st_gt);
+  st_lo = __reduce_add_sync(FULL, (u32)min(st_lo, (ull)0xffffffffu));
+  if (lane == 0 && st_lo) atomicAdd(&ctrl->below_floor, st_lo);
 }
 
 // K4T: count the ties of T candidates (d_1 == theta, max not unique,
@@ -494,6 +503,101 @@ __device__ __forceinline__ u32 count_ties_warp(const u32* __restrict__ keys, u64
   u32 c = 0;
   for (u64 e = lane; e < len; e += 32) c += to_key<MODE>(keys[b + e]) == theta;
   return __reduce_add_sync(FULL, c);
+}
+
+// K4h: the pool floor for calls that re-read many E keys (ascending input:
+// 8.4 M keys above theta for k = 2^16).  An exact histogram of the pool's keys
+// -- the E candidates' keys above theta plus the A records' single keys -- in
+// PF_BINS linear bins over (theta, maxkey]; the last CTA takes the lower edge
+// of the bin holding the k-th largest as `pfloor`.  At least k pool keys are
+// >= pfloor, so the answer lies above it: K4 stages only those (the rest is
+// counted for |C|), and P_gt shrinks to ~k + one bin, skipping the staging /
+// copy / select over millions of keys.  Exits at once for small re-reads.
+constexpr int PF_BINS = 2048;
+#ifndef DTOPK_PF_MIN_KEYS
+#define DTOPK_PF_MIN_KEYS (1ull << 21)
+#endif
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k4h_floor(K4Args a, const uint4* __restrict__ rec, u64 k) {
+  pdl_trigger();
+  pdl_wait();
+  Ctrl* ctrl = a.ctrl;
+  if (ld_volatile_u32(&ctrl->small_done)) return;
+  const u64 nE = min((u64)ld_volatile_u32(&ctrl->nE), a.cap_e);
+  const int alpha = a.alpha;
+  const u64 total = nE << alpha;
+  if (alpha < 2 || total < max((u64)DTOPK_PF_MIN_KEYS, 8 * k)) return;  // pfloor stays 0
+  __shared__ u32 sh[PF_BINS];
+  __shared__ ull scratch[8];
+  __shared__ int am_last;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < PF_BINS; i += 256) sh[i] = 0;
+  __syncthreads();
+  const u32 theta = ctrl->res.theta;
+  const u32 mx = ld_volatile_u32(&ctrl->maxkey);
+  if (mx <= theta) return;  // nothing above theta
+  const u64 range = (u64)(mx - theta);  // keys theta+1 .. mx
+  const u64 W = 1ull << alpha;
+  // E candidates: uint4 per thread and step (a uint4 never straddles a subrange)
+  for (u64 q = (u64)blockIdx.x * 256 + tid; q < total / 4; q += (u64)gridDim.x * 256) {
+    const u64 v0 = q * 4;
+    const u64 phys = ((u64)a.e_sid[v0 >> alpha] << alpha) | (v0 & (W - 1));
+    u32 x[4];
+    if (phys + 4 <= a.n) {
+      const uint4 v = ld_nc_v4(a.keys + phys);
+      x[0] = to_key<MODE>(v.x);
+      x[1] = to_key<MODE>(v.y);
+      x[2] = to_key<MODE>(v.z);
+      x[3] = to_key<MODE>(v.w);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; c++) x[c] = phys + c < a.n ? to_key<MODE>(a.keys[phys + c]) : 0u;
+    }
+    // sorted / narrow inputs put a thread's 4 keys and a warp's 128 in one bin:
+    // count runs per thread, then one atomic per warp when its bins agree
+    u32 bin = 0xffffffffu, cnt = 0;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      if (x[c] <= theta) continue;
+      const u32 bb = (u32)(((u64)(x[c] - theta - 1) * PF_BINS) / range);
+      if (bb != bin) {
+        if (cnt) atomicAdd(&sh[bin], cnt);
+        bin = bb;
+        cnt = 0;
+      }
+      cnt++;
+    }
+    const u32 act = __activemask();
+    const u32 b0 = __shfl_sync(act, bin, __ffs(act) - 1);
+    if (__all_sync(act, bin == b0)) {
+      const u32 tot = __reduce_add_sync(act, cnt);
+      if ((int)(threadIdx.x & 31) == __ffs(act) - 1 && tot && bin != 0xffffffffu) atomicAdd(&sh[bin], tot);
+    } else if (cnt) {
+      atomicAdd(&sh[bin], cnt);
+    }
+  }
+  // A records: their one key above theta (d_1)
+  const u64 nrec = ctrl->sup_total;
+  for (u64 r = (u64)blockIdx.x * 256 + tid; r < nrec; r += (u64)gridDim.x * 256) {
+    const uint4 rc = rec[r];
+    if ((rc.w & 7u) == CLS_A && rc.y > theta) atomicAdd(&sh[(u32)(((u64)(rc.y - theta - 1) * PF_BINS) / range)], 1u);
+  }
+  __syncthreads();
+  for (int i = tid; i < PF_BINS; i += 256)
+    if (sh[i]) atomicAdd(&ctrl->pf_hist[i], (ull)sh[i]);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = atomicAdd(&ctrl->pf_ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  __shared__ DigitResult res;
+  find_digit<PF_BINS>(ctrl->pf_hist, k, &res, scratch);  // the bin holding the k-th largest
+  if (tid == 0 && res.valid) {
+    const u32 lo = theta + 1u + (u32)(((u64)res.digit * range) / PF_BINS);  // <= its smallest key
+    ctrl->pfloor = lo;
+  }
 }
 
 // Ties of one subrange counted by one lane (16-byte loads, 8 in flight): the
@@ -683,7 +787,7 @@ struct K5Args {
   int exact;         // DTOPK_FLAG_EXACT_STATS: never skip (exact concatenated_len)
 };
 
-__device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64& g, u64& e) {
+__device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64& g, u64& e, u32 pf) {
   const u32 x = rc.w;
   const u32 cls = x & 7u;
   g = 0;
@@ -691,7 +795,7 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64&
   if (cls == CLS_NONE) {
     return;
   } else if (cls == CLS_A) {
-    g = 1;
+    g = rc.y >= pf;  // its one key above theta, unless below the pool floor
   } else if (cls == CLS_B) {
     e = 1;
   } else if (cls == CLS_C) {
@@ -717,14 +821,14 @@ __device__ __forceinline__ void rec_counts(const K5Args& a, const uint4 rc, u64&
 //             P_gt (index order) and in the first-k tie list
 template <bool EMIT>
 __device__ __forceinline__ void k5_tile_counts(const K5Args& a, u64 i0, u64 total, uint4 (&rcs)[K5_RPT],
-                                               u64 (&cg)[K5_RPT], u64 (&ce)[K5_RPT], u64& tg, u64& te) {
+                                               u64 (&cg)[K5_RPT], u64 (&ce)[K5_RPT], u64& tg, u64& te, u32 pf) {
   tg = te = 0;
 #pragma unroll
   for (int r = 0; r < K5_RPT; r++)
     rcs[r] = i0 + r < total ? a.rec.r[i0 + r] : make_uint4(0u, 0u, 0u, CLS_NONE);
 #pragma unroll
   for (int r = 0; r < K5_RPT; r++) {
-    rec_counts(a, rcs[r], cg[r], ce[r]);
+    rec_counts(a, rcs[r], cg[r], ce[r], pf);
     tg += cg[r];
     te += ce[r];
   }
@@ -741,11 +845,12 @@ __global__ void __launch_bounds__(256) k5_count(K5Args a) {
   Ctrl* ctrl = a.ctrl;
   const u64 total = ctrl->sup_total;
   const u64 T = max((u64)1, (total + K5_TILE - 1) / K5_TILE);
+  const u32 pf = ld_volatile_u32(&ctrl->pfloor);
   ull st_concat = 0;
   for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
     uint4 rcs[K5_RPT];
     u64 cg[K5_RPT], ce[K5_RPT], tg, te;
-    k5_tile_counts<false>(a, tile * K5_TILE + (u64)tid * K5_RPT, total, rcs, cg, ce, tg, te);
+    k5_tile_counts<false>(a, tile * K5_TILE + (u64)tid * K5_RPT, total, rcs, cg, ce, tg, te, pf);
 #pragma unroll
     for (int r = 0; r < K5_RPT; r++) {
       const u32 x = rcs[r].w, cls = x & 7u;
@@ -767,6 +872,9 @@ __global__ void __launch_bounds__(256) k5_count(K5Args a) {
     for (int w = 0; w < 8; w++) t += s_cc[w];
     if (t) atomicAdd((ull*)&ctrl->res.concatenated_len, t);
     am_last = atomicAdd(&ctrl->k5_ticket, 1u) == gridDim.x - 1;
+    // E keys above theta left out of the pool by the floor still count in |C|
+    // (every E record is fully qualified when the floor is used: beta <= 2)
+    if (am_last && ld_volatile_u32(&ctrl->pfloor)) atomicAdd((ull*)&ctrl->res.concatenated_len, ctrl->below_floor);
   }
   __syncthreads();
   if (!am_last) return;
@@ -835,13 +943,14 @@ __global__ void __launch_bounds__(256, DTOPK_K5E_MINB) k5_emit(K5Args a) {
   const u64 total = ctrl->sup_total;
   const u64 T = max((u64)1, (total + K5_TILE - 1) / K5_TILE);
   const u64 G = ctrl->res.pool_gt;
+  const u32 pf = ld_volatile_u32(&ctrl->pfloor);
   for (u64 tile = blockIdx.x; tile < T; tile += gridDim.x) {
     const u64 gx = a.tile_g[tile], ex = a.tile_e[tile];
     const u64 gnext = tile + 1 < T ? a.tile_g[tile + 1] : G;
     if (gnext == gx && ex >= a.k) continue;  // no key > theta and every tie beyond position k
     uint4 rcs[K5_RPT];
     u64 cg[K5_RPT], ce[K5_RPT], tg, te;
-    k5_tile_counts<true>(a, tile * K5_TILE + (u64)tid * K5_RPT, total, rcs, cg, ce, tg, te);
+    k5_tile_counts<true>(a, tile * K5_TILE + (u64)tid * K5_RPT, total, rcs, cg, ce, tg, te, pf);
     const u64 ig = block_incl_scan_256<u64>(tg, scratch_g);
     const u64 ie = block_incl_scan_256<u64>(te, scratch_e);
     u64 gpos = gx + ig - tg, epos = ex + ie - te;
@@ -852,7 +961,7 @@ __global__ void __launch_bounds__(256, DTOPK_K5E_MINB) k5_emit(K5Args a) {
       const u32 cls = x & 7u;
       const u64 sid = rc.x;
       const u64 base = sid << a.alpha;
-      if (cls == CLS_A) {
+      if (cls == CLS_A && cg[r]) {
         a.gt_keys[gpos] = rc.y;
         a.gt_idx[gpos] = base + meta_p1(rc.z);
       } else if (cls == CLS_B) {

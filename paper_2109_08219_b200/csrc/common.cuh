@@ -163,6 +163,11 @@ struct Ctrl {
   u32 trunc;            // pass 3: tie-only superset entries past tie_cut are dropped (enough ties before it)
   u32 tie_cut;          // last K2b segment whose tie-only entries are kept
   u32 tb_done;          // K2c last-CTA counter
+  // pool floor (K4h, large E re-reads): the exact k-th-largest bin of the pool's keys
+  u32 pfloor;           // keys below it (and above theta) stay out of P_gt; 0 = off
+  u32 pf_ticket;        // K4h last-CTA counter
+  ull below_floor;      // E keys in (theta, pfloor): counted into |C| by K5
+  alignas(16) ull pf_hist[2048];
   alignas(16) ull samp_hist[NBD1];  // K0: first-digit histogram of the sampled subranges' delegates
 };
 

@@ -438,7 +438,8 @@ __global__ void tail_decide(Ctrl* ctrl, u64 k, cudaGraphConditionalHandle c_sel,
     return;
   }
   const u64 G = ctrl->res.pool_gt;
-  ctrl->sort_lo = ctrl->res.theta;
+  // the pool's keys lie in [max(theta, pool floor), maxkey]: the bucket sort's range
+  ctrl->sort_lo = max(ctrl->res.theta, ctrl->pfloor);
   if (ctrl->res.path == PATH_MERGE) {
     ctrl->big_mode = BIG_MERGE;  // pool = P_gt ++ ties, sorted in place
     ctrl->sort_src = 0;
