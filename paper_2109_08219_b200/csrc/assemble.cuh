@@ -539,42 +539,57 @@ __global__ void __launch_bounds__(256) k4h_floor(K4Args a, const uint4* __restri
   if (mx <= theta) return;  // nothing above theta
   const u64 range = (u64)(mx - theta);  // keys theta+1 .. mx
   const u64 W = 1ull << alpha;
-  // E candidates: uint4 per thread and step (a uint4 never straddles a subrange)
-  for (u64 q = (u64)blockIdx.x * 256 + tid; q < total / 4; q += (u64)gridDim.x * 256) {
-    const u64 v0 = q * 4;
-    const u64 phys = ((u64)a.e_sid[v0 >> alpha] << alpha) | (v0 & (W - 1));
-    u32 x[4];
-    if (phys + 4 <= a.n) {
-      const uint4 v = ld_nc_v4(a.keys + phys);
-      x[0] = to_key<MODE>(v.x);
-      x[1] = to_key<MODE>(v.y);
-      x[2] = to_key<MODE>(v.z);
-      x[3] = to_key<MODE>(v.w);
-    } else {
+  // E candidates: 4 uint4 per thread and step, their subrange-id and key loads in
+  // flight together (a uint4 never straddles a subrange)
+  const u64 nq = total / 4;
+  const u64 stride = (u64)gridDim.x * 256;
+  for (u64 q0 = (u64)blockIdx.x * 256 + tid; q0 < nq; q0 += 4 * stride) {
+    u64 phys[4];
 #pragma unroll
-      for (int c = 0; c < 4; c++) x[c] = phys + c < a.n ? to_key<MODE>(a.keys[phys + c]) : 0u;
+    for (int u = 0; u < 4; u++) {
+      const u64 v0 = (q0 + u * stride) * 4;
+      phys[u] = q0 + u * stride < nq ? (((u64)a.e_sid[v0 >> alpha] << alpha) | (v0 & (W - 1))) : ~0ull;
     }
-    // sorted / narrow inputs put a thread's 4 keys and a warp's 128 in one bin:
-    // count runs per thread, then one atomic per warp when its bins agree
-    u32 bin = 0xffffffffu, cnt = 0;
+    u32 xs[4][4];
 #pragma unroll
-    for (int c = 0; c < 4; c++) {
-      if (x[c] <= theta) continue;
-      const u32 bb = (u32)(((u64)(x[c] - theta - 1) * PF_BINS) / range);
-      if (bb != bin) {
-        if (cnt) atomicAdd(&sh[bin], cnt);
-        bin = bb;
-        cnt = 0;
+    for (int u = 0; u < 4; u++) {
+      if (phys[u] != ~0ull && phys[u] + 4 <= a.n) {
+        const uint4 v = ld_nc_v4(a.keys + phys[u]);
+        xs[u][0] = to_key<MODE>(v.x);
+        xs[u][1] = to_key<MODE>(v.y);
+        xs[u][2] = to_key<MODE>(v.z);
+        xs[u][3] = to_key<MODE>(v.w);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+          xs[u][c] = phys[u] != ~0ull && phys[u] + c < a.n ? to_key<MODE>(a.keys[phys[u] + c]) : 0u;
       }
-      cnt++;
     }
-    const u32 act = __activemask();
-    const u32 b0 = __shfl_sync(act, bin, __ffs(act) - 1);
-    if (__all_sync(act, bin == b0)) {
-      const u32 tot = __reduce_add_sync(act, cnt);
-      if ((int)(threadIdx.x & 31) == __ffs(act) - 1 && tot && bin != 0xffffffffu) atomicAdd(&sh[bin], tot);
-    } else if (cnt) {
-      atomicAdd(&sh[bin], cnt);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      // sorted / narrow inputs put a thread's 4 keys and a warp's 128 in one bin:
+      // count runs per thread, then one atomic per warp when its bins agree
+      u32 bin = 0xffffffffu, cnt = 0;
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        const u32 x = xs[u][c];
+        if (x <= theta) continue;
+        const u32 bb = (u32)(((u64)(x - theta - 1) * PF_BINS) / range);
+        if (bb != bin) {
+          if (cnt) atomicAdd(&sh[bin], cnt);
+          bin = bb;
+          cnt = 0;
+        }
+        cnt++;
+      }
+      const u32 act = __activemask();
+      const u32 b0 = __shfl_sync(act, bin, __ffs(act) - 1);
+      if (__all_sync(act, bin == b0)) {
+        const u32 tot = __reduce_add_sync(act, cnt);
+        if ((int)(threadIdx.x & 31) == __ffs(act) - 1 && tot && bin != 0xffffffffu) atomicAdd(&sh[bin], tot);
+      } else if (cnt) {
+        atomicAdd(&sh[bin], cnt);
+      }
     }
   }
   // A records: their one key above theta (d_1)
