@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(256, BIG ? 3 : 2) k4_read(K4Args a) {
 // chunks already hold k ties -- every later tie lands beyond position k, so
 // its count is never needed (it stays 0; concatenated_len is then a lower
 // bound, flagged through concat_skipped_fq).
-constexpr u32 K4T_PARALLEL_MAX = 4096;
+constexpr u32 K4T_PARALLEL_MAX = 65536;  // T candidates counted all at once (truncated tie-heavy calls stay below: <= ~k / 2)
 constexpr u32 K4T_CHUNKS_PER_TICKET = 8;  // 32-record chunks (one per warp) per ticket
 
 template <int MODE>
