@@ -405,7 +405,10 @@ void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, i
   launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2,
              k2.sup_cnt, k2.sup_off, k2.D, L.D_len);
   counted();
-  if (trunc_ok && beta <= 2) {
+#ifndef DTOPK_NOOPT_EXP
+#define DTOPK_NOOPT_EXP 0  // experiment: 1 = leave out the call-dependent optional kernels (K2c, K4h, big K4)
+#endif
+  if (trunc_ok && beta <= 2 && !DTOPK_NOOPT_EXP) {
     launch_pdl(k2c_tie_bounds, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.D, L.D_len, L.R2, L.g2, beta,
                k, reinterpret_cast<uint2*>(ws + L.tseg));
     counted();
@@ -690,13 +693,13 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   K4Args k4{keys, n, alpha, ctrl, e_sid, reinterpret_cast<u32*>(ws + L.stg_key),
             reinterpret_cast<u64*>(ws + L.stg_idx), reinterpret_cast<u32*>(ws + L.seg_gt),
             reinterpret_cast<u32*>(ws + L.seg_eq), L.cap_e};
-  if (beta <= 2 && (L.cap_e << alpha) >= DTOPK_PF_MIN_KEYS) {  // pool floor (every E record is then fully qualified)
+  if (beta <= 2 && (L.cap_e << alpha) >= DTOPK_PF_MIN_KEYS && !DTOPK_NOOPT_EXP) {  // pool floor (every E record is then fully qualified)
     launch_pdl(k4h_floor<MODE>, dim3(nsm * 4), dim3(256), 0, s, k4, static_cast<const uint4*>(rc.r), k);
     counted();
   }
   launch_pdl(k4_read<MODE, 0>, dim3(grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 4)), dim3(256), 0, s,
              k4);
-  if (L.cap_e << alpha >= DTOPK_K4_BIG_KEYS) {
+  if (L.cap_e << alpha >= DTOPK_K4_BIG_KEYS && !DTOPK_NOOPT_EXP) {
     launch_pdl(k4_read<MODE, 1>, dim3(grid_for(std::max<u64>(L.k4_tiles, (L.cap_e + 255) / 256), nsm * 3)), dim3(256),
                0, s, k4);
     counted();

@@ -124,3 +124,26 @@ def test_sharded_begin_uses_filter(oracle_mod, cuda):
     ek, ei = oracle_mod.topk_with_indices(v.cpu().numpy(), k)
     np.testing.assert_array_equal(p.indices.cpu().numpy(), ei)
     assert int(p.header().filtered) == 1
+
+
+# ---------------------------------------------------------------- pool floor (K4h)
+@pytest.mark.parametrize("case,k,largest", [
+    ("ascending", 1 << 14, True),        # 4 M keys above theta, floor keeps ~k
+    ("ascending_dups", 1 << 14, True),   # every key 4 times: ties straddle the floor's bin
+    ("descending", 1 << 14, False),      # smallest of a descending vector: the same shape mirrored
+    ("ascending_f32", 8192, True),
+])
+def test_pool_floor(case, k, largest, oracle_mod, cuda):
+    """Calls that re-read >= 2M keys above theta take the pool floor: values,
+    indices and the reference counters (|C| included) stay exact, and the pool
+    shrinks to about k."""
+    n = 1 << 24
+    if case == "ascending_f32":
+        v = torch.arange(n, device=cuda, dtype=torch.float32) - n / 2
+    elif case == "ascending_dups":
+        v = (torch.arange(n, device=cuda, dtype=torch.int64) // 4).to(torch.int32).view(torch.uint32)
+    else:
+        v = data.generate(case, n, seed=0, device=cuda)
+    alpha = 10 if case == "ascending_f32" else 9
+    r = check_topk(v, k, oracle_mod, largest=largest, alpha=alpha, auto_alpha=False)
+    assert int(r.stats.device["pool_gt"]) < 4 * k  # the floor cut the pool (millions of keys above theta)
