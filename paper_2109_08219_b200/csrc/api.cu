@@ -265,12 +265,12 @@ void launch_k1(const K1Args& a, cudaStream_t s, int nsm, u64 nch, int merge = 1)
   if (a.c_end > a.c_begin) {
     // the full-range launch keeps the grid the record streams were sized for (k1_grid)
     k1_delegates<MODE, B><<<grid_for(a.c_begin == 0 && a.c_end == nch ? nch : a.c_end - a.c_begin, nsm * K1_CPS),
-                            K1_THREADS, K1_SMEM, s>>>(a);
+                            k1_threads<B>(), K1_SMEM, s>>>(a);
     counted();
   }
   if (merge && a.alpha > K1_LOG_CHUNK) {
     k1_merge<B><<<grid_for((a.S + 255) / 256, nsm * 4), 256, 0, s>>>(a.partial, a.pmeta, nch, a.alpha, a.S, a.D,
-                                                                       a.meta, a.hist1);
+                                                                       a.meta, a.hist1, a.lin);
     counted();
   }
 }
@@ -298,7 +298,8 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
            reinterpret_cast<u32*>(ws + L.chunk_cnt),
            L.fcap,
            k1 ? c0 : 0,
-           k1 ? std::min<u64>(c1, L.nch) : 0};
+           k1 ? std::min<u64>(c1, L.nch) : 0,
+           MODE >= 2 ? 1 : 0};
   switch (beta) {
     case 1: launch_k1<MODE, 1>(a, s, nsm, L.nch, merge); break;
     case 2: launch_k1<MODE, 2>(a, s, nsm, L.nch, merge); break;
@@ -320,7 +321,7 @@ void stage_delegates(const u32* keys, u64 n, int alpha, int beta, u32* D, char* 
   }
 }
 
-K2Args k2_args(char* ws, const Layout& L, u64 k, int beta, int alpha = 0, int fmode = 0,
+K2Args k2_args(char* ws, const Layout& L, u64 k, int beta, int lin, int alpha = 0, int fmode = 0,
                cudaGraphConditionalHandle fb = {}, int fb_graph = 0) {
   return K2Args{reinterpret_cast<u32*>(ws + L.D),
                 L.D_len,
@@ -344,7 +345,8 @@ K2Args k2_args(char* ws, const Layout& L, u64 k, int beta, int alpha = 0, int fm
                 L.nch,
                 alpha,
                 fb,
-                fb_graph};
+                fb_graph,
+                lin};
 }
 
 // Graph capture context: when `graph` is set, run_finish ends the main
@@ -400,10 +402,11 @@ bool cond_end(cudaStream_t inner) {
 
 // K2 pass 3 (theta from the bucket members) and K2b (the exact superset of a
 // large-bucket call).
-void theta_resolve(char* ws, const Layout& L, u64 k, int beta, cudaStream_t s, int nsm, bool trunc_ok = false) {
-  const K2Args k2 = k2_args(ws, L, k, beta);
+void theta_resolve(char* ws, const Layout& L, u64 k, int beta, int lin, cudaStream_t s, int nsm,
+                   bool trunc_ok = false) {
+  const K2Args k2 = k2_args(ws, L, k, beta, lin);
   launch_pdl(k2_pass3, dim3(grid_for(L.g2, nsm)), dim3(256), 0, s, k2.ctrl, k2.selbuf, k2.region_cnt, L.g2, L.R2,
-             k2.sup_cnt, k2.sup_off, k2.D, L.D_len);
+             k2.sup_cnt, k2.sup_off, k2.D, L.D_len, lin);
   counted();
 #ifndef DTOPK_NOOPT_EXP
 #define DTOPK_NOOPT_EXP 0  // experiment: 1 = leave out the call-dependent optional kernels (K2c, K4h, big K4)
@@ -433,13 +436,13 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
     rec(ev, 0, s);
     if (alpha > K1_LOG_CHUNK) stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, s, nsm, 0, 0, 0, 1, 0);
     rec(ev, 1, s);
-    const K2Args k2 = k2_args(ws, L, k, beta, alpha, 0);
+    const K2Args k2 = k2_args(ws, L, k, beta, MODE >= 2, alpha, 0);
     if (beta == 2)
       launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
     else
       launch_pdl(k2_scan_delegates<0>, dim3(L.g2), dim3(256), 0, s, k2);
     counted();
-    if (!fused) theta_resolve(ws, L, k, beta, s, nsm);
+    if (!fused) theta_resolve(ws, L, k, beta, MODE >= 2, s, nsm);
     rec(ev, 2, s);
     return;
   }
@@ -461,7 +464,8 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
   rec(ev, 1, s);
   DTOPK_RANGE("FirstK");
   const bool g = gc != nullptr && filt;
-  const K2Args k2 = k2_args(ws, L, k, beta, alpha, filt ? 1 : 0, g ? gc->fb : cudaGraphConditionalHandle{}, g ? 1 : 0);
+  const K2Args k2 =
+      k2_args(ws, L, k, beta, MODE >= 2, alpha, filt ? 1 : 0, g ? gc->fb : cudaGraphConditionalHandle{}, g ? 1 : 0);
   if (beta == 2)
     launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, s, k2);
   else
@@ -477,7 +481,7 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
       fs = gc->s6;
     }
     stage_delegates<MODE>(keys, n, alpha, beta, D, ws, L, fs, nsm, 2);
-    const K2Args k2f = k2_args(ws, L, k, beta, alpha, 2);
+    const K2Args k2f = k2_args(ws, L, k, beta, MODE >= 2, alpha, 2);
     if (beta == 2)
       launch_pdl(k2_scan_delegates<1>, dim3(L.g2), dim3(256), 0, fs, k2f);
     else
@@ -485,7 +489,7 @@ void run_begin(const u32* keys, u64 n, u64 k, int alpha, int beta, char* ws, con
     counted();
     if (g) gc->ok = gc->ok && cond_end(gc->s6);
   }
-  if (!fused) theta_resolve(ws, L, k, beta, s, nsm);
+  if (!fused) theta_resolve(ws, L, k, beta, MODE >= 2, s, nsm);
   rec(ev, 2, s);
 }
 
@@ -663,7 +667,7 @@ void run_finish(const u32* keys, u64 n, u64 k, int alpha, int beta, u32 flags, c
   // fused call: theta was left to fast_tail; the general chain resolves it itself.
   // No external theta here, so a tie-heavy call may drop tie-only superset
   // entries past the first k ties (not with exact stats: |C| counts every one)
-  if (fused) theta_resolve(ws, L, k, beta, s, nsm, (flags & DTOPK_FLAG_EXACT_STATS) == 0);
+  if (fused) theta_resolve(ws, L, k, beta, MODE >= 2, s, nsm, (flags & DTOPK_FLAG_EXACT_STATS) == 0);
   nvtxRangePushA("Concat");
   Records rc{reinterpret_cast<uint4*>(ws + L.rec)};
   u32* e_sid = reinterpret_cast<u32*>(ws + L.e_sid);

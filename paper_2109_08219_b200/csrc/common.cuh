@@ -63,38 +63,57 @@ __device__ __forceinline__ u32 dig3(u32 k) { return k & 0x3ffu; }
 // they crowd the top of the key range: a linear top-11-bit bucket can hold
 // most of D (the max of 2048 uniform keys lands in the top 1/2048 of the
 // range with probability 0.63).  The first digit is therefore log-scale in
-// the distance from the top, d = ~key: (leading zeros of d, next 6 bits of
-// d), 33 x 64 buckets ordered like the keys.  A bucket is a key interval
-// [kmin, kmin + 2^r) with r <= 25; digit 2 = (key - kmin) >> 13 (12 bits),
-// digit 3 = (key - kmin) & 8191.
-constexpr int NBD1 = 2560;  // 2112 used, padded to 256 x an even count (find_digit reads bin pairs)
+// the distance from the top, d = ~key: (leading zeros of d, next DSB bits of
+// d), 33 x 2^DSB buckets ordered like the keys.  A bucket is a key interval
+// [kmin, kmin + 2^r) with r <= 31 - DSB; digit 2 = (key - kmin) >> 13,
+// digit 3 = (key - kmin) & 8191.  DSB = 7 (was 6): float32 keys put a whole
+// octave of values in one (clz, 6-bit) bucket, so theta's bucket outgrew the
+// one-CTA tail on N(0,1) data; 7 bits halve every bucket.
+constexpr int DSB = 7;                                  // sub-bits of the first digit
+constexpr u32 DSB_MASK = (1u << DSB) - 1u;
+// float32 keys are already logarithmic (sign, exponent, mantissa), and their
+// maxima crowd near the data's maximum, not near 0xffffffff: for them the first
+// digit is linear, the top 13 key bits (16 buckets per octave).  N(0,1) data at
+// k = 1024: theta's bucket 33,862 delegates with the log digit, ~3 k linear.
+constexpr int DLIN_SHIFT = 19;
+constexpr int NBD1 = 8192;  // max(33 x 128 log buckets, 2^13 linear), a multiple of 512 (find_digit reads bin pairs)
 constexpr int NBD2 = 4096, NBD3 = 8192;
-constexpr int DSH3 = 13;  // digit 2 = (key - kmin) >> 13 (12 bits), digit 3 = low 13 bits
+constexpr int DSH3 = 13;  // digit 2 = (key - kmin) >> 13 (<= 11 bits), digit 3 = low 13 bits
 __device__ __forceinline__ u32 ddig1(u32 key) {
   const u32 d = ~key;
-  if (d == 0) return (32u << 6) | 63u;
+  if (d == 0) return (32u << DSB) | DSB_MASK;
   const u32 c = __clz(d);
-  const u32 m = c >= 31 ? 0u : (d << (c + 1)) >> 26;
-  return (c << 6) | (63u - m);
+  const u32 m = c >= 31 ? 0u : (d << (c + 1)) >> (32 - DSB);
+  return (c << DSB) | (DSB_MASK - m);
 }
 // key interval [kmin, kmax] of log bucket b
 __device__ __forceinline__ void dbucket_range(u32 b, u32& kmin, u32& kmax) {
-  const u32 c = b >> 6, m = 63u - (b & 63u);
+  const u32 c = b >> DSB, m = DSB_MASK - (b & DSB_MASK);
   if (c >= 32) {
     kmin = kmax = 0xffffffffu;
     return;
   }
   const u32 lead = 1u << (31 - c);
   u32 dlo, dhi;
-  if (c <= 25) {
-    const u32 r = 25 - c;
+  if (c <= 31 - DSB) {
+    const u32 r = 31 - DSB - c;
     dlo = lead | (m << r);
     dhi = dlo | ((1u << r) - 1u);
   } else {
-    dlo = dhi = lead | (m >> (c - 25));
+    dlo = dhi = lead | (m >> (c - (31 - DSB)));
   }
   kmin = ~dhi;
   kmax = ~dlo;
+}
+
+__device__ __forceinline__ u32 ddig(u32 key, bool lin) { return lin ? (key >> DLIN_SHIFT) : ddig1(key); }
+__device__ __forceinline__ void dbucket(u32 b, bool lin, u32& kmin, u32& kmax) {
+  if (lin) {
+    kmin = b << DLIN_SHIFT;
+    kmax = kmin | ((1u << DLIN_SHIFT) - 1u);
+  } else {
+    dbucket_range(b, kmin, kmax);
+  }
 }
 
 // ---------------------------------------------------------------------------

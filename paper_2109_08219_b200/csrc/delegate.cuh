@@ -49,6 +49,12 @@ constexpr int K1_PREFETCH = DTOPK_K1_PREFETCH;  // chunks prefetched into L2 ahe
 // few log-scale bins, so same-address atomics serialise inside a warp
 constexpr int K1_HCOPIES = DTOPK_K1_HCOPIES;
 constexpr int K1_THREADS = (K1_CWARPS + 1) * 32;
+// beta >= 3 ladders are compute-bound at 8 consumer warps (f32 beta 3: 0.86 ms vs
+// 0.74 at beta 2); 16 warps (one per ring stage) restore the stream: 0.78 ms
+template <int B>
+constexpr int k1_cwarps() { return B >= 3 ? 16 : K1_CWARPS; }
+template <int B>
+constexpr int k1_threads() { return (k1_cwarps<B>() + 1) * 32; }
 constexpr size_t K1_SMEM = (size_t)K1_STAGES * K1_CHUNK * 4 + 2 * K1_STAGES * 8 + (size_t)NBD1 * 4 * K1_HCOPIES;
 
 struct K1Args {
@@ -71,6 +77,7 @@ struct K1Args {
   u32* chunk_cnt;  // [nchunks] (offset of chunk c's records in its warp's stream << 6) | count
   u64 fcap;        // records per warp stream: ceil(nchunks / (grid * 8)) * (2048 >> alpha)
   u64 c_begin, c_end;  // chunks this launch reduces (a streamed host input arrives range by range)
+  int lin;             // first digit: linear (float32 keys) or log-scale (uint32)
 };
 
 // Per-lane accumulator: top-B ladder, uint4 index p of the running maximum
@@ -235,13 +242,13 @@ __device__ __forceinline__ void emit_subrange(const K1Args& a, u32* shist, u64 s
     if (one_writer) {  // a single emitting lane: no aggregation needed
       if (w) {
 #pragma unroll
-        for (int i = 0; i < B; i++) atomicAdd(&shist[ddig1(L[i])], 1u);
+        for (int i = 0; i < B; i++) atomicAdd(&shist[ddig(L[i], a.lin)], 1u);
       }
     } else {
 #pragma unroll
       for (int i = 0; i < B; i++) {
         // plain shared atomics: measured faster than match_any aggregation, also on all-equal input
-        if (w) atomicAdd(&shist[ddig1(L[i])], 1u);
+        if (w) atomicAdd(&shist[ddig(L[i], a.lin)], 1u);
       }
     }
   }
@@ -270,7 +277,7 @@ __device__ __forceinline__ void emit_filtered(const K1Args& a, u32* shist, u64 c
     if constexpr (K1_HCOPIES > 1) shist += (threadIdx.x & (K1_HCOPIES - 1)) * NBD1;
 #pragma unroll
     for (int i = 0; i < B; i++)
-      if (w) atomicAdd(&shist[ddig1(L[i])], 1u);
+      if (w) atomicAdd(&shist[ddig(L[i], a.lin)], 1u);
   }
 }
 
@@ -476,7 +483,9 @@ __device__ __forceinline__ u64 k1_chunk_of(u64 i, u64 c0, u64 c1) {
 }
 
 template <int MODE, int B>
-__global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
+__global__ void __launch_bounds__(k1_threads<B>(), K1_CPS) k1_delegates(K1Args a) {
+  constexpr int CW = k1_cwarps<B>();
+  static_assert(K1_STAGES % CW == 0, "each consumer warp owns whole ring stages");
   pdl_trigger();
   if (a.fmode == 2 && !ld_volatile_u32(&a.ctrl->filt_fail)) return;  // fallback pass not needed
 #ifdef DTOPK_K1_FORCE_FT  // profiling only (tools/k1_alpha.py): filtered emission with a fixed floor
@@ -494,7 +503,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
 
   const u64 nch = (a.n + K1_CHUNK - 1) >> K1_LOG_CHUNK;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < NBD1 * K1_HCOPIES; i += K1_THREADS) shist[i] = 0;
+  for (int i = tid; i < NBD1 * K1_HCOPIES; i += k1_threads<B>()) shist[i] = 0;
   if (tid == 0) {
     for (int s = 0; s < K1_STAGES; s++) {
       mbar_init(&full[s], 1);
@@ -506,7 +515,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
 
   // Iteration i of this CTA handles chunk blockIdx.x + i*gridDim.x in stage
   // i % 16, consumed by warp i % 8; the stage's parity flips every 16 iterations.
-  if (warp == K1_CWARPS) {
+  if (warp == CW) {
     if (lane == 0) {
       u64 i = 0;
       const u64 pol = l2_policy_evict_first();
@@ -535,7 +544,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   } else {
     u64 i = warp;
     u32 wrun = 0;  // records in this warp's stream (filtered mode)
-    for (u64 c = k1_chunk_of(i, a.c_begin, a.c_end); c != ~0ull; i += K1_CWARPS, c = k1_chunk_of(i, a.c_begin, a.c_end)) {
+    for (u64 c = k1_chunk_of(i, a.c_begin, a.c_end); c != ~0ull; i += CW, c = k1_chunk_of(i, a.c_begin, a.c_end)) {
       const u32 s = (u32)(i % K1_STAGES);
       const u32 ph = (u32)(i / K1_STAGES) & 1u;
       mbar_wait(&full[s], ph);
@@ -558,7 +567,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1_CPS) k1_delegates(K1Args a) {
   }
   __syncthreads();
   if (a.do_hist) {
-    for (int i = tid; i < NBD1; i += K1_THREADS) {
+    for (int i = tid; i < NBD1; i += k1_threads<B>()) {
       u32 v = 0;
 #pragma unroll
       for (int h = 0; h < K1_HCOPIES; h++) v += shist[h * NBD1 + i];
@@ -639,11 +648,11 @@ __global__ void __launch_bounds__(256) k0_sample(const u32* __restrict__ keys, i
         if (per == 1) k0_merge<B>(b0, b1, __shfl_xor_sync(FULL, b0, o), __shfl_xor_sync(FULL, b1, o));
       }
       if ((lane & (G - 1)) == 0) {
-        atomicAdd(&sh[ddig1(a0)], 1u);
-        if (B >= 2) atomicAdd(&sh[ddig1(a1)], 1u);
+        atomicAdd(&sh[ddig(a0, MODE >= 2)], 1u);
+        if (B >= 2) atomicAdd(&sh[ddig(a1, MODE >= 2)], 1u);
         if (per == 1) {
-          atomicAdd(&sh[ddig1(b0)], 1u);
-          if (B >= 2) atomicAdd(&sh[ddig1(b1)], 1u);
+          atomicAdd(&sh[ddig(b0, MODE >= 2)], 1u);
+          if (B >= 2) atomicAdd(&sh[ddig(b1, MODE >= 2)], 1u);
         }
       }
     }
@@ -665,7 +674,7 @@ __global__ void __launch_bounds__(256) k0_sample(const u32* __restrict__ keys, i
   if (tid == 0) {
     const bool on = ns > 0 && rs <= ns && res.valid && (res.above + res.cnt) * 4 <= ns;
     u32 kmin, kmax;
-    dbucket_range(res.digit, kmin, kmax);
+    dbucket(res.digit, MODE >= 2, kmin, kmax);
     ctrl->filt_t = kmin;
     ctrl->filt_on = on ? 1u : 0u;
     ctrl->res.filtered = on ? 1u : 0u;
@@ -676,7 +685,7 @@ __global__ void __launch_bounds__(256) k0_sample(const u32* __restrict__ keys, i
 template <int B>
 __global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial, const u32* __restrict__ pmeta,
                                                 u64 nch, int alpha, u64 S, u32* __restrict__ D,
-                                                u32* __restrict__ meta, ull* __restrict__ hist1) {
+                                                u32* __restrict__ meta, ull* __restrict__ hist1, int lin) {
   pdl_trigger();
   __shared__ u32 shist[NBD1];
   for (int i = threadIdx.x; i < NBD1; i += 256) shist[i] = 0;
@@ -702,7 +711,7 @@ __global__ void __launch_bounds__(256) k1_merge(const u32* __restrict__ partial,
 #pragma unroll
     for (int i = 0; i < B; i++) L[i] = A.L[i];
 #pragma unroll
-    for (int i = 0; i < B; i++) hist_add_agg(shist, ddig1(L[i]), s < S);
+    for (int i = 0; i < B; i++) hist_add_agg(shist, ddig(L[i], lin), s < S);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NBD1; i += 256) {
@@ -747,7 +756,7 @@ __global__ void __launch_bounds__(256) k1_generic(const u32* __restrict__ keys, 
       if (r == 0) d1 = m;
       if (lane == 0) {
         D[s * beta + r] = m;
-        atomicAdd(&hist1[ddig1(m)], 1ull);
+        atomicAdd(&hist1[ddig(m, MODE >= 2)], 1ull);
       }
     }
     // position of the first max and constant-subrange flag: second pass (cold path)

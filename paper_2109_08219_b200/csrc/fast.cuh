@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) fast_tail(FTArgs a) {
       return;
     }
     u32 kmin, kmax;
-    dbucket_range(r1.digit, kmin, kmax);
+    dbucket(r1.digit, MODE >= 2, kmin, kmax);
     ft_find_digit<NBD2 / FT_THREADS>(h2, NBD2, r1.rem, &s_r2, scratch);
     const u32 b2 = s_r2.digit;
     // region prefix (aliases the pool keys, unused until phase D), digit-3 histogram

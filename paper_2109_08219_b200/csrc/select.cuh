@@ -54,6 +54,7 @@ struct K2Args {
   int alpha;
   cudaGraphConditionalHandle fb;  // graph: set when the fallback must run
   int fb_graph;
+  int lin;  // first digit family (float32: linear)
 };
 
 #ifndef DTOPK_K2_MINB
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
   find_digit<NBD1>(a.ctrl->selD.hist1, a.k, &r1, scratch);
   if (blockIdx.x == 0 && tid == 0) a.ctrl->selD.r1 = r1;
   u32 kmin, kmax;
-  dbucket_range(r1.digit, kmin, kmax);
+  dbucket(r1.digit, a.lin != 0, kmin, kmax);
   const u32 span = kmax - kmin;
   if (records && (ld_volatile_u32(&a.ctrl->filt_t) > kmin || r1.cnt * 4 > a.nD)) {
     // the sampled floor missed theta's bucket (or the bucket is a large share of
@@ -496,7 +497,7 @@ __device__ __forceinline__ void p3_set_theta(Ctrl* ctrl, u32 kth, const DigitRes
 __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
                                                 const u32* __restrict__ region_cnt, u32 nregions, u64 R,
                                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off,
-                                                const u32* __restrict__ D, u64 nD) {
+                                                const u32* __restrict__ D, u64 nD, int lin) {
   pdl_trigger();
   pdl_wait();
   __shared__ u32 shist[NBD3];
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   if (small && blockIdx.x != 0) return;
   for (int i = tid; i < NBD3; i += 256) shist[i] = 0;
   u32 kmin, kmax;
-  dbucket_range(r1.digit, kmin, kmax);
+  dbucket(r1.digit, lin != 0, kmin, kmax);
   find_digit<NBD2>(ctrl->selD.hist2, r1.rem, &r2, scratch);
   if (blockIdx.x == 0 && tid == 0) ctrl->selD.r2 = r2;
   const u32 b2 = r2.digit;

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(K1B_THREADS) k1_bigbeta(const u32* __restrict_
       if (r < (u32)beta) {
         const u32 key = ~k[j];
         D[s * beta + r] = key;
-        atomicAdd(&hist1[ddig1(key)], 1ull);
+        atomicAdd(&hist1[ddig(key, MODE >= 2)], 1ull);
         if (r == 0) s_first = p[j];
       }
     }

@@ -17,8 +17,9 @@ for d in ascending all_equal few_distinct; do
     python tools/prof_case.py --dist $d --k 65536 --reps 3 > /dev/null 2>&1
 done
 python tools/ncu_launches.py $O/launches_*.csv > $O/launches_summary.txt
-for k in 1024 1048576; do
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:k1_delegates -s 2 -c 1 -o $O/k1_k$k \
+for ks in 1024:1 1048576:2; do  # skip the first call's K1 (and, at 2^20, its flag-gated fallback launch)
+  k=${ks%:*}; sk=${ks#*:}
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:k1_delegates -s $sk -c 1 -o $O/k1_k$k \
     python tools/prof_case.py --k $k --reps 2 > /dev/null 2>&1
   ncu -i $O/k1_k$k.ncu-rep --page raw --csv > $O/k1_k${k}_raw.csv 2>/dev/null
   rm -f $O/k1_k$k.ncu-rep
