@@ -153,3 +153,69 @@ def test_select_merge_gloo(world, seed, k, oracle_mod):
         vals, idx = out[r]
         np.testing.assert_array_equal(idx, ei)
         np.testing.assert_array_equal(vals, ek)
+
+
+class FailingOps(OracleOps):
+    """Rank 1 fails in begin (e.g. an out-of-memory or a bad shard)."""
+
+    def begin(self, shard, cfg):
+        if dist.get_rank() == 1:
+            raise RuntimeError("injected failure")
+        return super().begin(shard, cfg)
+
+
+def _edge_worker(rank, world, port, n, k, fail, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from oracle import oracle
+
+        import paper_2109_08219_b200 as dtopk
+
+        v = oracle.generate_uniform(n, seed=11)
+        lo, ln = dtopk.shard_bounds(n, world, rank)
+        shard = torch.from_numpy(v[lo:lo + ln].copy())
+        ops = FailingOps(oracle) if fail else OracleOps(oracle)
+        try:
+            r = dtopk.sharded_topk(shard, n, k, ops=ops)
+            out[rank] = ("ok", r.values.numpy().astype(np.uint32), r.indices.numpy())
+        except Exception as exc:  # noqa: BLE001 -- the test inspects the type
+            out[rank] = (type(exc).__name__, None, None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,k", [
+    (2, 1, 1),                 # rank 1's shard is empty
+    (3, 3 * 1000 + 1, 1500),   # ragged last shard, k above every shard's length
+    (3, 2, 2),                 # an empty shard and one-key shards (direct path)
+    (2, 20_001, 9_000),        # k close to a shard's length
+])
+def test_sharded_topk_ragged_and_empty_shards(world, n, k, oracle_mod):
+    """Every rank joins every collective whatever its shard (ragged
+    last shards and empty shards must not desynchronise the collectives)."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_edge_worker, args=(world, _free_port(), n, k, False, out), nprocs=world, join=True,
+                       start_method="spawn")
+    v = oracle_mod.generate_uniform(n, seed=11)
+    ek, ei = oracle_mod.topk_with_indices(v, k)
+    for r in range(world):
+        status, vals, idx = out[r]
+        assert status == "ok"
+        np.testing.assert_array_equal(idx, ei)
+        np.testing.assert_array_equal(vals, ek)
+
+
+def test_sharded_topk_failure_reaches_every_rank(oracle_mod):
+    """A rank that fails in begin raises WorkerFailed on every rank instead of
+    leaving its peers blocked in the theta all-reduce (distributed.py:238-241)."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_edge_worker, args=(2, _free_port(), 50_000, 100, True, out), nprocs=2, join=True,
+                       start_method="spawn")
+    assert out[0][0] == "WorkerFailed" and out[1][0] == "WorkerFailed"

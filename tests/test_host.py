@@ -261,3 +261,25 @@ def test_cli_parser_and_counts():
     assert a.max_resident == str(1 << 26)
     with pytest.raises(SystemExit):
         p.parse_args(["run", "--k", "1", "--backend", "heap"])
+
+
+def test_host_view_coercion():
+    """Host inputs of dr_topk's streamed path: the reference's
+    np.asarray(v, dtype=uint32) coercion, float32 kept, CUDA tensors excluded."""
+    import numpy as np
+    import torch
+
+    from paper_2109_08219_b200 import _device, _native
+    from paper_2109_08219_b200.core import EmptyInput
+
+    hv = _device.host_view([3, 1, 2])
+    assert hv.code == _native.DTYPE_U32 and hv.kind == "numpy" and hv.host.tolist() == [3, 1, 2]
+    hv = _device.host_view(np.array([-1, 5], dtype=np.int64))
+    assert hv.host.view(torch.int32).tolist() == [-1, 5]  # wrapped to uint32 bits like np.asarray(.., uint32)
+    hv = _device.host_view(np.arange(4, dtype=np.float32))
+    assert hv.code == _native.DTYPE_F32 and hv.host.dtype == torch.float32
+    hv = _device.host_view(torch.arange(5, dtype=torch.int32))
+    assert hv.kind == "torch_cpu" and hv.out_dtype == torch.int32 and hv.n == 5
+    with pytest.raises(EmptyInput):
+        _device.host_view(np.array([], dtype=np.uint32))
+    assert _device.STREAM_RANGE % 2048 == 0  # ranges are whole K1 chunks
