@@ -1022,6 +1022,24 @@ __global__ void __launch_bounds__(256) k5b_copy(Ctrl* ctrl, int alpha, u64 k, co
   const int lseg = alpha < 13 ? alpha : 13;
   const u64 seglen = 1ull << lseg;
   const u64 ppc = (1ull << alpha) >> lseg;
+  if (alpha <= 8) {
+    // small subranges (<= 256 keys, a few staged keys each at large k): one E
+    // candidate per thread, so the count / offset loads of 32 candidates are in
+    // flight per warp instead of one (k = 2^20: 31 k candidates, ~2 keys each)
+    for (u64 e = (u64)blockIdx.x * 256 + threadIdx.x; e < nE; e += (u64)gridDim.x * 256) {
+      const u64 eo = e_epos[e];
+      if (eo == ~0ull) continue;
+      const u64 go = e_gpos[e];
+      const u32 ng = seg_gt[e], ne = seg_eq[e];
+      const u64 sb = e << lseg;
+      for (u32 z = 0; z < ng; z++) {
+        gt_keys[go + z] = stg_key[sb + z];
+        gt_idx[go + z] = stg_idx[sb + z];
+      }
+      for (u32 z = 0; z < ne && eo + z < k; z++) ties[eo + z] = stg_idx[sb + seglen - 1 - z];
+    }
+    return;
+  }
   const u64 gw = ((u64)blockIdx.x * 256 + threadIdx.x) >> 5;
   const u64 nw = ((u64)gridDim.x * 256) >> 5;
   for (u64 sg = gw; sg < nE * ppc; sg += nw) {
