@@ -447,7 +447,7 @@ def run_ours(args):
         for _ in range(3):
             plan.launch(v, s_a)
             plan_b.launch(v, s_b)
-        torch.cuda.synchronize()
+        cool()
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         p0.record(stream)
         s_a.wait_stream(stream)
@@ -469,7 +469,7 @@ def run_ours(args):
     if world == 1:
         for _ in range(2):
             plan.launch(v, stream, events=ev_arrays[0])
-        torch.cuda.synchronize()
+        cool()
         b0 = torch.cuda.Event(enable_timing=True)
         b1 = torch.cuda.Event(enable_timing=True)
         b0.record(stream)
