@@ -1022,10 +1022,12 @@ __global__ void __launch_bounds__(256) k5b_copy(Ctrl* ctrl, int alpha, u64 k, co
   const int lseg = alpha < 13 ? alpha : 13;
   const u64 seglen = 1ull << lseg;
   const u64 ppc = (1ull << alpha) >> lseg;
-  if (alpha <= 8) {
-    // small subranges (<= 256 keys, a few staged keys each at large k): one E
+  if (alpha <= 6) {
+    // small subranges (<= 64 keys, a few staged keys each at large k): one E
     // candidate per thread, so the count / offset loads of 32 candidates are in
-    // flight per warp instead of one (k = 2^20: 31 k candidates, ~2 keys each)
+    // flight per warp instead of one (k = 2^20: 31 k candidates, ~2 keys each).
+    // Not for larger subranges: a candidate can stage all of its keys (ascending
+    // input at alpha 8: 256 per candidate, 1.09 vs 0.90 ms copied one by one)
     for (u64 e = (u64)blockIdx.x * 256 + threadIdx.x; e < nE; e += (u64)gridDim.x * 256) {
       const u64 eo = e_epos[e];
       if (eo == ~0ull) continue;
