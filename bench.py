@@ -529,7 +529,8 @@ def run_ours(args):
     # ---- k sweep (config 2), 1 GPU only
     if world == 1 and not args.no_sweep and rank == 0:
         sweep = []
-        for e in range(0, 21, args.sweep_stride):
+        exps = [int(x) for x in args.sweep_exps.split(",")] if args.sweep_exps else range(0, 21, args.sweep_stride)
+        for e in exps:
             kk = 1 << e
             p = DrTopK(n, dtopk.PipelineConfig(k=kk), _native.DTYPE_U32, torch.uint32, dev, timed=False,
                        use_graph=not args.no_graph)
@@ -662,6 +663,7 @@ def main():
     ap.add_argument("--log2n", type=int, default=30)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--sweep-stride", type=int, default=1)
+    ap.add_argument("--sweep-exps", default="", help="comma-separated log2(k) list for the sweep (A/B runs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE config 3-5 extra field")

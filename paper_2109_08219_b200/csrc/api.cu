@@ -72,9 +72,16 @@ struct Layout {
   u32 g2;
 };
 
-// fast_tail holds <= FT_CAND qualifying subranges, and at least k / beta
-// subranges qualify: for larger k it could only bail out (~18 us at k = 2^20).
-inline bool ft_enabled(int alpha, int beta, u64 k) { return alpha <= FT_MAX_ALPHA && k <= (u64)beta * FT_CAND; }
+// fast_tail holds <= FT_CAND qualifying subranges.  At least k / beta
+// subranges qualify, and about k on inputs without many equal keys (nearly every
+// candidate holds one key above theta), so above FT_CAND it would mostly bail
+// out (~18 us: k = 8192 at beta 2).
+#ifndef DTOPK_FT_KMAX_BETA
+#define DTOPK_FT_KMAX_BETA 0  // 1: admit k <= beta * FT_CAND (the bound for inputs with many equal keys)
+#endif
+inline bool ft_enabled(int alpha, int beta, u64 k) {
+  return alpha <= FT_MAX_ALPHA && k <= (u64)(DTOPK_FT_KMAX_BETA ? beta : 1) * FT_CAND;
+}
 
 // Filtered delegate pass (K0 sample -> K1 records -> K2 over records): where
 // K1's D + meta writes are a measurable share of the stream (alpha 6..8: 12 B

@@ -674,7 +674,13 @@ __device__ __forceinline__ void bucket_geometry(const Ctrl* c, u32& shift, u32& 
   const int bits = range ? 32 - __clz(range) : 0;  // d < 2^bits
   const int lb = 31 - __clz(want);
   shift = bits > lb ? (u32)(bits - lb) : 0u;
-  nb = (u32)min((ull)want, range ? ((ull)range >> shift) + 1ull : 1ull);
+  // range >> shift lies in [want / 2, want): one bit less of shift when that
+  // leaves the buckets above 3/4 of BK_CAP on average (k = 2^14: 5 buckets of
+  // ~3.3k keys overflowed BK_CAP and sent the sort to the LSD fallback, ~50 us;
+  // more, smaller buckets measured ~3 us slower at k = 2^20)
+  const u64 nb0 = range ? ((ull)range >> shift) + 1ull : 1ull;
+  if (shift > 0 && m > nb0 * (u64)(BK_CAP / 4 * 3) && 2ull * want <= (ull)BK_MAX) shift--;
+  nb = (u32)min((ull)BK_MAX, range ? ((ull)range >> shift) + 1ull : 1ull);
 }
 
 __device__ __forceinline__ void bucket_chunk(u64 m, u64& lo, u64& hi) {

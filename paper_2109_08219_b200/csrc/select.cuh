@@ -507,6 +507,13 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   __shared__ u32 s_rcnt[P3_REGIONS];
   const int tid = threadIdx.x;
   __shared__ DigitResult r2;
+#ifdef DTOPK_P3_PROFILE
+  unsigned long long pt[6];
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt[0]));
+#define P3_MARK(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt[i]))
+#else
+#define P3_MARK(i)
+#endif
   if (ld_volatile_u32(&ctrl->small_done)) return;  // fast_tail resolved theta and finished the call
   const DigitResult r1 = ctrl->selD.r1;
   // a small compacted bucket (small k): one CTA resolves theta from the members
@@ -516,9 +523,11 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   for (int i = tid; i < NBD3; i += 256) shist[i] = 0;
   u32 kmin, kmax;
   dbucket(r1.digit, lin != 0, kmin, kmax);
+  P3_MARK(1);
   find_digit<NBD2>(ctrl->selD.hist2, r1.rem, &r2, scratch);
   if (blockIdx.x == 0 && tid == 0) ctrl->selD.r2 = r2;
   const u32 b2 = r2.digit;
+  P3_MARK(2);
   if (small) {
     // region counts -> exclusive prefix (thread t owns regions t*P3_RPT ..), then
     // a flat loop over the members: member i lives in the region whose prefix
@@ -561,7 +570,14 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
         if (x[u] != 0xffffffffu && (x[u] >> DSH3) == b2) atomicAdd(&shist[x[u] & ((1u << DSH3) - 1u)], 1u);
     }
     __syncthreads();
+    P3_MARK(3);
     k2_resolve_theta(ctrl, kmin, r1, r2, nregions, sup_cnt, sup_off, &r3, scratch, nD, shist);
+    P3_MARK(4);
+#ifdef DTOPK_P3_PROFILE
+    if (tid == 0)
+      printf("p3 small: members=%u regions=%u | r1 %llu find2 %llu loop %llu resolve %llu ns\n", total, nregions,
+             pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3]);
+#endif
     return;
   }
   if (r1.cnt * 4 > nD) {
