@@ -410,7 +410,9 @@ __device__ void find_digit(const ull* hist, ull k_rem, DigitResult* out, ull* sc
 }
 
 // find_digit over a shared-memory u32 histogram (same contract as find_digit).
-template <int NB>
+// PAD: bin b is stored at b + b / 32 (thread t's PER = 32 bins then start 33 t
+// words apart: conflict-free, instead of a 32-way conflict on every read).
+template <int NB, bool PAD = false>
 __device__ void find_digit_sm(const u32* sh, ull k_rem, DigitResult* out, ull* scratch) {
   constexpr int PER = NB / 256;
   const int t = threadIdx.x;
@@ -418,7 +420,8 @@ __device__ void find_digit_sm(const u32* sh, ull k_rem, DigitResult* out, ull* s
   ull sum = 0;
 #pragma unroll
   for (int i = 0; i < PER; i++) {
-    loc[i] = sh[NB - 1 - (t * PER + i)];
+    const u32 b = (u32)(NB - 1 - (t * PER + i));
+    loc[i] = sh[PAD ? b + (b >> 5) : b];
     sum += loc[i];
   }
   if (t == 0) out->valid = 0;

@@ -62,23 +62,29 @@ struct K2Args {
 #endif
 constexpr int K2_SEG_PER = 24;  // superset segments per thread in the prefix (8 warps x <= 768 K2 CTAs)
 
-// Exclusive prefix of the superset segment counts -> sup_off, sup_total (one CTA).
-__device__ void k2_superset_prefix(Ctrl* ctrl, u32 nregions, const u32* __restrict__ sup_cnt,
-                                   u32* __restrict__ sup_off, ull* scratch) {
+// The superset segment counts of thread t: segments [t * K2_SEG_PER, +K2_SEG_PER),
+// read as uint4 (sup_cnt is padded to 256 * K2_SEG_PER; nseg = 8 * nregions <=
+// 8 * 768 = 256 * K2_SEG_PER).
+__device__ __forceinline__ void k2_sup_load(const u32* __restrict__ sup_cnt, uint4 (&x)[K2_SEG_PER / 4]) {
+  const uint4* c4 = reinterpret_cast<const uint4*>(sup_cnt) + threadIdx.x * (K2_SEG_PER / 4);
+#pragma unroll
+  for (int q = 0; q < K2_SEG_PER / 4; q++) x[q] = __ldcg(&c4[q]);
+}
+
+// Exclusive prefix of the superset segment counts (loaded by k2_sup_load) ->
+// sup_off, sup_total (one CTA).
+__device__ __forceinline__ void k2_superset_prefix_regs(Ctrl* ctrl, u32 nregions, const uint4 (&x)[K2_SEG_PER / 4],
+                                                        u32* __restrict__ sup_off, ull* scratch) {
   const int tid = threadIdx.x;
-  // nseg = 8 * nregions <= 8 * 768 = 256 * K2_SEG_PER: thread t owns segments
-  // [t * K2_SEG_PER, +K2_SEG_PER), read as uint4 (sup_cnt is padded to 256 * K2_SEG_PER)
   const u32 nseg = nregions * 8;
   u32 c[K2_SEG_PER];
   u32 sum = 0;
-  const uint4* c4 = reinterpret_cast<const uint4*>(sup_cnt) + tid * (K2_SEG_PER / 4);
 #pragma unroll
   for (int q = 0; q < K2_SEG_PER / 4; q++) {
-    const uint4 x = __ldcg(&c4[q]);
-    c[4 * q] = x.x;
-    c[4 * q + 1] = x.y;
-    c[4 * q + 2] = x.z;
-    c[4 * q + 3] = x.w;
+    c[4 * q] = x[q].x;
+    c[4 * q + 1] = x[q].y;
+    c[4 * q + 2] = x[q].z;
+    c[4 * q + 3] = x[q].w;
   }
 #pragma unroll
   for (int q = 0; q < K2_SEG_PER; q++) {
@@ -100,18 +106,23 @@ __device__ void k2_superset_prefix(Ctrl* ctrl, u32 nregions, const u32* __restri
   }
 }
 
-// Resolve theta from the digit-3 histogram (ctrl->selD.hist3, or the CTA's
-// shared-memory histogram when `sh3` is set) and publish the exclusive prefix
-// of the superset segment counts.  One CTA (256 threads).
-__device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, const DigitResult& r2, u32 nregions,
-                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off, DigitResult* r3,
-                                 ull* scratch, u64 nD, const u32* sh3 = nullptr) {
-  const int tid = threadIdx.x;
+__device__ void k2_superset_prefix(Ctrl* ctrl, u32 nregions, const u32* __restrict__ sup_cnt,
+                                   u32* __restrict__ sup_off, ull* scratch) {
+  uint4 x[K2_SEG_PER / 4];
+  k2_sup_load(sup_cnt, x);
+  k2_superset_prefix_regs(ctrl, nregions, x, sup_off, scratch);
+}
+
+// theta = kmin + digit 2 + digit 3 from the digit-3 histogram (ctrl->selD.hist3,
+// or pass 3's padded shared-memory histogram when `sh3` is set).  One CTA.
+__device__ __forceinline__ void k2_theta_from_hist3(Ctrl* ctrl, u32 kmin, const DigitResult& r1,
+                                                    const DigitResult& r2, DigitResult* r3, ull* scratch,
+                                                    const u32* sh3) {
   if (sh3)
-    find_digit_sm<NBD3>(sh3, r2.rem, r3, scratch);
+    find_digit_sm<NBD3, true>(sh3, r2.rem, r3, scratch);
   else
     find_digit<NBD3>(ctrl->selD.hist3, r2.rem, r3, scratch);
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     const u32 kth = kmin + (r2.digit << DSH3) + r3->digit;
     ctrl->selD.r3 = *r3;
     ctrl->selD.kth = kth;
@@ -119,6 +130,14 @@ __device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, co
     ctrl->res.theta_slot = (int64_t)kth;
     ctrl->res.delegate_bucket = r1.cnt;
   }
+}
+
+// Resolve theta and publish the exclusive prefix of the superset segment
+// counts.  One CTA (256 threads).
+__device__ void k2_resolve_theta(Ctrl* ctrl, u32 kmin, const DigitResult& r1, const DigitResult& r2, u32 nregions,
+                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off, DigitResult* r3,
+                                 ull* scratch, u64 nD, const u32* sh3 = nullptr) {
+  k2_theta_from_hist3(ctrl, kmin, r1, r2, r3, scratch, sh3);
   if (sup_cnt == nullptr || r1.cnt * 4 > nD) return;  // deferred: K2b builds and offsets the superset
   k2_superset_prefix(ctrl, nregions, sup_cnt, sup_off, scratch);
 }
@@ -380,6 +399,11 @@ __global__ void __launch_bounds__(256, DTOPK_K2_MINB) k2_scan_delegates(K2Args a
 constexpr int P3_SMALL = DTOPK_P3_SMALL;  // bucket members resolved by one CTA
 constexpr int P3_RPT = 3;        // regions per thread in that CTA's prefix
 constexpr int P3_REGIONS = 256 * P3_RPT;
+constexpr int P3_LPT = 8;           // member loads in flight per thread (8 measured faster than 24)
+constexpr int P3_THREAD_MAX = 64;   // larger regions are loaded by whole warps
+// padded shared histogram index: thread t's 32 consecutive bins start 33 t
+// words apart, so find_digit_sm's per-thread block reads hit 32 banks
+__device__ __forceinline__ u32 p3_pad(u32 b) { return b + (b >> 5); }
 
 // Pass 3 of kth(D) over the compacted bucket regions;
 // the last CTA resolves theta and the superset record offsets.
@@ -494,17 +518,18 @@ __device__ __forceinline__ void p3_set_theta(Ctrl* ctrl, u32 kth, const DigitRes
   ctrl->res.delegate_bucket = r1.cnt;
 }
 
-__global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
+__global__ void __launch_bounds__(256, 1) k2_pass3(Ctrl* ctrl, const u32* __restrict__ selbuf,
                                                 const u32* __restrict__ region_cnt, u32 nregions, u64 R,
                                                 const u32* __restrict__ sup_cnt, u32* __restrict__ sup_off,
                                                 const u32* __restrict__ D, u64 nD, int lin) {
   pdl_trigger();
   pdl_wait();
-  __shared__ u32 shist[NBD3];
+  __shared__ u32 shist[NBD3 + NBD3 / 32];  // small path: bin b at p3_pad(b) (conflict-free digit scan)
   __shared__ DigitResult r3;
   __shared__ ull scratch[8];
   __shared__ int am_last;
-  __shared__ u32 s_rcnt[P3_REGIONS];
+  __shared__ u32 s_big[P3_REGIONS];
+  __shared__ u32 s_nbig;
   const int tid = threadIdx.x;
   __shared__ DigitResult r2;
 #ifdef DTOPK_P3_PROFILE
@@ -514,13 +539,27 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
 #else
 #define P3_MARK(i)
 #endif
+  const DigitResult r1 = ctrl->selD.r1;  // read before the flag: one round trip for both
   if (ld_volatile_u32(&ctrl->small_done)) return;  // fast_tail resolved theta and finished the call
-  const DigitResult r1 = ctrl->selD.r1;
   // a small compacted bucket (small k): one CTA resolves theta from the members
   // directly, without the grid-wide histogram flush and last-CTA hand-off
   const bool small = r1.cnt * 4 <= nD && r1.cnt <= (ull)P3_SMALL && nregions <= (u32)P3_REGIONS;
   if (small && blockIdx.x != 0) return;
-  for (int i = tid; i < NBD3; i += 256) shist[i] = 0;
+  // small path: the region counts and the superset segment counts are loaded
+  // before the digit-2 scan, so their round trips overlap it
+  u32 c[P3_RPT];
+  uint4 supx[K2_SEG_PER / 4];
+  const bool sup_now = small && sup_cnt != nullptr;  // (r1.cnt * 4 <= nD holds on the small path)
+  if (small) {
+#pragma unroll
+    for (int q = 0; q < P3_RPT; q++) {
+      const u32 g = (u32)tid * P3_RPT + q;
+      c[q] = g < nregions ? __ldcg(region_cnt + g) : 0u;
+    }
+    if (sup_now) k2_sup_load(sup_cnt, supx);
+  }
+  for (int i = tid; i < NBD3 + NBD3 / 32; i += 256) shist[i] = 0;
+  if (tid == 0) s_nbig = 0;
   u32 kmin, kmax;
   dbucket(r1.digit, lin != 0, kmin, kmax);
   P3_MARK(1);
@@ -529,53 +568,68 @@ __global__ void __launch_bounds__(256) k2_pass3(Ctrl* ctrl, const u32* __restric
   const u32 b2 = r2.digit;
   P3_MARK(2);
   if (small) {
-    // region counts -> exclusive prefix (thread t owns regions t*P3_RPT ..), then
-    // a flat loop over the members: member i lives in the region whose prefix
-    // interval holds i (binary search in shared memory)
-    u32 c[P3_RPT], sum = 0;
+    // thread t owns regions t*P3_RPT .. and loads their members itself, P3_LPT
+    // loads in flight (a region holds ~members / regions keys: ~7 at k = 2^20);
+    // a region above P3_THREAD_MAX members goes to a list that whole warps load.
+    // (A flat member loop with a binary search per member over the region
+    // prefix took 17 us for 4k members at k = 2^20.)
 #pragma unroll
     for (int q = 0; q < P3_RPT; q++) {
       const u32 g = (u32)tid * P3_RPT + q;
-      c[q] = g < nregions ? region_cnt[g] : 0u;
-      sum += c[q];
+      if (c[q] > (u32)P3_THREAD_MAX) {
+        s_big[atomicAdd(&s_nbig, 1u)] = g;
+        c[q] = 0;
+      }
     }
-    const u32 incl = block_incl_scan_256<u32>(sum, reinterpret_cast<u32*>(scratch));
-    u32 run = incl - sum;
+    u32 tot = 0;
 #pragma unroll
-    for (int q = 0; q < P3_RPT; q++) {
-      s_rcnt[tid * P3_RPT + q] = run;  // exclusive prefix of region tid*P3_RPT+q
-      run += c[q];
-    }
-    __shared__ u32 s_total;
-    if (tid == 255) s_total = incl;
-    __syncthreads();
-    const u32 total = s_total;
-    for (u32 i0 = 0; i0 < total; i0 += 256 * 4) {
-      u32 x[4];
+    for (int q = 0; q < P3_RPT; q++) tot += c[q];
+    for (u32 j0 = 0; j0 < tot; j0 += P3_LPT) {
+      u32 x[P3_LPT];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const u32 i = i0 + u * 256 + tid;
+      for (int u = 0; u < P3_LPT; u++) {
+        u32 j = j0 + u;
         x[u] = 0xffffffffu;
-        if (i < total) {
-          u32 lo = 0, hi = nregions;  // last region with prefix <= i
-          while (hi - lo > 1) {
-            const u32 mid = (lo + hi) >> 1;
-            if (s_rcnt[mid] <= i) lo = mid; else hi = mid;
-          }
-          x[u] = selbuf[(u64)lo * R + (i - s_rcnt[lo])] - kmin;
+        if (j < tot) {
+          int q = 0;
+#pragma unroll
+          for (int r = 0; r < P3_RPT - 1; r++)
+            if (q == r && j >= c[r]) {
+              j -= c[r];
+              q = r + 1;
+            }
+          x[u] = selbuf[(u64)((u32)tid * P3_RPT + q) * R + j] - kmin;
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; u++)
-        if (x[u] != 0xffffffffu && (x[u] >> DSH3) == b2) atomicAdd(&shist[x[u] & ((1u << DSH3) - 1u)], 1u);
+      for (int u = 0; u < P3_LPT; u++)
+        if (x[u] != 0xffffffffu && (x[u] >> DSH3) == b2) atomicAdd(&shist[p3_pad(x[u] & ((1u << DSH3) - 1u))], 1u);
+    }
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5;
+    for (u32 b = warp; b < s_nbig; b += 8) {
+      const u32 g = s_big[b], cnt = region_cnt[g];
+      const u32* reg = selbuf + (u64)g * R;
+      for (u32 i0 = 0; i0 < cnt; i0 += 32 * P3_LPT) {
+        u32 x[P3_LPT];
+#pragma unroll
+        for (int u = 0; u < P3_LPT; u++) {
+          const u32 i = i0 + u * 32 + lane;
+          x[u] = i < cnt ? reg[i] - kmin : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < P3_LPT; u++)
+          if (x[u] != 0xffffffffu && (x[u] >> DSH3) == b2) atomicAdd(&shist[p3_pad(x[u] & ((1u << DSH3) - 1u))], 1u);
+      }
     }
     __syncthreads();
     P3_MARK(3);
-    k2_resolve_theta(ctrl, kmin, r1, r2, nregions, sup_cnt, sup_off, &r3, scratch, nD, shist);
+    k2_theta_from_hist3(ctrl, kmin, r1, r2, &r3, scratch, shist);
+    if (sup_now) k2_superset_prefix_regs(ctrl, nregions, supx, sup_off, scratch);
     P3_MARK(4);
 #ifdef DTOPK_P3_PROFILE
     if (tid == 0)
-      printf("p3 small: members=%u regions=%u | r1 %llu find2 %llu loop %llu resolve %llu ns\n", total, nregions,
+      printf("p3 small: members=%llu regions=%u | r1 %llu find2 %llu loop %llu resolve %llu ns\n", r1.cnt, nregions,
              pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3]);
 #endif
     return;

@@ -9,6 +9,7 @@ v=sys.argv[1]
 try:
     d=json.load(open(f"gpurun_out/ab/{v}.json"))
     print(v, "ms", round(d["ms_per_step"],4), "k1_ms", round(d["roofline"]["kernel_ms"],4), "sweep", [(s["k"], s["ms"], round(s["stage_ms"]["Delegate"],4)) for s in d["k_sweep"]])
+    print("   tail (ms - eager K1)", [(s["k"], round(s["ms"] - s["stage_ms"]["Delegate"], 4)) for s in d["k_sweep"]])
 except Exception as e:
     print(v, "failed", e)
 PY
