@@ -106,6 +106,24 @@ def test_dr_topk_adversarial(dist, k, oracle_mod, cuda):
     check_topk(v, k, oracle_mod)
 
 
+@pytest.mark.parametrize("dist,k", [("uniform", 4097), ("uniform", 6000), ("uniform", 8192), ("ascending", 6000),
+                                    ("descending", 6000), ("nd_u32", 7000), ("clustered", 6000)])
+def test_pass3_one_cta_path(dist, k, oracle_mod, cuda):
+    """K2 pass 3's one-CTA path (theta bucket <= 8192 members, select.cuh
+    k2_pass3): thread-owned regions, and the warp list for regions above 64
+    members ("clustered": every key above 2^31 sits in one block of 20000, so
+    the bucket members fill one or two K2 regions)."""
+    n = 1 << 22
+    if dist == "clustered":
+        v = data.generate("uniform", n, seed=5, device=cuda)
+        vi = v.view(torch.int32)
+        vi &= 0x7FFFFFFF
+        vi[n // 2: n // 2 + 20000] |= torch.tensor(-0x80000000, dtype=torch.int32, device=cuda)
+    else:
+        v = data.generate(dist, n, seed=5, device=cuda)
+    check_topk(v, k, oracle_mod)
+
+
 @pytest.mark.parametrize("k", [20_000, 300_000])
 @pytest.mark.parametrize("case", ["uniform", "normal_f32_smallest", "skewed_bucket", "two_values"])
 def test_big_answer_sorts(case, k, oracle_mod, cuda):

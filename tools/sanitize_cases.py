@@ -42,6 +42,7 @@ n = 1 << 20
 u = data.generate("uniform", n, seed=1, device=dev)
 check("fast_tail k=64", u, 64)
 check("general chain k=4096", u, 4096)
+check("general chain k=6000 (pass 3 one-CTA path)", u, 6000)
 check("large pool k=2^17 (select+bucket sort)", u, 1 << 17)
 check("direct path", u[:5000].clone(), 4999)
 check("beta 3", u, 1000, beta=3)
