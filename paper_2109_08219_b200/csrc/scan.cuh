@@ -650,6 +650,10 @@ constexpr int BK_TARGET = DTOPK_BK_TARGET;    // elements per bucket aimed for
 constexpr int BK_CAP = 4096;      // largest bucket bucket_sort takes (16 per thread)
 constexpr int BK_SUB_BITS = DTOPK_BK_SUB_BITS;  // sub-bins of the in-bucket counting sort
 constexpr int BK_SUB = 1 << BK_SUB_BITS;
+#ifndef DTOPK_BK_LPT
+#define DTOPK_BK_LPT 4
+#endif
+constexpr int BK_LPT = DTOPK_BK_LPT;  // key loads in flight per thread in bucket_count / bucket_scatter
 
 struct BucketBufs {
   u32* total;   // [BK_MAX] bucket sizes (zeroed per run)
@@ -701,12 +705,12 @@ __global__ void __launch_bounds__(512) bucket_count(Ctrl* ctrl, SortBufs b, Buck
   u64 lo, end;
   bucket_chunk(ctrl->sort_m, lo, end);
   u64 i = lo + threadIdx.x;
-  for (; i + 3 * 512 < end; i += 4 * 512) {
-    u32 d[4];
+  for (; i + (BK_LPT - 1) * 512 < end; i += BK_LPT * 512) {
+    u32 d[BK_LPT];
 #pragma unroll
-    for (int q = 0; q < 4; q++) d[q] = hi - keys[i + q * 512];
+    for (int q = 0; q < BK_LPT; q++) d[q] = hi - keys[i + q * 512];
 #pragma unroll
-    for (int q = 0; q < 4; q++) atomicAdd(&h[d[q] >> shift], 1u);
+    for (int q = 0; q < BK_LPT; q++) atomicAdd(&h[d[q] >> shift], 1u);
   }
   for (; i < end; i += 512) atomicAdd(&h[(hi - keys[i]) >> shift], 1u);
   __syncthreads();
@@ -779,12 +783,12 @@ __global__ void __launch_bounds__(512) bucket_scatter(Ctrl* ctrl, SortBufs b, Bu
   u64 lo, end;
   bucket_chunk(ctrl->sort_m, lo, end);
   u64 i = lo + threadIdx.x;
-  for (; i + 3 * 512 < end; i += 4 * 512) {
-    u32 d[4];
+  for (; i + (BK_LPT - 1) * 512 < end; i += BK_LPT * 512) {
+    u32 d[BK_LPT];
 #pragma unroll
-    for (int q = 0; q < 4; q++) d[q] = hi - keys[i + q * 512];
+    for (int q = 0; q < BK_LPT; q++) d[q] = hi - keys[i + q * 512];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
+    for (int q = 0; q < BK_LPT; q++) {
       const u32 pos = atomicAdd(&cur[d[q] >> shift], 1u);
       bb.comp[pos] = ((unsigned long long)d[q] << 32) | (u32)(i + q * 512);
     }
