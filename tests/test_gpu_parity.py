@@ -353,6 +353,27 @@ def test_graph_plan_replay_matches_eager(k, oracle_mod, cuda):
         v.view(torch.int32)[::97] += 1  # new data, same buffer: the plan re-reads it
 
 
+@pytest.mark.parametrize("k", [5000, 70000])
+def test_graph_plan_switches_tie_heavy(k, oracle_mod, cuda):
+    """One graph plan replayed over one buffer whose contents switch between
+    uniform, tie-heavy and sorted keys: every device-decided path (K2c / K2b on a
+    large theta bucket, the pool floor, the graph's conditional tails) follows
+    the contents of each launch (api.cu run_finish)."""
+    from paper_2109_08219_b200 import _native
+    from paper_2109_08219_b200.pipeline import DrTopK
+
+    n = 1 << 22
+    buf = torch.empty(n, dtype=torch.uint32, device=cuda)
+    p = DrTopK(n, dtopk.PipelineConfig(k=k), _native.DTYPE_U32, torch.uint32, cuda, use_graph=True)
+    for dist in ["uniform", "few_distinct", "all_equal", "uniform", "few_distinct", "ascending"]:
+        buf.copy_(data.generate(dist, n, seed=3, device=cuda))
+        p.launch(buf)
+        torch.cuda.synchronize()
+        ek, ei = oracle_mod.topk_with_indices(buf.cpu().numpy(), k)
+        np.testing.assert_array_equal(p.indices.cpu().numpy(), ei)
+        np.testing.assert_array_equal(p.values.cpu().numpy(), ek)
+
+
 def test_sharded_two_ranks_on_one_gpu(cuda):
     """The multi-rank product path (ShardedTopK and sharded_topk) against the
     oracle with 2 ranks; gloo lets both ranks share this box's single GPU."""
