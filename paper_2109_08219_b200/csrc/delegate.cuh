@@ -590,6 +590,9 @@ __global__ void __launch_bounds__(k1_threads<B>(), K1_CPS) k1_delegates(K1Args a
 // stays off when the chosen buckets hold more than a quarter of the sample
 // (tie-heavy / narrow-range input: the floor would keep most subranges).
 // Reads 1/K0_GROUP of the input.
+#ifndef DTOPK_K0_R
+#define DTOPK_K0_R 1.25  // sample rank of the floor, in units of k (theta is at rank k of D)
+#endif
 constexpr int K0_GROUP = 512;
 constexpr int K0_REGIONS = 64;
 __host__ __device__ __forceinline__ u64 k0_run(u64 nch_full) {
@@ -668,7 +671,7 @@ __global__ void __launch_bounds__(256) k0_sample(const u32* __restrict__ keys, i
   __threadfence();
   const ull ns = K0_REGIONS * k0_run(nch_full) * (2048ull >> alpha) * (u64)B;  // sampled delegates
   const double f = (double)ns / (double)nD;
-  const double R = (double)k * 1.25 + 64.0;
+  const double R = (double)k * DTOPK_K0_R + 64.0;
   const ull rs = (ull)ceil(R * f + 4.0 * sqrt(R * f) + 8.0);
   find_digit<NBD1>(ctrl->samp_hist, rs, &res, scratch);
   if (tid == 0) {
