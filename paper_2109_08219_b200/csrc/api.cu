@@ -30,7 +30,7 @@
 #include "stage.cuh"
 
 #ifndef DTOPK_K2_CPS
-#define DTOPK_K2_CPS 4  // K2 CTAs (regions) per SM
+#define DTOPK_K2_CPS 3  // K2 CTAs (regions) per SM (A/B: 3 beats 2, 4, 5 at k = 2^14..2^20)
 #endif
 
 using namespace dtopk;
