@@ -58,7 +58,7 @@ struct K2Args {
 };
 
 #ifndef DTOPK_K2_MINB
-#define DTOPK_K2_MINB 4  // K2 min CTAs per SM: caps registers so all DTOPK_K2_CPS regions of an SM are resident (single wave)
+#define DTOPK_K2_MINB 3  // K2 min CTAs per SM = DTOPK_K2_CPS: all regions of an SM resident (single wave), 80 registers (4: 64, ~6 us slower)
 #endif
 constexpr int K2_SEG_PER = 24;  // superset segments per thread in the prefix (8 warps x <= 768 K2 CTAs)
 
